@@ -1,0 +1,307 @@
+"""Plain fp64 CPU oracle of MoA heterogeneous sliding-window attention.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+module.  It shares no code with the CUDA path (``paper_2406_14909_b200``) and
+imports nothing from it.
+
+Every function below is the plain definition from the paper, written out in
+float64 with Python/numpy, no blocking, no fusion, no reordering:
+
+* Eq. 1 (``eq:attention_compute``):
+  ``S = Q K^T,  A = softmax(S + M),  O = A V``.
+* The mask ``M`` of one head is the MoA sliding-window mask with attention
+  sinks ("the initial few tokens (64 tokens for MoA) are not
+  masked"; "Prefix ... remain visible to all attention
+  heads"; PAPER.md:625-637 visual-element table).
+* The span of a head comes from the elastic rule, Eq. 2 (PAPER.md:181,
+  ``eq:search_space``) ``S_h = alpha_h + beta_h * N``, clipped to [0, N]
+  (PAPER.md:692).  The span includes the sinks ("The attention
+  span equals the sliding-window span plus the number of initially unmasked
+  tokens").
+* Decode keeps a static per-head cache of sinks + the most recent window and
+  "replace[s] the old KV-Cache that exceeds the span with the latest"
+  (``sec:appendix/effiency_experiment_setup``).
+
+Readings of silent / ambiguous passages are the ones listed in DESIGN.md
+section "Readings".  The ones this file relies on:
+
+* c2: windows are passed separately from the sink count; the window of a
+  rule is ``W = max(0, clip(S, 0, N) - s)``.
+* c3: the window counts the query itself: key j is in the window of query i
+  iff ``i - j < W``.
+* c6: ``alpha + beta*N`` is rounded up (ceil) before clipping.
+* c7: ``W = 0`` is allowed only with ``s >= 1``.
+* c8: the softmax scale tau is an explicit argument (Eq. 1 has none).
+* c9: decode windows are frozen at their prefill value.
+* c10: GQA: q-head h reads kv-group ``h // G``; the cache of a group holds
+  ``W_g = max_{h in g} W_h`` recent rows; every q-head masks to its own W_h.
+* c13: ring slot of position p: ``p`` if ``p < s`` else
+  ``s + (p - s) mod W_g``.
+
+Parity pins for every function are in ``tests/test_oracle_pins.py``; none of
+them is "parity unpinned".
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+__all__ = [
+    "span_of",
+    "window_of",
+    "group_windows",
+    "visible",
+    "visible_keys",
+    "attend",
+    "prefill",
+    "prefill_rows",
+    "prefill_dense_mask",
+    "decode",
+    "slot_of",
+    "resident_positions",
+    "cache_image",
+    "density",
+    "visible_pairs",
+]
+
+
+# ---------------------------------------------------------------------------
+# Elastic rule -> span -> window (Eq. 2; clip PAPER.md:692)
+# ---------------------------------------------------------------------------
+
+def span_of(alpha: float, beta: float, N: int) -> int:
+    """Attention span of one head at input length N (Eq. 2).
+
+    ``S = alpha + beta * N`` (alpha = base span in tokens, beta = expansion
+    rate; reading c1 -- App. A's ``alpha x N + beta`` at PAPER.md:609 has the
+    roles swapped, and the search ranges at PAPER.md:692, alpha in
+    [-2048, 8192] and beta in [0, 1], only make sense this way round).
+    Rounded up (reading c6) and "clipped to the range between 0 and the
+    current input length".
+    """
+    s = math.ceil(alpha + beta * N)
+    return int(min(max(s, 0), N))
+
+
+def window_of(span: int, n_sink: int) -> int:
+    """Sliding-window length of a head whose span is ``span`` (reading c2).
+
+    "The attention span equals the sliding-window span plus the number of
+    initially unmasked tokens", so window = span - sinks,
+    floored at 0 (a sink-only head).
+    """
+    return int(max(0, span - n_sink))
+
+
+def group_windows(windows_q, group_size: int) -> np.ndarray:
+    """Cache capacity of each kv-group, ``W_g = max_{h in g} W_h`` (c10)."""
+    w = np.asarray(windows_q, dtype=np.int64)
+    assert w.size % group_size == 0
+    return w.reshape(-1, group_size).max(axis=1)
+
+
+# ---------------------------------------------------------------------------
+# The mask predicate and Eq. 1
+# ---------------------------------------------------------------------------
+
+def visible(i: int, j: int, W: int, s: int) -> bool:
+    """True iff key j is visible to query i: causal, and a sink or in the
+    window.  ``V(h,i) = { j : 0 <= j <= i and (j < s or i - j < W) }``."""
+    return 0 <= j <= i and (j < s or i - j < W)
+
+
+def visible_keys(i: int, W: int, s: int) -> np.ndarray:
+    """Sorted list of visible key positions of query i (brute-force
+    enumeration of the predicate, O(i))."""
+    return np.array([j for j in range(i + 1) if visible(i, j, W, s)],
+                    dtype=np.int64)
+
+
+def attend(q: np.ndarray, Kj: np.ndarray, Vj: np.ndarray, tau: float):
+    """One row of Eq. 1 restricted to the visible keys.
+
+    ``z_j = tau * q . k_j`` ; ``a = softmax(z)`` ; ``o = sum_j a_j v_j``.
+    Also returns ``lse = log sum_j exp(z_j)``.  fp64 throughout.
+    """
+    if Kj.shape[0] == 0:
+        raise ValueError("empty softmax row (W = 0 and s = 0 is invalid, c7)")
+    z = tau * (Kj.astype(np.float64) @ q.astype(np.float64))
+    m = z.max()
+    w = np.exp(z - m)
+    l = w.sum()
+    o = (w @ Vj.astype(np.float64)) / l
+    return o, m + math.log(l)
+
+
+def _check_shapes(Q, K, V, windows_q):
+    B, N, Hq, d = Q.shape
+    assert K.shape[0] == B and K.shape[1] == N and K.shape[3] == d
+    assert V.shape == K.shape
+    Hkv = K.shape[2]
+    assert Hq % Hkv == 0
+    assert len(windows_q) == Hq
+    return B, N, Hq, Hkv, d, Hq // Hkv
+
+
+def prefill_rows(Q, K, V, windows_q, n_sink: int, tau: float, rows):
+    """Eq. 1 for a list of sampled outputs ``rows = [(b, h, i), ...]``.
+
+    Returns (O [len(rows), d], LSE [len(rows)]) in fp64.  Each row gathers
+    its visible set V(h,i) by enumerating the predicate and attends over it.
+    """
+    B, N, Hq, Hkv, d, G = _check_shapes(Q, K, V, windows_q)
+    O = np.zeros((len(rows), d), dtype=np.float64)
+    L = np.zeros(len(rows), dtype=np.float64)
+    for r, (b, h, i) in enumerate(rows):
+        g = h // G
+        J = visible_keys(int(i), int(windows_q[h]), n_sink)
+        O[r], L[r] = attend(Q[b, i, h], K[b, J, g], V[b, J, g], tau)
+    return O, L
+
+
+def prefill(Q, K, V, windows_q, n_sink: int, tau: float):
+    """Causal prefill with the per-head MoA mask (Eq. 1 + PAPER.md:178).
+
+    Q: [B, N, Hq, d]; K, V: [B, N, Hkv, d] (any float dtype, upcast to fp64).
+    windows_q: window W_h of every q-head.  Returns O [B, N, Hq, d] and
+    LSE [B, Hq, N], both fp64.
+    """
+    B, N, Hq, Hkv, d, G = _check_shapes(Q, K, V, windows_q)
+    rows = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(N)]
+    o, l = prefill_rows(Q, K, V, windows_q, n_sink, tau, rows)
+    O = o.reshape(B, Hq, N, d).transpose(0, 2, 1, 3).copy()
+    LSE = l.reshape(B, Hq, N)
+    return O, LSE
+
+
+def prefill_dense_mask(Q, K, V, windows_q, n_sink: int, tau: float):
+    """Second, brute-force formulation of the same prefill: a dense N x N
+    additive mask M with a finite -1e30 sentinel for masked cells
+    (SPEC.md:69 design decision), A = softmax(S + M) by rows, masked
+    probabilities snapped to exact 0, O = A V (Eq. 1 verbatim).
+    Meant for N <= 64."""
+    B, N, Hq, Hkv, d, G = _check_shapes(Q, K, V, windows_q)
+    O = np.zeros((B, N, Hq, d), dtype=np.float64)
+    LSE = np.zeros((B, Hq, N), dtype=np.float64)
+    for b in range(B):
+        for h in range(Hq):
+            g = h // G
+            M = np.full((N, N), -1e30)
+            for i in range(N):
+                for j in range(N):
+                    if visible(i, j, int(windows_q[h]), n_sink):
+                        M[i, j] = 0.0
+            S = tau * (Q[b, :, h].astype(np.float64) @ K[b, :, g].astype(np.float64).T)
+            X = S + M
+            mx = X.max(axis=1, keepdims=True)
+            E = np.exp(X - mx)
+            E[M != 0.0] = 0.0
+            A = E / E.sum(axis=1, keepdims=True)
+            O[b, :, h] = A @ V[b, :, g].astype(np.float64)
+            LSE[b, h] = mx[:, 0] + np.log(E.sum(axis=1))
+    return O, LSE
+
+
+# ---------------------------------------------------------------------------
+# Decode: one new query at absolute position p
+# ---------------------------------------------------------------------------
+
+def decode(q, K_hist, V_hist, p: int, windows_q, n_sink: int, tau: float):
+    """Decode step at position p, computed from the FULL history.
+
+    q: [B, Hq, d]; K_hist, V_hist: [B, >= p+1, Hkv, d] hold every token's K/V
+    since position 0 (never the ring).  Windows are frozen at their prefill
+    value (reading c9), so this is row i = p of Eq. 1 with the same mask.
+    Returns O [B, Hq, d], LSE [B, Hq].
+    """
+    B, Hq, d = q.shape
+    Hkv = K_hist.shape[2]
+    G = Hq // Hkv
+    O = np.zeros((B, Hq, d), dtype=np.float64)
+    L = np.zeros((B, Hq), dtype=np.float64)
+    for b in range(B):
+        for h in range(Hq):
+            g = h // G
+            J = visible_keys(p, int(windows_q[h]), n_sink)
+            O[b, h], L[b, h] = attend(q[b, h], K_hist[b, J, g], V_hist[b, J, g], tau)
+    return O, L
+
+
+# ---------------------------------------------------------------------------
+# The compact cache image (readings c10, c13)
+# ---------------------------------------------------------------------------
+
+def slot_of(pos: int, n_sink: int, W_g: int):
+    """Cache row of absolute position ``pos`` in a group's region of
+    ``n_sink + W_g`` rows (reading c13); None if the group stores no ring."""
+    if pos < n_sink:
+        return pos
+    if W_g == 0:
+        return None
+    return n_sink + (pos - n_sink) % W_g
+
+
+def resident_positions(p: int, n_sink: int, W_g: int):
+    """Positions a group's cache holds after position p was written: the
+    sinks {0..min(s, p+1)-1} and the most recent W_g non-sink positions
+    {max(s, p-W_g+1)..p} ("replace the old KV-Cache that exceeds the span
+    with the latest")."""
+    sinks = list(range(min(n_sink, p + 1)))
+    recent = list(range(max(n_sink, p - W_g + 1), p + 1))
+    return sinks + recent
+
+
+def cache_image(K_hist, V_hist, p: int, windows_g, n_sink: int):
+    """Expected cache contents after position p was written.
+
+    Returns, per (b, g), a tuple (K_img, V_img, valid) with K_img, V_img
+    [n_sink + W_g, d] copies of the history rows (same dtype as the inputs,
+    so a bitwise comparison is possible) and ``valid`` a bool mask of the
+    rows that hold a position; invalid rows are excluded from comparison.
+    """
+    B = K_hist.shape[0]
+    Hkv = K_hist.shape[2]
+    d = K_hist.shape[3]
+    out = {}
+    for b in range(B):
+        for g in range(Hkv):
+            Wg = int(windows_g[g])
+            Kimg = np.zeros((n_sink + Wg, d), dtype=K_hist.dtype)
+            Vimg = np.zeros((n_sink + Wg, d), dtype=V_hist.dtype)
+            valid = np.zeros(n_sink + Wg, dtype=bool)
+            for pos in resident_positions(p, n_sink, Wg):
+                r = slot_of(pos, n_sink, Wg)
+                Kimg[r] = K_hist[b, pos, g]
+                Vimg[r] = V_hist[b, pos, g]
+                valid[r] = True
+            out[(b, g)] = (Kimg, Vimg, valid)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Accounting (PAPER.md:375 density; Eq. 1 work)
+# ---------------------------------------------------------------------------
+
+def density(windows, n_sink: int, N: int) -> float:
+    """"the ratio of the average in-memory KV-Cache length to sequence
+    length during decoding": mean over heads of
+    min(N, s + W_h) / N (reading c11)."""
+    w = np.asarray(windows, dtype=np.int64)
+    return float(np.mean(np.minimum(N, n_sink + w)) / N)
+
+
+def visible_pairs(N: int, W: int, s: int) -> int:
+    """Number of (query, key) pairs one head attends to in prefill, by
+    enumerating the predicate row by row (sum over i of |V(h,i)|)."""
+    total = 0
+    for i in range(N):
+        n_sink = min(s, i + 1)
+        lo = max(0, i - W + 1)
+        n_win = i + 1 - lo if W > 0 else 0
+        # keys counted twice: sinks that are also in the window
+        overlap = max(0, min(s, i + 1) - lo) if W > 0 else 0
+        total += n_sink + n_win - overlap
+    return total

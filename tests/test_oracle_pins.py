@@ -1,0 +1,236 @@
+"""Pins of the fp64 oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: a printed example, a closed
+form, a library routine for a special case, an invariant or brute force.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from moa_workloads import ALPHA_GRID, BETA_GRID, CONFIGS, rule_table
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rand(shape, seed):
+    return np.random.default_rng(seed).standard_normal(shape)
+
+
+# --- printed examples --------------------------------------------------------
+
+def test_softmax_printed_example():
+    """softmax([1,2,3]) = [0.09003, 0.24473, 0.66524] +- 1e-5.
+    Realised through the oracle's attention row: q.k_j = j+1 (tau = 1) and
+    V = identity, so O is exactly the softmax weight vector."""
+    with open(os.path.join(GOLDEN, "softmax_example.txt")) as f:
+        line = [l for l in f if l.strip() and not l.startswith("#")][0].split()
+    scores = np.array([float(x) for x in line[:3]])
+    expected = np.array([float(x) for x in line[3:6]])
+    tol = float(line[6])
+    q = np.array([1.0, 0.0, 0.0])
+    K = np.stack([[s, 0.0, 0.0] for s in scores])
+    V = np.eye(3)
+    o, lse = oracle.attend(q, K, V, tau=1.0)
+    assert np.max(np.abs(o - expected)) < tol
+    assert abs(lse - math.log(np.exp(scores).sum())) < 1e-12
+
+
+def test_span_window_density_examples():
+    with open(os.path.join(GOLDEN, "span_examples.txt")) as f:
+        rows = [l.split("#")[0].split() for l in f if l.strip() and not l.startswith("#")]
+    n = 0
+    for kind, a, b, N, s, exp in rows:
+        a, b, N, s = float(a), float(b), int(N), int(s)
+        span = oracle.span_of(a, b, N)
+        if kind == "span":
+            assert span == int(exp), (a, b, N)
+        elif kind == "window":
+            assert oracle.window_of(span, s) == int(exp), (a, b, N)
+        elif kind == "density":
+            w = oracle.window_of(span, s)
+            assert abs(oracle.density([w], s, N) - float(exp)) < 1e-12
+        n += 1
+    assert n >= 10
+
+
+def test_mask_predicate_hand_written_picture():
+    """The predicate against a hand-typed N=8, W=3, s=2 mask picture."""
+    with open(os.path.join(GOLDEN, "mask_N8_W3_s2.txt")) as f:
+        pic = [l.strip() for l in f if l.strip() and not l.startswith("#")]
+    assert len(pic) == 8
+    for i in range(8):
+        got = "".join("1" if oracle.visible(i, j, 3, 2) else "." for j in range(8))
+        assert got == pic[i], (i, got, pic[i])
+        assert list(oracle.visible_keys(i, 3, 2)) == [j for j in range(8) if pic[i][j] == "1"]
+
+
+# --- special cases that reduce to a library routine / closed form ------------
+
+@pytest.mark.parametrize("G", [1, 2])
+@pytest.mark.parametrize("s", [0, 4])
+@pytest.mark.parametrize("extra", [0, 7])
+def test_full_span_is_causal_attention(G, s, extra):
+    """Any W >= N reproduces textbook causal attention (north_star), checked
+    against torch.nn.functional.scaled_dot_product_attention(is_causal=True)
+    in fp64 on the CPU."""
+    B, N, Hkv, d = 2, 40, 2, 16
+    Hq = Hkv * G
+    Q, K, V = _rand((B, N, Hq, d), 1), _rand((B, N, Hkv, d), 2), _rand((B, N, Hkv, d), 3)
+    tau = 1 / math.sqrt(d)
+    O, LSE = oracle.prefill(Q, K, V, [N + extra] * Hq, s, tau)
+    q = torch.from_numpy(Q).permute(0, 2, 1, 3)
+    k = torch.from_numpy(K).permute(0, 2, 1, 3).repeat_interleave(G, dim=1)
+    v = torch.from_numpy(V).permute(0, 2, 1, 3).repeat_interleave(G, dim=1)
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, scale=tau)
+    ref = ref.permute(0, 2, 1, 3).numpy()
+    assert np.max(np.abs(O - ref)) < 1e-12
+    # LSE of the causal row via a plain log-sum-exp over j <= i
+    S = tau * torch.einsum("bhid,bhjd->bhij", q, k)
+    S = S.masked_fill(torch.triu(torch.ones(N, N, dtype=torch.bool), 1), float("-inf"))
+    assert np.max(np.abs(LSE - torch.logsumexp(S, -1).numpy())) < 1e-12
+
+
+def test_window_one_no_sink_is_own_value_row():
+    """W = 1, s = 0: the softmax has one element, so O_i = V_i exactly."""
+    B, N, H, d = 2, 33, 3, 8
+    Q, K, V = _rand((B, N, H, d), 4), _rand((B, N, H, d), 5), _rand((B, N, H, d), 6)
+    O, _ = oracle.prefill(Q, K, V, [1] * H, 0, 0.3)
+    assert np.array_equal(O, V)
+
+
+def _closed_form_visible(i, W, s):
+    """Count and position-sum of V(h,i) by arithmetic series (no predicate)."""
+    n1 = min(s, i + 1)
+    sum1 = n1 * (n1 - 1) / 2
+    if W > 0:
+        lo = max(i - W + 1, n1)
+        n2 = max(0, i - lo + 1)
+        sum2 = (lo + i) * n2 / 2 if n2 else 0.0
+    else:
+        n2, sum2 = 0, 0.0
+    return n1 + n2, sum1 + sum2
+
+
+@pytest.mark.parametrize("W,s", [(1, 0), (5, 0), (5, 3), (0, 3), (17, 4), (64, 1), (100, 0), (3, 20)])
+def test_constant_keys_average_visible_positions(W, s):
+    """Constant K makes every visible score equal, so O_i is the plain mean
+    of the visible V rows; with V[j] = (1, j) the second output is the mean
+    visible position, known in closed form.  LSE = tau q.k + log |V(h,i)|."""
+    N, d = 70, 2
+    Q = _rand((1, N, 1, d), 7)
+    K = np.ones((1, N, 1, d)) * 0.5
+    V = np.stack([np.ones(N), np.arange(N, dtype=np.float64)], axis=1)[None, :, None, :]
+    O, LSE = oracle.prefill(Q, K, V, [W], s, 0.7)
+    for i in range(N):
+        cnt, tot = _closed_form_visible(i, W, s)
+        assert abs(O[0, i, 0, 0] - 1.0) < 1e-12
+        assert abs(O[0, i, 0, 1] - tot / cnt) < 1e-9
+        assert abs(LSE[0, 0, i] - (0.7 * Q[0, i, 0] @ K[0, 0, 0] + math.log(cnt))) < 1e-12
+
+
+def test_rows_sum_to_one():
+    """Softmax rows sum to 1: with V = 1 every output is 1."""
+    B, N, Hq, Hkv, d = 1, 50, 4, 2, 8
+    Q, K = _rand((B, N, Hq, d), 8), _rand((B, N, Hkv, d), 9)
+    V = np.ones((B, N, Hkv, d))
+    O, _ = oracle.prefill(Q, K, V, [0, 3, 17, 60], 2, 1.3)
+    assert np.max(np.abs(O - 1.0)) < 1e-12
+
+
+# --- brute force on tiny inputs ----------------------------------------------
+
+def test_gather_equals_dense_mask_bruteforce():
+    """Gather-set formulation == dense additive-mask formulation, exhaustive
+    over W in [0, N+1] and s in {0..4} for N = 12 (and a GQA group)."""
+    B, N, Hkv, G, d = 1, 12, 1, 2, 4
+    Q, K, V = _rand((B, N, Hkv * G, d), 10), _rand((B, N, Hkv, d), 11), _rand((B, N, Hkv, d), 12)
+    for s in range(5):
+        for W in range(N + 2):
+            if W == 0 and s == 0:
+                continue
+            w = [W, max(W - 1, 0) if s else W]
+            O1, L1 = oracle.prefill(Q, K, V, w, s, 0.5)
+            O2, L2 = oracle.prefill_dense_mask(Q, K, V, w, s, 0.5)
+            assert np.max(np.abs(O1 - O2)) < 1e-13
+            assert np.max(np.abs(L1 - L2)) < 1e-12
+
+
+def test_empty_row_rejected():
+    with pytest.raises(ValueError):
+        oracle.prefill(_rand((1, 4, 1, 2), 1), _rand((1, 4, 1, 2), 2), _rand((1, 4, 1, 2), 3), [0], 0, 1.0)
+
+
+# --- decode and the cache image ----------------------------------------------
+
+def test_decode_is_prefill_row():
+    """A decode step at position p attends exactly like prefill row p of the
+    full prompt (windows frozen, reading c9)."""
+    B, N, Hq, Hkv, d, s = 2, 60, 4, 2, 8, 3
+    W = [5, 9, 1, 70]
+    Q, K, V = _rand((B, N, Hq, d), 13), _rand((B, N, Hkv, d), 14), _rand((B, N, Hkv, d), 15)
+    O, L = oracle.prefill(Q, K, V, W, s, 0.4)
+    for p in (0, 2, 3, 17, 59):
+        o, l = oracle.decode(Q[:, p], K[:, : p + 1], V[:, : p + 1], p, W, s, 0.4)
+        assert np.max(np.abs(o - O[:, p])) < 1e-13
+        assert np.max(np.abs(l - L[:, :, p])) < 1e-13
+
+
+def test_cache_image_ring_invariants():
+    """SPEC.md:463/470/486: resident = min(p+1, s+W); after w+k steps the ring
+    holds exactly the last w positions; sinks never move; each slot's row is
+    the history row of the position it holds."""
+    B, T, Hkv, d, s = 1, 80, 3, 4, 4
+    Wg = [0, 7, 16]
+    K = _rand((B, T, Hkv, d), 16)
+    V = _rand((B, T, Hkv, d), 17)
+    for p in range(T):
+        img = oracle.cache_image(K, V, p, Wg, s)
+        for g, w in enumerate(Wg):
+            Ki, Vi, valid = img[(0, g)]
+            assert valid.sum() == min(p + 1, s + w)
+            held = oracle.resident_positions(p, s, w)
+            for pos in held:
+                r = oracle.slot_of(pos, s, w)
+                assert np.array_equal(Ki[r], K[0, pos, g]) and np.array_equal(Vi[r], V[0, pos, g])
+            if p >= s + w:
+                assert sorted(held) == list(range(min(s, p + 1))) + list(range(p - w + 1, p + 1))
+            for pos in range(min(s, p + 1)):
+                assert oracle.slot_of(pos, s, w) == pos
+    # every ring slot is reused once per W_g positions (eviction of the oldest)
+    assert [oracle.slot_of(p, 4, 7) for p in range(4, 20)] == [4 + (p - 4) % 7 for p in range(4, 20)]
+
+
+def test_visible_pairs_closed_form():
+    """Sum_i |V(h,i)| = W(W+1)/2 + (N-W)W + sum_{i>=W} min(s, i-W+1) for
+    W <= N, and brute force for small N."""
+    for N, W, s in [(30, 0, 3), (30, 7, 0), (30, 7, 5), (30, 30, 2), (31, 40, 2), (64, 17, 20)]:
+        brute = sum(len(oracle.visible_keys(i, W, s)) for i in range(N))
+        assert oracle.visible_pairs(N, W, s) == brute
+    N, W, s = 4096, 1984, 64
+    closed = W * (W + 1) // 2 + (N - W) * W + sum(min(s, i - W + 1) for i in range(W, N))
+    assert oracle.visible_pairs(N, W, s) == closed
+    assert abs(closed / (N * (N + 1) / 2) - 0.750) < 0.001   # 0.750 of causal
+
+
+# --- the committed rule tables ---------------------------------------------
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_rule_tables_shape_density(name):
+    cfg = CONFIGS[name]
+    t = rule_table(name)
+    a, b = np.array(t["alpha"]), np.array(t["beta"])
+    assert a.shape == (cfg.layers, cfg.hq)
+    assert set(a.ravel()) <= set(ALPHA_GRID) and set(b.ravel()) <= set(BETA_GRID)
+    for l in range(cfg.layers):
+        assert len(set(zip(a[l], b[l]))) <= 2
+        for g in range(cfg.hkv):                               # one rule per kv-group
+            sl = slice(g * cfg.group, (g + 1) * cfg.group)
+            assert len(set(zip(a[l, sl], b[l, sl]))) == 1
+    w = [[oracle.window_of(oracle.span_of(x, y, cfg.N), cfg.n_sink) for x, y in zip(a[l], b[l])]
+         for l in range(cfg.layers)]
+    dens = np.mean([oracle.density(wl, cfg.n_sink, cfg.N) for wl in w])
+    assert abs(dens - cfg.target_density) < 0.01
