@@ -1,0 +1,220 @@
+/*
+ * moa.h -- C ABI of the B200 (sm_100a) MoA attention hot path.
+ *
+ * MoA = "Mixture of Attention Spans" (arXiv 2406.14909).  Every (layer, head)
+ * attends only to a few global sink tokens plus its own window of recent keys;
+ * the window follows the head's elastic rule S_h = alpha_h + beta_h * N
+ * (Eq. 2, clipped to [0, N] per PAPER.md:692).  Citations are
+ * PAPER.md line numbers and SURVEY.md sections.
+ *
+ * Mask of q-head h (token granular, reading c5): key j is visible to query i
+ * iff  0 <= j <= i  and  ( j < n_sink  or  i - j < W_h ).
+ *   - sinks: "the initial few tokens (64 tokens for MoA) are not masked"
+ *     (PAPER.md:178);
+ *   - window W_h counts the query itself (reading c3);
+ *   - output: O = softmax(tau * Q K^T + M) V  (Eq. 1).
+ *
+ * GQA (reading c10): q-head h reads kv-group g = h / G, G = Hq / Hkv.  The
+ * cache of group g holds W_g = max_{h in g} W_h recent rows; each q-head
+ * still masks to its own W_h.
+ *
+ * Tensor layouts (row-major, elements of the context dtype):
+ *   prefill  Q, O : [B, N, Hq_local, d]  token rows, stride *_row_stride
+ *            K, V : [B, N, Hkv_local, d] token rows, stride kv_row_stride
+ *            batch stride = N * row_stride; head h at offset h * d in a row.
+ *            A rank holding a head shard passes pointers to its first local
+ *            head and the full row stride.
+ *   decode   q, o : [B, Hq_local, d]   batch stride *_batch_stride
+ *            k_new, v_new : [B, Hkv_local, d] batch stride kv_batch_stride
+ *   lse      fp32; prefill [B, Hq_local, N], decode [B, Hq_local]
+ *            (natural log of the softmax denominator incl. tau, i.e.
+ *             lse = log sum_j exp(tau q.k_j)).
+ *   KV cache (caller-owned device memory, reading c13):
+ *            per layer, per sequence b, per local group g one region of
+ *            (n_sink + W_g) rows of d elements: [sink rows | ring rows].
+ *            Position p lives in row p if p < n_sink, else in row
+ *            n_sink + (p - n_sink) mod W_g  ("replace the old KV-Cache that
+ *            exceeds the span with the latest").  K and V have
+ *            identical layouts in two separate buffers.
+ *
+ * Ownership: the caller owns every device buffer (Q/K/V/O, caches,
+ * workspace).  The library owns the context and its small host/device span
+ * tables.  moa_prefill / moa_cache_fill / moa_kv_append / moa_decode_step
+ * never allocate, never synchronise the host and only enqueue work on the
+ * given stream (CUDA-graph capturable).
+ *
+ * Errors: every call returns moa_status.  Argument validation failures return
+ * immediately with nothing launched and a message in moa_last_error()
+ * (thread-local).  A sticky asynchronous CUDA fault is reported as
+ * MOA_ERR_CUDA by the next call.  No exception or abort crosses the ABI.
+ * A context is not thread-safe: use one per (thread, device).
+ */
+#ifndef MOA_H_
+#define MOA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct moa_ctx moa_ctx;          /* opaque */
+typedef void *moa_stream_t;              /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum {
+  MOA_OK = 0,
+  MOA_ERR_INVALID_ARG = 1,   /* bad pointer / value (e.g. W < 0, W = 0 with n_sink = 0) */
+  MOA_ERR_SHAPE = 2,         /* dims not supported or inconsistent (head_dim not 64/128 ...) */
+  MOA_ERR_STATE = 3,         /* call out of order (spans unset, cache unbound, wrong pos) */
+  MOA_ERR_UNSUPPORTED = 4,   /* valid request this build does not implement */
+  MOA_ERR_OOM = 5,           /* host allocation failed / workspace too small */
+  MOA_ERR_CUDA = 6           /* CUDA runtime/driver error (message has the CUDA string) */
+} moa_status;
+
+typedef enum { MOA_BF16 = 0, MOA_FP32 = 1 } moa_dtype;
+
+/* Version string of the library build. */
+const char *moa_version(void);
+/* Message of the last non-OK status on this thread ("" if none). */
+const char *moa_last_error(void);
+
+/*
+ * Create a context.
+ *   device       CUDA device ordinal, or -1 for a host-only planning context
+ *                (span tables, layout and schedule queries work; launches
+ *                return MOA_ERR_STATE).
+ *   dtype        I/O dtype of Q/K/V/O and the cache (compute is fp32).
+ *   num_layers, num_q_heads, num_kv_heads: the model's totals (Hq % Hkv == 0).
+ *   head_dim     64 or 128.
+ *   max_batch    largest batch any call will pass (plans decode splits).
+ *   kv_group_begin, kv_group_end: the kv-groups this context serves
+ *                [begin, end) (all groups: 0, num_kv_heads).  Its local
+ *                q-heads are [begin*G, end*G).
+ */
+moa_status moa_create(moa_ctx **out, int device, moa_dtype dtype, int num_layers,
+                      int num_q_heads, int num_kv_heads, int head_dim, int max_batch,
+                      int kv_group_begin, int kv_group_end);
+moa_status moa_destroy(moa_ctx *ctx);
+
+/*
+ * Host helper: elastic rules -> windows.  For every head
+ *   span   = clamp(ceil(alpha + beta * N), 0, N)   (Eq. 2; clip PAPER.md:692;
+ *                                                  ceil = reading c6)
+ *   window = max(0, span - n_sink)                 (span = window + sinks)
+ * alpha, beta, window_out: n_heads entries (host memory).
+ */
+moa_status moa_resolve_spans(const float *alpha, const float *beta, int n_heads, int64_t N,
+                             int n_sink, int32_t *window_out);
+
+/*
+ * Install the spans of one layer (host memory; frozen for the whole decode,
+ * PAPER.md:704, reading c9).
+ *   window_per_q_head  num_q_heads entries (ALL heads of the layer; the
+ *                      context keeps its shard).  W >= 0; W = 0 needs n_sink >= 1.
+ *   n_sink             global sink tokens (64 for MoA).
+ *   N                  prompt length the spans were resolved at (>= 1).
+ * Builds the span table, cache offsets, the prefill block-skip schedule and
+ * the decode work list, and uploads them.  Invalidates a bound cache's layout
+ * if the layer's footprint changes (re-bind after the last set_spans).
+ */
+moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_head,
+                         int n_sink, int64_t N);
+
+/* Bytes of the K (and of the V) cache of all layers / of one layer for
+ * `batch` sequences.  All layers' spans must be set for the first form. */
+moa_status moa_cache_bytes(const moa_ctx *ctx, int batch, size_t *k_bytes, size_t *v_bytes);
+moa_status moa_layer_cache_bytes(const moa_ctx *ctx, int layer, int batch, size_t *k_bytes,
+                                 size_t *v_bytes);
+/* Scratch needed by moa_prefill / moa_decode_step for `batch` sequences
+ * (max over layers whose spans are set; >= 256 bytes). */
+moa_status moa_workspace_bytes(const moa_ctx *ctx, int batch, size_t *bytes);
+
+/* Bind caller-owned device memory as the cache of every layer (layer l at
+ * byte offset sum_{l'<l} layer bytes) or of one layer.  256-byte aligned. */
+moa_status moa_bind_cache(moa_ctx *ctx, void *k_cache, void *v_cache, int batch);
+moa_status moa_bind_layer_cache(moa_ctx *ctx, int layer, void *k_cache, void *v_cache, int batch);
+
+/*
+ * Causal prefill of one layer with the per-head MoA mask (Eq. 1 + the mask
+ * above), then the cache fill of rows [0, min(s,N)) and [max(s, N-W_g), N)
+ * (SURVEY §8(a) a4+a5).  bf16: tcgen05 tensor-core kernel; fp32: FFMA kernel.
+ *   scale      tau (the softmax scale; Eq. 1 has none, reading c8).
+ *   lse_out    nullable, fp32 [B, Hq_local, N].
+ *   workspace  device scratch of moa_workspace_bytes (may be NULL if 0 needed).
+ * Afterwards the layer's next decode position is N.
+ */
+moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, const void *v,
+                       void *o, int64_t q_row_stride, int64_t kv_row_stride,
+                       int64_t o_row_stride, int batch, int64_t N, float scale, float *lse_out,
+                       void *workspace, size_t ws_bytes, moa_stream_t stream);
+
+/* Cache fill alone (a5): write the resident rows of a prompt of length N
+ * (K/V as in moa_prefill) into the layer's cache; next position = N. */
+moa_status moa_cache_fill(moa_ctx *ctx, int layer, const void *k, const void *v,
+                          int64_t kv_row_stride, int batch, int64_t N, moa_stream_t stream);
+
+/*
+ * Append the K/V of absolute position `pos` (a6): for every (b, g) write
+ * k_new/v_new into row slot(pos).  A group with W_g = 0 stores only sink
+ * positions.  `pos` must equal the layer's next position (N after prefill,
+ * then +1 per append).
+ */
+moa_status moa_kv_append(moa_ctx *ctx, int layer, const void *k_new, const void *v_new,
+                         int64_t kv_batch_stride, int batch, int64_t pos, moa_stream_t stream);
+
+/*
+ * One decode step of one layer at position `pos` (a7 + a8): every local
+ * q-head attends over its group's cache restricted to its own window,
+ * split-KV partials in `workspace`, merged by LSE into o.  `pos` must be the
+ * last appended position (append before decode: the token sees itself).
+ *   lse_out nullable fp32 [B, Hq_local].
+ */
+moa_status moa_decode_step(moa_ctx *ctx, int layer, const void *q, void *o,
+                           int64_t q_batch_stride, int64_t o_batch_stride, int batch,
+                           int64_t pos, float scale, float *lse_out, void *workspace,
+                           size_t ws_bytes, moa_stream_t stream);
+
+/* Append + decode in one launch (a6 + a7 + a8 fused): identical results to
+ * moa_kv_append(pos) followed by moa_decode_step(pos). */
+moa_status moa_decode_step_fused(moa_ctx *ctx, int layer, const void *q, const void *k_new,
+                                 const void *v_new, void *o, int64_t q_batch_stride,
+                                 int64_t kv_batch_stride, int64_t o_batch_stride, int batch,
+                                 int64_t pos, float scale, float *lse_out, void *workspace,
+                                 size_t ws_bytes, moa_stream_t stream);
+
+/* ---------------- host-side introspection (planning contexts too) ---------------- */
+
+/* Window of a local q-head / cache capacity W_g of a local group. */
+moa_status moa_get_window(const moa_ctx *ctx, int layer, int q_head_local, int32_t *window);
+moa_status moa_get_group_window(const moa_ctx *ctx, int layer, int group_local, int32_t *w_g);
+/* Row of position `pos` inside group region (slot), -1 if not stored. */
+moa_status moa_slot_of(const moa_ctx *ctx, int layer, int group_local, int64_t pos, int64_t *slot);
+/* Row offset (in rows of d elements, from the layer's cache base) and row
+ * count of the region of sequence b, local group g. */
+moa_status moa_cache_region(const moa_ctx *ctx, int layer, int b, int group_local,
+                            int64_t *row_offset, int64_t *rows);
+/* Byte offset of a layer inside a moa_bind_cache buffer laid out for `batch`. */
+moa_status moa_layer_offset(const moa_ctx *ctx, int layer, int batch, size_t *byte_offset);
+
+/* Prefill block-skip schedule (a2): the kv tiles (of MOA_TILE keys) that q-tile
+ * `q_tile` (rows [q_tile*MOA_TILE, ...)) of local q-head h visits, in visit
+ * order, with flags 1 = EDGE (needs the mask) / 0 = FULL.  *n_tiles is set
+ * to the count; at most max_tiles entries are written. */
+#define MOA_TILE 128
+moa_status moa_prefill_tiles(const moa_ctx *ctx, int layer, int q_head_local, int q_tile,
+                             int32_t *tiles, uint8_t *edge, int max_tiles, int32_t *n_tiles);
+/* Work-item order of the prefill kernel: n_items (q_head_local, q_tile) pairs,
+ * longest first (LPT).  items: 2 * max_items int32. */
+moa_status moa_prefill_items(const moa_ctx *ctx, int layer, int32_t *items, int max_items,
+                             int32_t *n_items);
+/* Decode work list: n chunks of (group_local, row_begin, row_end). */
+moa_status moa_decode_chunks(const moa_ctx *ctx, int layer, int32_t *chunks, int max_chunks,
+                             int32_t *n_chunks);
+/* Next position the layer expects to append (N after prefill/fill). */
+moa_status moa_next_pos(const moa_ctx *ctx, int layer, int64_t *pos);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOA_H_ */

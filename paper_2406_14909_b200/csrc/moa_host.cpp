@@ -1,0 +1,660 @@
+// moa_host.cpp -- C ABI entry points and the host runtime of libmoa.so:
+// span resolution (Eq. 2), span table, compact cache layout, prefill
+// block-skip schedule, decode work list, validation and error reporting.
+// See include/moa.h for the contract of every call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <numeric>
+
+#include "moa_internal.h"
+
+using moa::LayerPlan;
+
+namespace {
+
+thread_local std::string g_err;
+
+moa_status fail(moa_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+moa_status ok() { return MOA_OK; }
+
+moa_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(MOA_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool active = false;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+      active = cudaSetDevice(dev) == cudaSuccess;
+    }
+  }
+  ~DeviceGuard() {
+    if (active) cudaSetDevice(prev);
+  }
+};
+
+// A sticky asynchronous fault from earlier work is reported by the next call.
+moa_status check_sticky(const moa_ctx *ctx) {
+  if (ctx->device < 0) return MOA_OK;
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "earlier asynchronous CUDA error");
+  return MOA_OK;
+}
+
+size_t esize(const moa_ctx *c) { return c->dtype == MOA_BF16 ? 2 : 4; }
+
+moa_status check_layer(const moa_ctx *ctx, int layer, bool need_set) {
+  if (!ctx) return fail(MOA_ERR_INVALID_ARG, "ctx is NULL");
+  if (layer < 0 || layer >= ctx->L)
+    return fail(MOA_ERR_INVALID_ARG, "layer %d out of range [0, %d)", layer, ctx->L);
+  if (need_set && !ctx->layers[layer].set)
+    return fail(MOA_ERR_STATE, "moa_set_spans was not called for layer %d", layer);
+  return MOA_OK;
+}
+
+int decode_chunk_rows_override() {
+  const char *e = std::getenv("MOA_DECODE_CHUNK");
+  if (!e) return 0;
+  int v = std::atoi(e);
+  return v > 0 ? v : 0;
+}
+
+void free_tables(LayerPlan &p) {
+  if (p.d_tables) cudaFree(p.d_tables);
+  p.d_tables = nullptr;
+  p.d_win_q = p.d_win_g = nullptr;
+  p.d_g_off = nullptr;
+  p.d_items = p.d_chunks = p.d_g_chunk = nullptr;
+  p.d_counters = nullptr;
+}
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
+  if (ctx->device < 0) return MOA_OK;
+  size_t o_winq = 0;
+  size_t o_wing = align16(o_winq + p.win_q.size() * 4);
+  size_t o_goff = align16(o_wing + p.win_g.size() * 4);
+  size_t o_items = align16(o_goff + p.g_off.size() * 8);
+  size_t o_chunks = align16(o_items + p.items.size() * 4);
+  size_t o_gch = align16(o_chunks + p.chunks.size() * 4);
+  size_t o_cnt = align16(o_gch + p.g_chunk.size() * 4);
+  size_t total = align16(o_cnt + (size_t)ctx->max_batch * ctx->ngl * 4);
+  std::vector<unsigned char> host(total, 0);
+  std::memcpy(host.data() + o_winq, p.win_q.data(), p.win_q.size() * 4);
+  std::memcpy(host.data() + o_wing, p.win_g.data(), p.win_g.size() * 4);
+  std::memcpy(host.data() + o_goff, p.g_off.data(), p.g_off.size() * 8);
+  std::memcpy(host.data() + o_items, p.items.data(), p.items.size() * 4);
+  std::memcpy(host.data() + o_chunks, p.chunks.data(), p.chunks.size() * 4);
+  std::memcpy(host.data() + o_gch, p.g_chunk.data(), p.g_chunk.size() * 4);
+  DeviceGuard dg(ctx->device);
+  free_tables(p);
+  void *d = nullptr;
+  cudaError_t e = cudaMalloc(&d, total);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(span tables)");
+  e = cudaMemcpy(d, host.data(), total, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(e, "cudaMemcpy(span tables)");
+  }
+  auto *b = static_cast<unsigned char *>(d);
+  p.d_tables = d;
+  p.d_win_q = reinterpret_cast<const int32_t *>(b + o_winq);
+  p.d_win_g = reinterpret_cast<const int32_t *>(b + o_wing);
+  p.d_g_off = reinterpret_cast<const int64_t *>(b + o_goff);
+  p.d_items = reinterpret_cast<const int32_t *>(b + o_items);
+  p.d_chunks = reinterpret_cast<const int32_t *>(b + o_chunks);
+  p.d_g_chunk = reinterpret_cast<const int32_t *>(b + o_gch);
+  p.d_counters = reinterpret_cast<int *>(b + o_cnt);
+  return MOA_OK;
+}
+
+size_t layer_bytes(const moa_ctx *ctx, const LayerPlan &p, int batch) {
+  return (size_t)batch * (size_t)p.rows_per_seq * (size_t)ctx->d * esize(ctx);
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+extern "C" {
+
+const char *moa_version(void) { return "moa-b200 0.1 (sm_100a)"; }
+
+const char *moa_last_error(void) { return g_err.c_str(); }
+
+moa_status moa_create(moa_ctx **out, int device, moa_dtype dtype, int num_layers,
+                      int num_q_heads, int num_kv_heads, int head_dim, int max_batch,
+                      int kv_group_begin, int kv_group_end) {
+  if (!out) return fail(MOA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (dtype != MOA_BF16 && dtype != MOA_FP32) return fail(MOA_ERR_INVALID_ARG, "bad dtype %d", (int)dtype);
+  if (num_layers <= 0 || num_q_heads <= 0 || num_kv_heads <= 0 || max_batch <= 0)
+    return fail(MOA_ERR_SHAPE, "layers/heads/max_batch must be positive");
+  if (num_q_heads % num_kv_heads != 0)
+    return fail(MOA_ERR_SHAPE, "num_q_heads %d not a multiple of num_kv_heads %d", num_q_heads, num_kv_heads);
+  if (head_dim != 64 && head_dim != 128)
+    return fail(MOA_ERR_SHAPE, "head_dim %d unsupported (64 or 128)", head_dim);
+  int G = num_q_heads / num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return fail(MOA_ERR_UNSUPPORTED, "GQA group size %d unsupported (1, 2, 4 or 8)", G);
+  if (kv_group_begin < 0 || kv_group_end > num_kv_heads || kv_group_begin >= kv_group_end)
+    return fail(MOA_ERR_SHAPE, "kv-group shard [%d, %d) invalid for %d groups", kv_group_begin,
+                kv_group_end, num_kv_heads);
+  if (device >= 0) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device >= n) return fail(MOA_ERR_INVALID_ARG, "device %d >= device count %d", device, n);
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+      return fail(MOA_ERR_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)",
+                  device, prop.major, prop.minor);
+  }
+  moa_ctx *c = new (std::nothrow) moa_ctx();
+  if (!c) return fail(MOA_ERR_OOM, "host allocation failed");
+  c->device = device;
+  c->dtype = dtype;
+  c->L = num_layers;
+  c->Hq = num_q_heads;
+  c->Hkv = num_kv_heads;
+  c->G = G;
+  c->d = head_dim;
+  c->max_batch = max_batch;
+  c->g0 = kv_group_begin;
+  c->g1 = kv_group_end;
+  c->ngl = kv_group_end - kv_group_begin;
+  c->nql = c->ngl * G;
+  c->layers.resize(num_layers);
+  *out = c;
+  return ok();
+}
+
+moa_status moa_destroy(moa_ctx *ctx) {
+  if (!ctx) return MOA_OK;
+  {
+    DeviceGuard dg(ctx->device);
+    for (auto &p : ctx->layers) free_tables(p);
+  }
+  delete ctx;
+  return MOA_OK;
+}
+
+moa_status moa_resolve_spans(const float *alpha, const float *beta, int n_heads, int64_t N,
+                             int n_sink, int32_t *window_out) {
+  if (!alpha || !beta || !window_out) return fail(MOA_ERR_INVALID_ARG, "NULL argument");
+  if (n_heads < 0 || N < 1 || n_sink < 0) return fail(MOA_ERR_INVALID_ARG, "bad n_heads/N/n_sink");
+  for (int h = 0; h < n_heads; ++h) {
+    // Eq. 2 in double: alpha + beta * N (exact for the paper's grid), ceil, clip [0, N].
+    double sp = std::ceil((double)alpha[h] + (double)beta[h] * (double)N);
+    if (!(sp == sp)) return fail(MOA_ERR_INVALID_ARG, "NaN rule at head %d", h);
+    if (sp < 0) sp = 0;
+    if (sp > (double)N) sp = (double)N;
+    int64_t span = (int64_t)sp;
+    int64_t w = span - n_sink;
+    window_out[h] = (int32_t)(w > 0 ? w : 0);
+  }
+  return ok();
+}
+
+moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_head, int n_sink,
+                         int64_t N) {
+  moa_status st = check_layer(ctx, layer, false);
+  if (st) return st;
+  if (!window_per_q_head) return fail(MOA_ERR_INVALID_ARG, "window_per_q_head is NULL");
+  if (n_sink < 0 || n_sink > (1 << 20)) return fail(MOA_ERR_INVALID_ARG, "n_sink %d invalid", n_sink);
+  if (N < 1 || N > (int64_t(1) << 31)) return fail(MOA_ERR_INVALID_ARG, "N %lld invalid", (long long)N);
+  for (int h = 0; h < ctx->Hq; ++h) {
+    int w = window_per_q_head[h];
+    if (w < 0 || w > (1 << 30)) return fail(MOA_ERR_INVALID_ARG, "window[%d] = %d invalid", h, w);
+    if (w == 0 && n_sink == 0)
+      return fail(MOA_ERR_INVALID_ARG, "window[%d] = 0 with no sinks: empty softmax row (reading c7)", h);
+  }
+  LayerPlan &p = ctx->layers[layer];
+  LayerPlan np;
+  np.set = true;
+  np.n_sink = n_sink;
+  np.N = N;
+  const int G = ctx->G;
+  np.win_q.resize(ctx->nql);
+  for (int h = 0; h < ctx->nql; ++h) np.win_q[h] = window_per_q_head[ctx->g0 * G + h];
+  np.win_g.resize(ctx->ngl);
+  np.g_off.resize(ctx->ngl);
+  int64_t off = 0;
+  for (int g = 0; g < ctx->ngl; ++g) {
+    int wg = 0;
+    for (int j = 0; j < G; ++j) wg = std::max(wg, np.win_q[g * G + j]);
+    np.win_g[g] = wg;
+    np.g_off[g] = off;
+    off += (int64_t)n_sink + wg;
+  }
+  np.rows_per_seq = off;
+
+  // prefill work items, longest (most kv tiles) first
+  const int nqt = (int)((N + moa::kTile - 1) / moa::kTile);
+  struct It { int h, qt, cnt; };
+  std::vector<It> its;
+  its.reserve((size_t)ctx->nql * nqt);
+  for (int h = 0; h < ctx->nql; ++h)
+    for (int qt = 0; qt < nqt; ++qt) {
+      int64_t i0 = (int64_t)qt * moa::kTile;
+      int64_t i1 = std::min<int64_t>(N, i0 + moa::kTile) - 1;
+      its.push_back({h, qt, moa::kv_tile_ranges(i0, i1, np.win_q[h], n_sink).count()});
+    }
+  std::stable_sort(its.begin(), its.end(), [](const It &a, const It &b) { return a.cnt > b.cnt; });
+  np.items.resize(its.size() * 2);
+  for (size_t i = 0; i < its.size(); ++i) {
+    np.items[2 * i] = its[i].h;
+    np.items[2 * i + 1] = its[i].qt;
+  }
+
+  // decode work list: split every group region into chunks of ~chunk_rows rows
+  int64_t total_rows = off * ctx->max_batch;
+  const int64_t target_ctas = 148 * 6;
+  int64_t c = (total_rows + target_ctas - 1) / target_ctas;
+  c = ((c + 63) / 64) * 64;
+  c = std::max<int64_t>(64, std::min<int64_t>(c, 4096));
+  if (int ov = decode_chunk_rows_override()) c = ov;
+  np.chunk_rows = (int)c;
+  np.g_chunk.resize(ctx->ngl + 1);
+  np.max_chunks_per_group = 0;
+  for (int g = 0; g < ctx->ngl; ++g) {
+    np.g_chunk[g] = (int32_t)(np.chunks.size() / 3);
+    int64_t R = (int64_t)n_sink + np.win_g[g];
+    int n = 0;
+    for (int64_t r0 = 0; r0 < R; r0 += c, ++n) {
+      np.chunks.push_back(g);
+      np.chunks.push_back((int32_t)r0);
+      np.chunks.push_back((int32_t)std::min<int64_t>(R, r0 + c));
+    }
+    np.max_chunks_per_group = std::max(np.max_chunks_per_group, n);
+  }
+  np.g_chunk[ctx->ngl] = (int32_t)(np.chunks.size() / 3);
+
+  // keep a bound cache if the footprint is unchanged
+  bool same = p.set && p.rows_per_seq == np.rows_per_seq && p.n_sink == np.n_sink && p.win_g == np.win_g;
+  if (same) {
+    np.k_cache = p.k_cache;
+    np.v_cache = p.v_cache;
+    np.bound_batch = p.bound_batch;
+    np.next_pos = p.k_cache ? 0 : -1;
+  }
+  st = upload_tables(ctx, np);
+  if (st) return st;
+  {
+    DeviceGuard dg(ctx->device);
+    free_tables(p);
+  }
+  p = np;
+  return ok();
+}
+
+moa_status moa_layer_cache_bytes(const moa_ctx *ctx, int layer, int batch, size_t *k_bytes,
+                                 size_t *v_bytes) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (batch < 1) return fail(MOA_ERR_INVALID_ARG, "batch %d invalid", batch);
+  size_t b = layer_bytes(ctx, ctx->layers[layer], batch);
+  if (k_bytes) *k_bytes = b;
+  if (v_bytes) *v_bytes = b;
+  return ok();
+}
+
+moa_status moa_cache_bytes(const moa_ctx *ctx, int batch, size_t *k_bytes, size_t *v_bytes) {
+  if (!ctx) return fail(MOA_ERR_INVALID_ARG, "ctx is NULL");
+  if (batch < 1) return fail(MOA_ERR_INVALID_ARG, "batch %d invalid", batch);
+  size_t tot = 0;
+  for (int l = 0; l < ctx->L; ++l) {
+    if (!ctx->layers[l].set) return fail(MOA_ERR_STATE, "spans of layer %d not set", l);
+    tot += align256(layer_bytes(ctx, ctx->layers[l], batch));
+  }
+  if (k_bytes) *k_bytes = tot;
+  if (v_bytes) *v_bytes = tot;
+  return ok();
+}
+
+moa_status moa_layer_offset(const moa_ctx *ctx, int layer, int batch, size_t *byte_offset) {
+  moa_status st = check_layer(ctx, layer, false);
+  if (st) return st;
+  if (!byte_offset) return fail(MOA_ERR_INVALID_ARG, "byte_offset is NULL");
+  size_t off = 0;
+  for (int l = 0; l < layer; ++l) {
+    if (!ctx->layers[l].set) return fail(MOA_ERR_STATE, "spans of layer %d not set", l);
+    off += align256(layer_bytes(ctx, ctx->layers[l], batch));
+  }
+  *byte_offset = off;
+  return ok();
+}
+
+moa_status moa_workspace_bytes(const moa_ctx *ctx, int batch, size_t *bytes) {
+  if (!ctx || !bytes) return fail(MOA_ERR_INVALID_ARG, "NULL argument");
+  if (batch < 1) return fail(MOA_ERR_INVALID_ARG, "batch %d invalid", batch);
+  size_t mx = 256;
+  for (const auto &p : ctx->layers)
+    if (p.set)
+      mx = std::max(mx, moa::decode_ws_bytes(batch, (int)(p.chunks.size() / 3), ctx->G, ctx->d));
+  *bytes = mx;
+  return ok();
+}
+
+moa_status moa_bind_layer_cache(moa_ctx *ctx, int layer, void *k_cache, void *v_cache, int batch) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (!k_cache || !v_cache) return fail(MOA_ERR_INVALID_ARG, "cache pointer is NULL");
+  if (((uintptr_t)k_cache | (uintptr_t)v_cache) & 255)
+    return fail(MOA_ERR_INVALID_ARG, "cache pointers must be 256-byte aligned");
+  if (batch < 1 || batch > ctx->max_batch)
+    return fail(MOA_ERR_INVALID_ARG, "batch %d not in [1, max_batch=%d]", batch, ctx->max_batch);
+  LayerPlan &p = ctx->layers[layer];
+  p.k_cache = k_cache;
+  p.v_cache = v_cache;
+  p.bound_batch = batch;
+  p.next_pos = 0;
+  return ok();
+}
+
+moa_status moa_bind_cache(moa_ctx *ctx, void *k_cache, void *v_cache, int batch) {
+  if (!ctx) return fail(MOA_ERR_INVALID_ARG, "ctx is NULL");
+  size_t kb = 0;
+  moa_status st = moa_cache_bytes(ctx, batch, &kb, nullptr);
+  if (st) return st;
+  size_t off = 0;
+  for (int l = 0; l < ctx->L; ++l) {
+    st = moa_bind_layer_cache(ctx, l, static_cast<char *>(k_cache) + off,
+                              static_cast<char *>(v_cache) + off, batch);
+    if (st) return st;
+    off += align256(layer_bytes(ctx, ctx->layers[l], batch));
+  }
+  return ok();
+}
+
+// ---------------------------------------------------------------------------------------------
+// launches
+// ---------------------------------------------------------------------------------------------
+
+static moa_status check_launch_common(const moa_ctx *ctx, int layer, int batch) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (ctx->device < 0) return fail(MOA_ERR_STATE, "planning context (device -1) cannot launch");
+  const LayerPlan &p = ctx->layers[layer];
+  if (!p.k_cache) return fail(MOA_ERR_STATE, "no cache bound for layer %d", layer);
+  if (batch < 1 || batch > p.bound_batch)
+    return fail(MOA_ERR_INVALID_ARG, "batch %d not in [1, bound batch %d]", batch, p.bound_batch);
+  return check_sticky(ctx);
+}
+
+static bool aligned16(const void *ptr) { return ((uintptr_t)ptr & 15) == 0; }
+
+moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, const void *v,
+                       void *o, int64_t q_row_stride, int64_t kv_row_stride,
+                       int64_t o_row_stride, int batch, int64_t N, float scale, float *lse_out,
+                       void *workspace, size_t ws_bytes, moa_stream_t stream) {
+  (void)workspace;
+  (void)ws_bytes;
+  moa_status st = check_launch_common(ctx, layer, batch);
+  if (st) return st;
+  LayerPlan &p = ctx->layers[layer];
+  if (!q || !k || !v || !o) return fail(MOA_ERR_INVALID_ARG, "q/k/v/o must be non-NULL");
+  if (N != p.N)
+    return fail(MOA_ERR_SHAPE, "prefill N=%lld but spans were set for N=%lld", (long long)N, (long long)p.N);
+  const int64_t d = ctx->d;
+  if (q_row_stride < ctx->nql * d || o_row_stride < ctx->nql * d || kv_row_stride < ctx->ngl * d)
+    return fail(MOA_ERR_SHAPE, "row strides smaller than local heads * head_dim");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) ||
+      (q_row_stride * (int64_t)esize(ctx)) % 16 || (kv_row_stride * (int64_t)esize(ctx)) % 16 ||
+      (o_row_stride * (int64_t)esize(ctx)) % 16)
+    return fail(MOA_ERR_INVALID_ARG, "q/k/v/o pointers and row strides must be 16-byte aligned");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(MOA_ERR_INVALID_ARG, "scale must be finite > 0");
+  DeviceGuard dg(ctx->device);
+  moa::PrefillArgs a{};
+  a.q = q; a.k = k; a.v = v; a.o = o;
+  a.q_row_stride = q_row_stride; a.kv_row_stride = kv_row_stride; a.o_row_stride = o_row_stride;
+  a.batch = batch; a.N = N; a.scale = scale; a.lse = lse_out; a.n_sink = p.n_sink;
+  a.nql = ctx->nql; a.G = ctx->G; a.d = ctx->d;
+  a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
+  int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_tc(a, stream);
+  if (e) return cuda_fail((cudaError_t)e, "prefill launch");
+  moa::CacheArgs c{};
+  c.k = k; c.v = v; c.row_stride = kv_row_stride; c.k_cache = p.k_cache; c.v_cache = p.v_cache;
+  c.rows_per_seq = p.rows_per_seq; c.d_g_off = p.d_g_off; c.d_win_g = p.d_win_g;
+  c.ngl = ctx->ngl; c.d = ctx->d; c.n_sink = p.n_sink; c.batch = batch; c.N_or_pos = N;
+  c.esize = (int)esize(ctx);
+  c.max_region_rows = (int64_t)p.n_sink + *std::max_element(p.win_g.begin(), p.win_g.end());
+  e = moa::launch_cache_fill(c, stream);
+  if (e) return cuda_fail((cudaError_t)e, "cache fill launch");
+  p.next_pos = N;
+  return ok();
+}
+
+moa_status moa_cache_fill(moa_ctx *ctx, int layer, const void *k, const void *v,
+                          int64_t kv_row_stride, int batch, int64_t N, moa_stream_t stream) {
+  moa_status st = check_launch_common(ctx, layer, batch);
+  if (st) return st;
+  LayerPlan &p = ctx->layers[layer];
+  if (!k || !v) return fail(MOA_ERR_INVALID_ARG, "k/v must be non-NULL");
+  if (N < 1) return fail(MOA_ERR_INVALID_ARG, "N must be >= 1");
+  if (kv_row_stride < ctx->ngl * ctx->d) return fail(MOA_ERR_SHAPE, "kv_row_stride too small");
+  if (!aligned16(k) || !aligned16(v) || (kv_row_stride * (int64_t)esize(ctx)) % 16)
+    return fail(MOA_ERR_INVALID_ARG, "k/v pointers and row stride must be 16-byte aligned");
+  DeviceGuard dg(ctx->device);
+  moa::CacheArgs c{};
+  c.k = k; c.v = v; c.row_stride = kv_row_stride; c.k_cache = p.k_cache; c.v_cache = p.v_cache;
+  c.rows_per_seq = p.rows_per_seq; c.d_g_off = p.d_g_off; c.d_win_g = p.d_win_g;
+  c.ngl = ctx->ngl; c.d = ctx->d; c.n_sink = p.n_sink; c.batch = batch; c.N_or_pos = N;
+  c.esize = (int)esize(ctx);
+  c.max_region_rows = (int64_t)p.n_sink + *std::max_element(p.win_g.begin(), p.win_g.end());
+  int e = moa::launch_cache_fill(c, stream);
+  if (e) return cuda_fail((cudaError_t)e, "cache fill launch");
+  p.next_pos = N;
+  return ok();
+}
+
+moa_status moa_kv_append(moa_ctx *ctx, int layer, const void *k_new, const void *v_new,
+                         int64_t kv_batch_stride, int batch, int64_t pos, moa_stream_t stream) {
+  moa_status st = check_launch_common(ctx, layer, batch);
+  if (st) return st;
+  LayerPlan &p = ctx->layers[layer];
+  if (!k_new || !v_new) return fail(MOA_ERR_INVALID_ARG, "k_new/v_new must be non-NULL");
+  if (pos != p.next_pos)
+    return fail(MOA_ERR_STATE, "kv_append pos=%lld but layer %d expects %lld", (long long)pos, layer,
+                (long long)p.next_pos);
+  if (kv_batch_stride < ctx->ngl * ctx->d) return fail(MOA_ERR_SHAPE, "kv_batch_stride too small");
+  if (!aligned16(k_new) || !aligned16(v_new) || (kv_batch_stride * (int64_t)esize(ctx)) % 16)
+    return fail(MOA_ERR_INVALID_ARG, "k_new/v_new and batch stride must be 16-byte aligned");
+  DeviceGuard dg(ctx->device);
+  moa::CacheArgs c{};
+  c.k = k_new; c.v = v_new; c.row_stride = kv_batch_stride; c.k_cache = p.k_cache; c.v_cache = p.v_cache;
+  c.rows_per_seq = p.rows_per_seq; c.d_g_off = p.d_g_off; c.d_win_g = p.d_win_g;
+  c.ngl = ctx->ngl; c.d = ctx->d; c.n_sink = p.n_sink; c.batch = batch; c.N_or_pos = pos;
+  c.esize = (int)esize(ctx);
+  c.max_region_rows = (int64_t)p.n_sink + *std::max_element(p.win_g.begin(), p.win_g.end());
+  int e = moa::launch_kv_append(c, stream);
+  if (e) return cuda_fail((cudaError_t)e, "kv_append launch");
+  p.next_pos = pos + 1;
+  return ok();
+}
+
+static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const void *k_new,
+                                const void *v_new, void *o, int64_t q_batch_stride,
+                                int64_t kv_batch_stride, int64_t o_batch_stride, int batch,
+                                int64_t pos, float scale, float *lse_out, void *workspace,
+                                size_t ws_bytes, moa_stream_t stream, bool fused) {
+  moa_status st = check_launch_common(ctx, layer, batch);
+  if (st) return st;
+  LayerPlan &p = ctx->layers[layer];
+  if (!q || !o) return fail(MOA_ERR_INVALID_ARG, "q/o must be non-NULL");
+  if (fused && (!k_new || !v_new)) return fail(MOA_ERR_INVALID_ARG, "k_new/v_new must be non-NULL");
+  int64_t expect = fused ? p.next_pos : p.next_pos - 1;
+  if (pos != expect || pos < 0)
+    return fail(MOA_ERR_STATE, "decode pos=%lld but layer %d expects %lld (append before decode)",
+                (long long)pos, layer, (long long)expect);
+  const int64_t d = ctx->d;
+  if (q_batch_stride < ctx->nql * d || o_batch_stride < ctx->nql * d)
+    return fail(MOA_ERR_SHAPE, "q/o batch stride smaller than local heads * head_dim");
+  if (fused && kv_batch_stride < ctx->ngl * d) return fail(MOA_ERR_SHAPE, "kv_batch_stride too small");
+  const int64_t es = (int64_t)esize(ctx);
+  if (!aligned16(q) || !aligned16(o) || (q_batch_stride * es) % 16 || (o_batch_stride * es) % 16 ||
+      (fused && (!aligned16(k_new) || !aligned16(v_new) || (kv_batch_stride * es) % 16)))
+    return fail(MOA_ERR_INVALID_ARG, "decode pointers and batch strides must be 16-byte aligned");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(MOA_ERR_INVALID_ARG, "scale must be finite > 0");
+  const int n_chunks = (int)(p.chunks.size() / 3);
+  size_t need = moa::decode_ws_bytes(batch, n_chunks, ctx->G, ctx->d);
+  if (!workspace || ws_bytes < need)
+    return fail(MOA_ERR_OOM, "workspace of %zu bytes < %zu needed", ws_bytes, need);
+  if (!aligned16(workspace)) return fail(MOA_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
+  DeviceGuard dg(ctx->device);
+  moa::DecodeArgs a{};
+  a.q = q; a.o = o; a.q_batch_stride = q_batch_stride; a.o_batch_stride = o_batch_stride;
+  a.k_new = fused ? k_new : nullptr; a.v_new = fused ? v_new : nullptr; a.kv_batch_stride = kv_batch_stride;
+  a.k_cache = p.k_cache; a.v_cache = p.v_cache; a.rows_per_seq = p.rows_per_seq;
+  a.d_g_off = p.d_g_off; a.d_win_g = p.d_win_g; a.d_win_q = p.d_win_q;
+  a.d_chunks = p.d_chunks; a.d_g_chunk = p.d_g_chunk; a.n_chunks = n_chunks;
+  a.max_chunks_per_group = p.max_chunks_per_group;
+  a.ngl = ctx->ngl; a.G = ctx->G; a.d = ctx->d; a.n_sink = p.n_sink; a.batch = batch;
+  a.pos = pos; a.scale = scale; a.lse = lse_out;
+  a.ws_part = static_cast<float *>(workspace);
+  a.counters = p.d_counters;
+  int e = moa::launch_decode(a, ctx->dtype, fused, stream);
+  if (e) return cuda_fail((cudaError_t)e, "decode launch");
+  if (fused) p.next_pos = pos + 1;
+  return ok();
+}
+
+moa_status moa_decode_step(moa_ctx *ctx, int layer, const void *q, void *o,
+                           int64_t q_batch_stride, int64_t o_batch_stride, int batch,
+                           int64_t pos, float scale, float *lse_out, void *workspace,
+                           size_t ws_bytes, moa_stream_t stream) {
+  return decode_common(ctx, layer, q, nullptr, nullptr, o, q_batch_stride, 0, o_batch_stride,
+                       batch, pos, scale, lse_out, workspace, ws_bytes, stream, false);
+}
+
+moa_status moa_decode_step_fused(moa_ctx *ctx, int layer, const void *q, const void *k_new,
+                                 const void *v_new, void *o, int64_t q_batch_stride,
+                                 int64_t kv_batch_stride, int64_t o_batch_stride, int batch,
+                                 int64_t pos, float scale, float *lse_out, void *workspace,
+                                 size_t ws_bytes, moa_stream_t stream) {
+  return decode_common(ctx, layer, q, k_new, v_new, o, q_batch_stride, kv_batch_stride,
+                       o_batch_stride, batch, pos, scale, lse_out, workspace, ws_bytes, stream, true);
+}
+
+// ---------------------------------------------------------------------------------------------
+// introspection
+// ---------------------------------------------------------------------------------------------
+
+moa_status moa_get_window(const moa_ctx *ctx, int layer, int q_head_local, int32_t *window) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (!window || q_head_local < 0 || q_head_local >= ctx->nql) return fail(MOA_ERR_INVALID_ARG, "bad head/ptr");
+  *window = ctx->layers[layer].win_q[q_head_local];
+  return ok();
+}
+
+moa_status moa_get_group_window(const moa_ctx *ctx, int layer, int group_local, int32_t *w_g) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (!w_g || group_local < 0 || group_local >= ctx->ngl) return fail(MOA_ERR_INVALID_ARG, "bad group/ptr");
+  *w_g = ctx->layers[layer].win_g[group_local];
+  return ok();
+}
+
+moa_status moa_slot_of(const moa_ctx *ctx, int layer, int group_local, int64_t pos, int64_t *slot) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (!slot || group_local < 0 || group_local >= ctx->ngl || pos < 0)
+    return fail(MOA_ERR_INVALID_ARG, "bad group/pos/ptr");
+  const LayerPlan &p = ctx->layers[layer];
+  *slot = moa::slot_of(pos, p.n_sink, p.win_g[group_local]);
+  return ok();
+}
+
+moa_status moa_cache_region(const moa_ctx *ctx, int layer, int b, int group_local,
+                            int64_t *row_offset, int64_t *rows) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (b < 0 || group_local < 0 || group_local >= ctx->ngl) return fail(MOA_ERR_INVALID_ARG, "bad b/group");
+  const LayerPlan &p = ctx->layers[layer];
+  if (row_offset) *row_offset = (int64_t)b * p.rows_per_seq + p.g_off[group_local];
+  if (rows) *rows = (int64_t)p.n_sink + p.win_g[group_local];
+  return ok();
+}
+
+moa_status moa_prefill_tiles(const moa_ctx *ctx, int layer, int q_head_local, int q_tile,
+                             int32_t *tiles, uint8_t *edge, int max_tiles, int32_t *n_tiles) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  const LayerPlan &p = ctx->layers[layer];
+  int nqt = (int)((p.N + moa::kTile - 1) / moa::kTile);
+  if (q_head_local < 0 || q_head_local >= ctx->nql || q_tile < 0 || q_tile >= nqt || !n_tiles)
+    return fail(MOA_ERR_INVALID_ARG, "bad head/tile/ptr");
+  int64_t i0 = (int64_t)q_tile * moa::kTile;
+  int64_t i1 = std::min<int64_t>(p.N, i0 + moa::kTile) - 1;
+  int W = p.win_q[q_head_local];
+  moa::TileRanges r = moa::kv_tile_ranges(i0, i1, W, p.n_sink);
+  int n = r.count();
+  *n_tiles = n;
+  for (int k2 = 0; k2 < n && k2 < max_tiles; ++k2) {
+    int t = r.at(k2);
+    if (tiles) tiles[k2] = t;
+    if (edge) edge[k2] = moa::kv_tile_full(i0, i1, t, W, p.n_sink) ? 0 : 1;
+  }
+  return ok();
+}
+
+moa_status moa_prefill_items(const moa_ctx *ctx, int layer, int32_t *items, int max_items,
+                             int32_t *n_items) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (!n_items) return fail(MOA_ERR_INVALID_ARG, "n_items is NULL");
+  const LayerPlan &p = ctx->layers[layer];
+  int n = (int)(p.items.size() / 2);
+  *n_items = n;
+  if (items)
+    for (int i = 0; i < n && i < max_items; ++i) {
+      items[2 * i] = p.items[2 * i];
+      items[2 * i + 1] = p.items[2 * i + 1];
+    }
+  return ok();
+}
+
+moa_status moa_decode_chunks(const moa_ctx *ctx, int layer, int32_t *chunks, int max_chunks,
+                             int32_t *n_chunks) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (!n_chunks) return fail(MOA_ERR_INVALID_ARG, "n_chunks is NULL");
+  const LayerPlan &p = ctx->layers[layer];
+  int n = (int)(p.chunks.size() / 3);
+  *n_chunks = n;
+  if (chunks)
+    for (int i = 0; i < n && i < max_chunks; ++i)
+      for (int j = 0; j < 3; ++j) chunks[3 * i + j] = p.chunks[3 * i + j];
+  return ok();
+}
+
+moa_status moa_next_pos(const moa_ctx *ctx, int layer, int64_t *pos) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (!pos) return fail(MOA_ERR_INVALID_ARG, "pos is NULL");
+  *pos = ctx->layers[layer].next_pos;
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+// moa_internal.h -- host runtime structures and the index arithmetic shared by
+// the host planner and the device kernels of libmoa.so (one product; the
+// oracle shares nothing with it).
+//
+// Mask (PAPER.md:178 sinks; reading c3 window incl. the query itself):
+//   key j visible to query i  <=>  0 <= j <= i  and  (j < s  or  i - j < W)
+// Ring slot of position p (reading c13):
+//   p < s ? p : s + (p - s) mod W_g
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/moa.h"
+
+#if defined(__CUDACC__)
+#define MOA_HD __host__ __device__ __forceinline__
+#else
+#define MOA_HD inline
+#endif
+
+namespace moa {
+
+constexpr int kTile = MOA_TILE;  // prefill q/kv tile (rows)
+
+// ------------------------------------------------------------------------------------------
+// Prefill block-skip schedule.  For q rows [i0, i1] (i1 inclusive, the last
+// REAL row of the tile) of a head with window W and s sinks the visited kv tiles are
+//   sink tiles   [0, ceil(min(s, i1+1) / T))
+//   window tiles [floor(max(0, i0-W+1) / T), floor(i1 / T) + 1)    (empty if W == 0)
+// merged into two disjoint ascending ranges [a0,a1) U [b0,b1).
+// ------------------------------------------------------------------------------------------
+struct TileRanges {
+  int a0, a1, b0, b1;
+  MOA_HD int count() const { return (a1 - a0) + (b1 - b0); }
+  MOA_HD int at(int k) const { return k < (a1 - a0) ? a0 + k : b0 + (k - (a1 - a0)); }
+};
+
+MOA_HD TileRanges kv_tile_ranges(int64_t i0, int64_t i1, int W, int s) {
+  TileRanges r;
+  int64_t nsink_keys = s < i1 + 1 ? (int64_t)s : i1 + 1;
+  r.a0 = 0;
+  r.a1 = (int)((nsink_keys + kTile - 1) / kTile);
+  if (W > 0) {
+    int64_t lo = i0 - W + 1;
+    if (lo < 0) lo = 0;
+    r.b0 = (int)(lo / kTile);
+    r.b1 = (int)(i1 / kTile) + 1;
+    if (r.b0 < r.a1) r.b0 = r.a1;
+    if (r.b1 < r.b0) r.b1 = r.b0;
+  } else {
+    r.b0 = r.b1 = r.a1;
+  }
+  return r;
+}
+
+// A kv tile needs no mask iff every (row, key) pair of the tile is visible:
+// all keys <= the first row (causal) and every non-sink key of the tile is
+// inside the window of the last row (the farthest pair).
+MOA_HD bool kv_tile_full(int64_t i0, int64_t i1, int t, int W, int s) {
+  int64_t j0 = (int64_t)t * kTile, j1 = j0 + kTile - 1;
+  if (j1 > i0) return false;
+  int64_t jn = j0 > s ? j0 : (int64_t)s;  // first non-sink key of the tile
+  return jn > j1 || (i1 - jn < W);
+}
+
+// Ring arithmetic (reading c13).
+MOA_HD int64_t slot_of(int64_t p, int s, int Wg) {
+  if (p < s) return p;
+  if (Wg <= 0) return -1;
+  return s + (p - s) % Wg;
+}
+
+// Position held by row `r` of a group region after position p was written
+// (-1 if the row holds nothing yet).  Sink rows hold r (if r <= p); ring row
+// k = r - s holds q = p - ((p - s - k) mod W_g) if q >= s.
+MOA_HD int64_t pos_of_row(int64_t r, int64_t p, int s, int Wg) {
+  if (r < s) return r <= p ? r : -1;
+  if (p < s) return -1;
+  int64_t k = r - s;
+  int64_t m = (p - s - k) % Wg;
+  if (m < 0) m += Wg;
+  int64_t q = p - m;
+  return q >= s ? q : -1;
+}
+
+// ------------------------------------------------------------------------------------------
+// Host runtime
+// ------------------------------------------------------------------------------------------
+struct LayerPlan {
+  bool set = false;
+  int n_sink = 0;
+  int64_t N = 0;
+  std::vector<int32_t> win_q;    // local q-heads
+  std::vector<int32_t> win_g;    // local groups: W_g
+  std::vector<int64_t> g_off;    // row offset of group g inside one sequence's region
+  int64_t rows_per_seq = 0;      // sum_g (s + W_g)
+  std::vector<int32_t> items;    // prefill work items: (h_local, q_tile) pairs, LPT order
+  std::vector<int32_t> chunks;   // decode chunks: (g_local, row_begin, row_end) triples
+  std::vector<int32_t> g_chunk;  // first chunk of each group, size ngl + 1
+  int chunk_rows = 0;
+  int max_chunks_per_group = 0;
+  // device copies of the tables (one allocation)
+  void *d_tables = nullptr;
+  const int32_t *d_win_q = nullptr;
+  const int32_t *d_win_g = nullptr;
+  const int64_t *d_g_off = nullptr;
+  const int32_t *d_items = nullptr;
+  const int32_t *d_chunks = nullptr;
+  const int32_t *d_g_chunk = nullptr;
+  int *d_counters = nullptr;     // [max_batch, ngl] decode combine tickets (zeroed at upload)
+  // bound cache
+  void *k_cache = nullptr;
+  void *v_cache = nullptr;
+  int bound_batch = 0;
+  int64_t next_pos = -1;  // next position to append; -1 = nothing written
+};
+
+}  // namespace moa
+
+struct moa_ctx {
+  int device = -1;
+  moa_dtype dtype = MOA_BF16;
+  int L = 0, Hq = 0, Hkv = 0, G = 1, d = 128, max_batch = 1;
+  int g0 = 0, g1 = 0, ngl = 0, nql = 0;  // local groups [g0, g1), counts
+  std::vector<moa::LayerPlan> layers;
+};
+
+namespace moa {
+
+// ---- launchers (kernels/*.cu); all return cudaError_t as int ----------------------------
+struct PrefillArgs {
+  const void *q, *k, *v;
+  void *o;
+  int64_t q_row_stride, kv_row_stride, o_row_stride;
+  int batch;
+  int64_t N;
+  float scale;
+  float *lse;
+  int n_sink;
+  int nql, G, d;
+  const int32_t *d_win_q;
+  const int32_t *d_items;
+  int n_items;
+};
+int launch_prefill_f32(const PrefillArgs &a, void *stream);
+int launch_prefill_bf16_tc(const PrefillArgs &a, void *stream);
+
+struct CacheArgs {
+  const void *k, *v;  // prompt K/V (fill) or new token (append)
+  int64_t row_stride; // fill: token row stride; append: batch stride
+  void *k_cache, *v_cache;
+  int64_t rows_per_seq;
+  const int64_t *d_g_off;
+  const int32_t *d_win_g;
+  int ngl, d, n_sink, batch;
+  int64_t N_or_pos;
+  int esize;
+  int64_t max_region_rows;  // n_sink + max_g W_g
+};
+int launch_cache_fill(const CacheArgs &a, void *stream);
+int launch_kv_append(const CacheArgs &a, void *stream);
+
+struct DecodeArgs {
+  const void *q;
+  void *o;
+  int64_t q_batch_stride, o_batch_stride;
+  const void *k_new, *v_new;  // fused append (nullable)
+  int64_t kv_batch_stride;
+  const void *k_cache, *v_cache;
+  int64_t rows_per_seq;
+  const int64_t *d_g_off;
+  const int32_t *d_win_g, *d_win_q;
+  const int32_t *d_chunks, *d_g_chunk;
+  int n_chunks, max_chunks_per_group;
+  int ngl, G, d, n_sink, batch;
+  int64_t pos;
+  float scale;
+  float *lse;
+  float *ws_part;       // [batch, n_chunks, G, d + 1] split partials (o, lse2)
+  int *counters;        // [max_batch, ngl] last-CTA-done tickets (library-owned, self-resetting)
+};
+int launch_decode(const DecodeArgs &a, moa_dtype dtype, bool fused, void *stream);
+
+size_t decode_ws_bytes(int batch, int n_chunks, int G, int d);
+
+}  // namespace moa

@@ -1,0 +1,223 @@
+"""Thin Python front-end over the C ABI (include/moa.h).
+
+``MoAContext`` wraps one ``moa_ctx``: it turns torch tensors into device
+pointers, element strides and the current CUDA stream, calls the library
+function of the same name and raises ``MoAError`` on a non-OK status.  Every
+step of the hot path runs in libmoa.so's CUDA kernels; PyTorch only supplies
+memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_float, c_int32, c_int64, c_size_t, c_uint8, c_void_p
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import MOA_BF16, MOA_FP32, MOA_TILE, MoAError, check  # noqa: F401
+
+_DT = {torch.bfloat16: MOA_BF16, torch.float32: MOA_FP32}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    if stream is None:
+        if not torch.cuda.is_available():
+            return None
+        stream = torch.cuda.current_stream()
+    return c_void_p(stream.cuda_stream)
+
+
+def resolve_spans(alpha: Sequence[float], beta: Sequence[float], N: int, n_sink: int):
+    """Elastic rules -> windows through ``moa_resolve_spans`` (Eq. 2)."""
+    n = len(alpha)
+    a = (c_float * n)(*alpha)
+    b = (c_float * n)(*beta)
+    w = (c_int32 * n)()
+    check(_lib.lib().moa_resolve_spans(a, b, n, int(N), int(n_sink), w), "moa_resolve_spans")
+    return list(w)
+
+
+class MoAContext:
+    """One context per (process, device): span tables, cache layout, launches."""
+
+    def __init__(self, num_layers: int, num_q_heads: int, num_kv_heads: int, head_dim: int,
+                 max_batch: int, dtype: torch.dtype = torch.bfloat16, device: int = 0,
+                 kv_group_begin: int = 0, kv_group_end: Optional[int] = None):
+        self.lib = _lib.lib()
+        self.dtype = dtype
+        self.device = device
+        self.L, self.Hq, self.Hkv, self.d = num_layers, num_q_heads, num_kv_heads, head_dim
+        self.G = num_q_heads // num_kv_heads
+        self.g0 = kv_group_begin
+        self.g1 = num_kv_heads if kv_group_end is None else kv_group_end
+        self.nql = (self.g1 - self.g0) * self.G
+        self.ngl = self.g1 - self.g0
+        ctx = c_void_p()
+        check(self.lib.moa_create(byref(ctx), device, _DT[dtype], num_layers, num_q_heads, num_kv_heads,
+                                  head_dim, max_batch, self.g0, self.g1), "moa_create")
+        self.ctx = ctx
+        self._cache = None
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.moa_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- planning ---------------------------------------------------------------------
+    def set_spans(self, layer: int, windows: Sequence[int], n_sink: int, N: int):
+        w = (c_int32 * len(windows))(*[int(x) for x in windows])
+        check(self.lib.moa_set_spans(self.ctx, layer, w, int(n_sink), int(N)), "moa_set_spans")
+
+    def cache_bytes(self, batch: int):
+        k, v = c_size_t(), c_size_t()
+        check(self.lib.moa_cache_bytes(self.ctx, batch, byref(k), byref(v)), "moa_cache_bytes")
+        return k.value, v.value
+
+    def layer_cache_bytes(self, layer: int, batch: int):
+        k, v = c_size_t(), c_size_t()
+        check(self.lib.moa_layer_cache_bytes(self.ctx, layer, batch, byref(k), byref(v)), "moa_layer_cache_bytes")
+        return k.value, v.value
+
+    def workspace_bytes(self, batch: int) -> int:
+        b = c_size_t()
+        check(self.lib.moa_workspace_bytes(self.ctx, batch, byref(b)), "moa_workspace_bytes")
+        return b.value
+
+    def layer_offset(self, layer: int, batch: int) -> int:
+        b = c_size_t()
+        check(self.lib.moa_layer_offset(self.ctx, layer, batch, byref(b)), "moa_layer_offset")
+        return b.value
+
+    def window(self, layer: int, h: int) -> int:
+        w = c_int32()
+        check(self.lib.moa_get_window(self.ctx, layer, h, byref(w)), "moa_get_window")
+        return w.value
+
+    def group_window(self, layer: int, g: int) -> int:
+        w = c_int32()
+        check(self.lib.moa_get_group_window(self.ctx, layer, g, byref(w)), "moa_get_group_window")
+        return w.value
+
+    def slot_of(self, layer: int, g: int, pos: int) -> int:
+        s = c_int64()
+        check(self.lib.moa_slot_of(self.ctx, layer, g, int(pos), byref(s)), "moa_slot_of")
+        return s.value
+
+    def cache_region(self, layer: int, b: int, g: int):
+        off, rows = c_int64(), c_int64()
+        check(self.lib.moa_cache_region(self.ctx, layer, b, g, byref(off), byref(rows)), "moa_cache_region")
+        return off.value, rows.value
+
+    def prefill_tiles(self, layer: int, h: int, q_tile: int):
+        n = c_int32()
+        check(self.lib.moa_prefill_tiles(self.ctx, layer, h, q_tile, None, None, 0, byref(n)), "moa_prefill_tiles")
+        tiles = (c_int32 * max(1, n.value))()
+        edge = (c_uint8 * max(1, n.value))()
+        check(self.lib.moa_prefill_tiles(self.ctx, layer, h, q_tile, tiles, edge, n.value, byref(n)),
+              "moa_prefill_tiles")
+        return list(tiles)[: n.value], [bool(e) for e in list(edge)[: n.value]]
+
+    def prefill_items(self, layer: int):
+        n = c_int32()
+        check(self.lib.moa_prefill_items(self.ctx, layer, None, 0, byref(n)), "moa_prefill_items")
+        buf = (c_int32 * max(1, 2 * n.value))()
+        check(self.lib.moa_prefill_items(self.ctx, layer, buf, n.value, byref(n)), "moa_prefill_items")
+        return [(buf[2 * i], buf[2 * i + 1]) for i in range(n.value)]
+
+    def decode_chunks(self, layer: int):
+        n = c_int32()
+        check(self.lib.moa_decode_chunks(self.ctx, layer, None, 0, byref(n)), "moa_decode_chunks")
+        buf = (c_int32 * max(1, 3 * n.value))()
+        check(self.lib.moa_decode_chunks(self.ctx, layer, buf, n.value, byref(n)), "moa_decode_chunks")
+        return [tuple(buf[3 * i: 3 * i + 3]) for i in range(n.value)]
+
+    def next_pos(self, layer: int) -> int:
+        p = c_int64()
+        check(self.lib.moa_next_pos(self.ctx, layer, byref(p)), "moa_next_pos")
+        return p.value
+
+    # ---- memory --------------------------------------------------------------------------
+    def bind_cache(self, k_cache: torch.Tensor, v_cache: torch.Tensor, batch: int):
+        check(self.lib.moa_bind_cache(self.ctx, _ptr(k_cache), _ptr(v_cache), batch), "moa_bind_cache")
+        self._cache = (k_cache, v_cache)
+        self._bound_batch = batch
+
+    def bind_layer_cache(self, layer: int, k_cache: torch.Tensor, v_cache: torch.Tensor, batch: int):
+        check(self.lib.moa_bind_layer_cache(self.ctx, layer, _ptr(k_cache), _ptr(v_cache), batch),
+              "moa_bind_layer_cache")
+
+    def alloc_cache(self, batch: int):
+        """Allocate (with torch) and bind the cache of all layers; returns (K, V) byte tensors."""
+        kb, vb = self.cache_bytes(batch)
+        dev = torch.device("cuda", self.device)
+        k = torch.empty(kb, dtype=torch.uint8, device=dev)
+        v = torch.empty(vb, dtype=torch.uint8, device=dev)
+        self.bind_cache(k, v, batch)
+        return k, v
+
+    def alloc_workspace(self, batch: int) -> torch.Tensor:
+        return torch.empty(self.workspace_bytes(batch), dtype=torch.uint8,
+                           device=torch.device("cuda", self.device))
+
+    # ---- launches ------------------------------------------------------------------------
+    @staticmethod
+    def _row_stride(t: torch.Tensor) -> int:
+        return t.stride(1)
+
+    def prefill(self, layer: int, q, k, v, o, scale: float, lse=None, workspace=None, stream=None):
+        B, N = q.shape[0], q.shape[1]
+        for t in (q, k, v, o):
+            assert t.stride(-1) == 1 and t.stride(-2) == self.d and t.stride(0) == N * t.stride(1)
+        ws = workspace
+        check(self.lib.moa_prefill(self.ctx, layer, _ptr(q), _ptr(k), _ptr(v), _ptr(o), q.stride(1), k.stride(1),
+                                   o.stride(1), B, N, float(scale), _ptr(lse), _ptr(ws),
+                                   0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
+              "moa_prefill")
+
+    def cache_fill(self, layer: int, k, v, stream=None):
+        B, N = k.shape[0], k.shape[1]
+        check(self.lib.moa_cache_fill(self.ctx, layer, _ptr(k), _ptr(v), k.stride(1), B, N, _stream(stream)),
+              "moa_cache_fill")
+
+    def kv_append(self, layer: int, k_new, v_new, pos: int, stream=None):
+        B = k_new.shape[0]
+        check(self.lib.moa_kv_append(self.ctx, layer, _ptr(k_new), _ptr(v_new), k_new.stride(0), B, int(pos),
+                                     _stream(stream)), "moa_kv_append")
+
+    def decode_step(self, layer: int, q, o, pos: int, scale: float, workspace, lse=None, stream=None):
+        B = q.shape[0]
+        check(self.lib.moa_decode_step(self.ctx, layer, _ptr(q), _ptr(o), q.stride(0), o.stride(0), B, int(pos),
+                                       float(scale), _ptr(lse), _ptr(workspace),
+                                       workspace.numel() * workspace.element_size(), _stream(stream)),
+              "moa_decode_step")
+
+    def decode_step_fused(self, layer: int, q, k_new, v_new, o, pos: int, scale: float, workspace, lse=None,
+                          stream=None):
+        B = q.shape[0]
+        check(self.lib.moa_decode_step_fused(self.ctx, layer, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(o),
+                                             q.stride(0), k_new.stride(0), o.stride(0), B, int(pos), float(scale),
+                                             _ptr(lse), _ptr(workspace),
+                                             workspace.numel() * workspace.element_size(), _stream(stream)),
+              "moa_decode_step_fused")
+
+    # ---- cache inspection (tests) --------------------------------------------------------
+    def cache_rows(self, layer: int, b: int, g: int, which: str = "k") -> torch.Tensor:
+        """The (n_sink + W_g, d) rows of region (b, g) as a view of the cache bound by
+        ``bind_cache``/``alloc_cache``."""
+        k, v = self._cache
+        buf = k if which == "k" else v
+        es = torch.tensor([], dtype=self.dtype).element_size()
+        off, rows = self.cache_region(layer, b, g)
+        start = self.layer_offset(layer, self._bound_batch) + off * self.d * es
+        return buf[start: start + rows * self.d * es].view(self.dtype).view(rows, self.d)

@@ -1,0 +1,156 @@
+"""Host runtime of libmoa.so (planning contexts, device = -1): CPU only.
+
+The span table, ring-slot arithmetic, cache layout, block-skip schedule and
+decode work list are checked exhaustively against the oracle's predicate and
+slot definitions.  No kernel is launched.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from moa_workloads import CONFIGS, rule_table
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def moa():
+    import paper_2406_14909_b200 as m
+    return m
+
+
+def test_library_exports_every_declared_symbol(moa):
+    with open(os.path.join(ROOT, "include", "moa.h")) as f:
+        hdr = f.read()
+    declared = set(re.findall(r"^\s*(?:moa_status|const char \*)\s*(moa_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 20
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2406_14909_b200", "libmoa.so"))
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(moa.EXPORTED)
+    lib.moa_version.restype = ctypes.c_char_p
+    assert b"sm_100a" in lib.moa_version()
+
+
+def test_resolve_spans_matches_oracle_on_rule_tables(moa):
+    for name in ("C2", "C3", "C4", "C5"):
+        cfg, t = CONFIGS[name], rule_table(name)
+        for l in range(cfg.layers):
+            w = moa.resolve_spans(t["alpha"][l], t["beta"][l], cfg.N, cfg.n_sink)
+            ref = [oracle.window_of(oracle.span_of(a, b, cfg.N), cfg.n_sink)
+                   for a, b in zip(t["alpha"][l], t["beta"][l])]
+            assert w == ref, (name, l)
+    # printed examples
+    assert moa.resolve_spans([64, -2048, 0], [0.5, 0.0, 1.0], 8192, 64) == [4096, 0, 8128]
+
+
+def _ctx(moa, L=1, Hq=4, Hkv=2, d=128, B=2, g0=0, g1=None):
+    return moa.MoAContext(L, Hq, Hkv, d, B, device=-1, kv_group_begin=g0, kv_group_end=g1)
+
+
+def test_slot_and_region_layout(moa):
+    s = 4
+    W = [0, 3, 7, 7, 16, 2, 1, 5]
+    c = _ctx(moa, Hq=8, Hkv=4, B=3)
+    c.set_spans(0, W, s, 64)
+    wg = oracle.group_windows(W, 2)
+    assert [c.group_window(0, g) for g in range(4)] == list(wg)
+    for g in range(4):
+        for p in range(200):
+            want = oracle.slot_of(p, s, int(wg[g]))
+            assert c.slot_of(0, g, p) == (-1 if want is None else want)
+    # regions tile [0, B * rows_per_seq) without overlap
+    spans = sorted(c.cache_region(0, b, g) for b in range(3) for g in range(4))
+    pos = 0
+    for off, rows in spans:
+        assert off == pos
+        pos += rows
+    assert pos == 3 * sum(s + int(x) for x in wg)
+    kb, vb = c.cache_bytes(3)
+    assert kb == vb == ((pos * 128 * 2 + 255) // 256) * 256
+
+
+def test_sharded_context_keeps_its_groups(moa):
+    W = list(range(1, 17))
+    full = _ctx(moa, Hq=16, Hkv=4)
+    full.set_spans(0, W, 2, 100)
+    shard = _ctx(moa, Hq=16, Hkv=4, g0=1, g1=3)
+    shard.set_spans(0, W, 2, 100)
+    assert [shard.window(0, h) for h in range(8)] == W[4:12]
+    assert [shard.group_window(0, g) for g in range(2)] == [full.group_window(0, 1), full.group_window(0, 2)]
+
+
+@pytest.mark.parametrize("N,s", [(300, 0), (300, 3), (300, 64), (257, 130), (128, 5), (40, 2)])
+def test_prefill_tile_schedule_is_exact(moa, N, s):
+    """Visited kv tiles == tiles holding >= 1 visible (row, key) pair of the
+    q tile; EDGE flag == not every pair of the tile visible (brute force)."""
+    T = 128
+    windows = [1, 2, 63, 128, 129, 200, N, N + 50] + ([0] if s else [5])
+    c = _ctx(moa, Hq=len(windows), Hkv=len(windows), B=1)
+    c.set_spans(0, windows, s, N)
+    nqt = (N + T - 1) // T
+    for h, W in enumerate(windows):
+        for qt in range(nqt):
+            rows = range(qt * T, min(N, qt * T + T))
+            vis_tiles = set()
+            full = {}
+            for t in range((N + T - 1) // T + 1):
+                keys = range(t * T, t * T + T)
+                pairs = [oracle.visible(i, j, W, s) for i in rows for j in keys]
+                if any(pairs):
+                    vis_tiles.add(t)
+                    full[t] = all(pairs)
+            tiles, edge = c.prefill_tiles(0, h, qt)
+            assert sorted(tiles) == sorted(vis_tiles), (h, W, qt)
+            assert len(tiles) == len(set(tiles))
+            for t, e in zip(tiles, edge):
+                assert e == (not full[t]), (h, W, qt, t)
+
+
+def test_prefill_items_lpt_permutation(moa):
+    N, s = 1000, 64
+    windows = [5, 900, 300, 64, 1000, 0]
+    c = _ctx(moa, Hq=6, Hkv=6, B=1)
+    c.set_spans(0, windows, s, N)
+    items = c.prefill_items(0)
+    nqt = (N + 127) // 128
+    assert sorted(items) == [(h, q) for h in range(6) for q in range(nqt)]
+    counts = [len(c.prefill_tiles(0, h, q)[0]) for h, q in items]
+    assert counts == sorted(counts, reverse=True)
+
+
+def test_decode_chunks_cover_each_region_once(moa):
+    W = [10, 700, 3000, 1, 64, 64, 2048, 5]
+    s = 64
+    c = _ctx(moa, Hq=8, Hkv=4, B=8)
+    c.set_spans(0, W, s, 4096)
+    wg = oracle.group_windows(W, 2)
+    chunks = c.decode_chunks(0)
+    for g in range(4):
+        cov = sorted((r0, r1) for gg, r0, r1 in chunks if gg == g)
+        assert cov[0][0] == 0 and cov[-1][1] == s + wg[g]
+        for (a0, a1), (b0, b1) in zip(cov, cov[1:]):
+            assert a1 == b0 and a0 < a1
+    gs = [gg for gg, *_ in chunks]
+    assert gs == sorted(gs)   # chunks of a group are contiguous (combine ranges)
+
+
+def test_validation_errors(moa):
+    from paper_2406_14909_b200 import MoAError
+    c = _ctx(moa)
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_spans(0, [0, 1, 2, 3], 0, 10)          # empty softmax row (reading c7)
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_spans(0, [-1, 1, 2, 3], 4, 10)
+    with pytest.raises(MoAError, match="SHAPE"):
+        _ctx(moa, d=96)
+    with pytest.raises(MoAError, match="UNSUPPORTED"):
+        _ctx(moa, Hq=6, Hkv=2)
+    with pytest.raises(MoAError, match="STATE"):
+        c.cache_bytes(1)                              # spans unset
+    c.set_spans(0, [1, 2, 3, 4], 4, 10)
+    assert c.next_pos(0) == -1
