@@ -81,3 +81,98 @@ def test_prefill_fp32_structured(moa):
         ctx, o, lse, _ = _prefill(moa, q, k, v, W, s, torch.float32, scale=1.0)
         O, L = oracle.prefill(f64(q), f64(k), f64(v), W, s, 1.0)
         assert np.abs(f64(o) - O).max() < 1e-5
+
+
+# ----------------------------------------------------------------------------------------
+# bf16: the tcgen05 tensor-core kernel
+# ----------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("N", [100, 300, 513])
+def test_prefill_bf16_small_full_compare(moa, d, N):
+    B, Hq, Hkv, s = 2, 6, 3, 4
+    W = [0, 1, 130, 257, 17, N + 3]
+    q = normal((B, N, Hq, d), 201, torch.bfloat16)
+    k = normal((B, N, Hkv, d), 202, torch.bfloat16)
+    v = normal((B, N, Hkv, d), 203, torch.bfloat16)
+    ctx, o, lse, scale = _prefill(moa, q, k, v, W, s, torch.bfloat16)
+    O, L = oracle.prefill(f64(q), f64(k), f64(v), W, s, scale)
+    err = np.abs(f64(o) - O)
+    assert np.isfinite(f64(o)).all()
+    assert err.max() < 2e-2, (err.max(), np.unravel_index(err.argmax(), err.shape))
+    assert np.abs(f64(lse) - L).max() < 2e-3
+    check_cache_image(ctx, 0, k, v, N - 1, W, s, B, 2)
+
+
+def test_prefill_bf16_structured(moa):
+    B, N, H, d, s = 1, 640, 4, 128, 64
+    W = [16, 200, 300, 640]
+    u = torch.zeros(d)
+    u[0] = 1.0
+    for sink_score in (12.0, -12.0):
+        spike = (torch.arange(N) % 16 == 0).float() * 8.0
+        k = (spike[None, :, None, None] * u).expand(B, N, H, d).clone()
+        k[:, :s] = sink_score * u
+        k = (k + 0.01 * normal((B, N, H, d), 5)).to(torch.bfloat16)
+        v = normal((B, N, H, d), 6, torch.bfloat16)
+        q = u.expand(B, N, H, d).clone().to(torch.bfloat16)
+        ctx, o, lse, _ = _prefill(moa, q, k, v, W, s, torch.bfloat16, scale=1.0)
+        O, L = oracle.prefill(f64(q), f64(k), f64(v), W, s, 1.0)
+        assert np.abs(f64(o) - O).max() < 2e-2, sink_score
+
+
+def _sample_rows(B, Hq, N, s, W, rng, n_rand=24):
+    rows = []
+    for b in sorted(set([0, B - 1])):
+        for h in range(Hq):
+            base = {0, s - 1, s, W[h] - 1, W[h], W[h] + 1, N - 1, N - 2, 127, 128}
+            base |= set(int(x) for x in rng.integers(0, N, n_rand // 4))
+            rows += [(b, h, i) for i in sorted(base) if 0 <= i < N]
+    return rows
+
+
+def _full_layer_prefill(moa, name, layer, batch=None):
+    cfg = CONFIGS[name]
+    dev = torch.device("cuda")
+    B = cfg.batch if batch is None else batch
+    t = rule_table(name)
+    W = moa.resolve_spans(t["alpha"][layer], t["beta"][layer], cfg.N, cfg.n_sink)
+    q, k, v = prefill_qkv(cfg, layer, batch=B, device=dev)
+    ctx = moa.MoAContext(1, cfg.hq, cfg.hkv, cfg.head_dim, B, dtype=torch.bfloat16)
+    ctx.set_spans(0, W, cfg.n_sink, cfg.N)
+    ctx.alloc_cache(B)
+    o = torch.empty_like(q)
+    lse = torch.empty(B, cfg.hq, cfg.N, dtype=torch.float32, device=dev)
+    scale = 1 / math.sqrt(cfg.head_dim)
+    ctx.prefill(0, q, k, v, o, scale, lse)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(layer)
+    rows = _sample_rows(B, cfg.hq, cfg.N, cfg.n_sink, W, rng)
+    bs = sorted(set(r[0] for r in rows))
+    qs, ks, vs = f64(q[bs]), f64(k[bs]), f64(v[bs])
+    remap = {b: i for i, b in enumerate(bs)}
+    O, L = oracle.prefill_rows(qs, ks, vs, W, cfg.n_sink, scale, [(remap[b], h, i) for b, h, i in rows])
+    got = np.stack([f64(o[b, i, h]) for b, h, i in rows])
+    gl = np.array([float(lse[b, h, i]) for b, h, i in rows])
+    assert np.abs(got - O).max() < 2e-2
+    assert np.abs(gl - L).max() < 2e-3
+    # the cache fill of the same call, bitwise, for the sampled sequences
+    wg = oracle.group_windows(W, cfg.group)
+    img = oracle.cache_image(bits(k[bs]), bits(v[bs]), cfg.N - 1, wg, cfg.n_sink)
+    for bi, b in enumerate(bs):
+        for g in range(cfg.hkv):
+            Ki, Vi, valid = img[(bi, g)]
+            assert np.array_equal(bits(ctx.cache_rows(0, b, g, "k"))[valid], Ki[valid])
+            assert np.array_equal(bits(ctx.cache_rows(0, b, g, "v"))[valid], Vi[valid])
+
+
+def test_c2_full_layer_prefill(moa):
+    _full_layer_prefill(moa, "C2", 20)
+
+
+def test_c3_gqa_prefill_slice(moa):
+    _full_layer_prefill(moa, "C3", 9, batch=2)
+
+
+def test_c4_full_layer_prefill(moa):
+    _full_layer_prefill(moa, "C4", 33)
