@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""MoA hot-path benchmark (BASELINE.json metric: decode + prefill tokens/s, % roofline).
+
+One step = one pass of the whole hot path over one batch of the C2 workload
+(configs[1], Vicuna-7B attention shape): span resolution is done once at
+setup; the timed step is the prefill of all 32 layers (tcgen05 kernel + cache
+fill, N = 4096, B = 8) followed by 512 decode tokens x 32 layers (fused
+append + split-KV decode + combine, one launch per layer-token).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): every rank serves its own batch of 8
+sequences (data parallel over independent sequences, no collective on the
+data path) -> "scaling": "weak".  Timing: barrier + synchronize on both sides,
+CUDA events on the launching stream, max over ranks.  The working set (8.6 GB
+of cache cycled over 32 layers, 268 MB per layer) exceeds the 126 MB L2, so no
+flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from moa_workloads import CONFIGS, decode_tokens, prefill_qkv, rule_table  # noqa: E402
+
+CFG = CONFIGS["C2"]
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+# --------------------------------------------------------------------------------------------
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons via NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------------------------
+def windows_all_layers(moa):
+    t = rule_table("C2")
+    return [moa.resolve_spans(t["alpha"][l], t["beta"][l], CFG.N, CFG.n_sink) for l in range(CFG.layers)]
+
+
+def algorithmic_work(windows, B, N, T, s, d, G):
+    """In-window work: prefill FLOPs = 4 d sum_{b,h} |V(h,i)| summed over i;
+    decode bytes per layer-token = sum_{b,g} min(p+1, s+W_g) * d * 2 (K,V) * 2 B + q/o/new-token bytes."""
+    def pairs(W):  # closed form of sum_i |V(h,i)| for W <= N, plain host arithmetic
+        W = min(W, N)
+        tot = W * (W + 1) // 2 + (N - W) * W
+        tot += sum(min(s, i - W + 1) for i in range(W, N)) if W > 0 else min(s, N) * N - (min(s, N) * (min(s, N) - 1)) // 2
+        return tot
+    flops = 0
+    dec_bytes = 0
+    for wl in windows:
+        flops += sum(4 * d * pairs(w) for w in wl) * B
+        wg = [max(wl[g * G:(g + 1) * G]) for g in range(len(wl) // G)]
+        rows = sum(min(N + T, s + w) for w in wg)  # ring full during decode (p >= N > s + W_g - 1)
+        dec_bytes += B * (rows * d * 2 * 2 + len(wl) * d * 2 * 2 + len(wg) * d * 2 * 2 * 2)
+    return flops, dec_bytes  # flops for all layers' prefill; bytes summed over layers for one token step
+
+
+# --------------------------------------------------------------------------------------------
+def cpu_oracle_decode_rate(seconds: float = 12.0):
+    """Oracle (fp64 numpy, single process) decode of layer 0, sequence 0, all 32 heads, for
+    consecutive positions p = N, N+1, ... until `seconds` elapse; returns tokens/s extrapolated to
+    the whole C2 decode workload (32 layers x 8 sequences) and a description."""
+    import oracle
+    import paper_2406_14909_b200 as moa
+
+    W = windows_all_layers(moa)[0]
+    d, s, N = CFG.head_dim, CFG.n_sink, CFG.N
+    g = torch.Generator().manual_seed(7)
+    hist = N + 64
+    K = torch.randn(1, hist, CFG.hkv, d, generator=g).to(torch.bfloat16).double().numpy()
+    V = torch.randn(1, hist, CFG.hkv, d, generator=g).to(torch.bfloat16).double().numpy()
+    q = torch.randn(64, 1, CFG.hq, d, generator=g).to(torch.bfloat16).double().numpy()
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds and n < 64:
+        oracle.decode(q[n], K[:, : N + n + 1], V[:, : N + n + 1], N + n, W, s, 1 / math.sqrt(d))
+        n += 1
+    dt = (time.perf_counter() - t0) / n  # seconds per (layer, sequence, token)
+    per_token_all = dt * CFG.layers * CFG.batch
+    rate = CFG.batch / per_token_all
+    return rate, {"kind": "oracle", "cores": 1,
+                  "sample": f"oracle.decode (fp64 numpy, 1 process) of layer 0, sequence 0, all {CFG.hq} heads, "
+                            f"{n} positions from p=N={N}; {dt*1e3:.1f} ms per (layer, sequence, token), "
+                            f"extrapolated to {CFG.layers} layers x {CFG.batch} sequences"}
+
+
+# --------------------------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (CPU) on the same workload/metric, bounded sample per step."""
+    if rank != 0:
+        return
+    rates = []
+    for _ in range(args.warmup):
+        cpu_oracle_decode_rate(seconds=2.0)
+    t0 = time.perf_counter()
+    desc = None
+    for _ in range(args.steps):
+        r, desc = cpu_oracle_decode_rate(seconds=8.0)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    value = float(statistics.median(rates))
+    line = {
+        "impl": "reference", "metric": "decode tokens/s", "value": value, "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(world),
+        "cpu_baseline": dict(desc, value=value, unit="tokens/s"),
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(world):
+    return {"workload": "C2: Vicuna-7B attention shape, 32 layers x 32 heads, d=128, N=4096 prefill + 512 "
+                        "decode tokens, batch 8 per GPU, MoA rule spans (mean density 0.50), 64 sinks",
+            "model": "vicuna-7b-attention (random synthetic Q/K/V)", "global_batch": CFG.batch * world,
+            "seq_len": CFG.N + CFG.decode_steps, "parallelism": f"dp{world}",
+            "l2": "no flush: working set 8.6 GB cache + 25.8 GB prefill inputs cycled over 32 layers >> 126 MB L2"}
+
+
+# --------------------------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import paper_2406_14909_b200 as moa
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    L, B, N, T, d, s = CFG.layers, CFG.batch, CFG.N, CFG.decode_steps, CFG.head_dim, CFG.n_sink
+    scale = 1 / math.sqrt(d)
+    windows = windows_all_layers(moa)
+    ctx = moa.MoAContext(L, CFG.hq, CFG.hkv, d, B, dtype=torch.bfloat16, device=local_rank)
+    for l in range(L):
+        ctx.set_spans(l, windows[l], s, N)
+    ctx.alloc_cache(B)
+    ws = ctx.alloc_workspace(B)
+    # resident inputs (distinct per layer and per rank)
+    Q, K, V = [], [], []
+    for l in range(L):
+        q, k, v = prefill_qkv(CFG, l + 1000 * rank, device=dev)
+        Q.append(q), K.append(k), V.append(v)
+    O = torch.empty_like(Q[0])
+    qd, kd, vd = decode_tokens(CFG, 1000 * rank, T, device=dev)
+    od = torch.empty(B, CFG.hq, d, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream()
+
+    n_ev = T * L
+    ev_d = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_ev)]
+    ev_p = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+
+    def step(record=False):
+        for l in range(L):
+            if record:
+                ev_p[l][0].record(stream)
+            ctx.prefill(l, Q[l], K[l], V[l], O, scale)
+            if record:
+                ev_p[l][1].record(stream)
+        ph = torch.cuda.Event(enable_timing=True)
+        ph.record(stream)
+        for t in range(T):
+            for l in range(L):
+                if record:
+                    ev_d[t * L + l][0].record(stream)
+                ctx.decode_step_fused(l, qd[t], kd[t], vd[t], od, N + t, scale, ws)
+                if record:
+                    ev_d[t * L + l][1].record(stream)
+        return ph
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    pre_ms, dec_ms, tot_ms, pk_ms, dk_ms = [], [], [], [], []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            barrier()
+            torch.cuda.synchronize()
+            e0, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ph = step(record=True)
+            e2.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            tot_ms.append(e0.elapsed_time(e2))
+            pre_ms.append(e0.elapsed_time(ph))
+            dec_ms.append(ph.elapsed_time(e2))
+            pk_ms.append(sum(a.elapsed_time(b) for a, b in ev_p))
+            dk_ms.append(sum(a.elapsed_time(b) for a, b in ev_d))
+    tot = sum(tot_ms)
+    pre = sum(pre_ms)
+    dec = sum(dec_ms)
+    if world > 1:
+        t = torch.tensor([tot, pre, dec], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot, pre, dec = t.tolist()
+    K_steps = args.steps
+    decode_tps = B * T * world * K_steps / (dec / 1e3)
+    prefill_tps = B * N * world * K_steps / (pre / 1e3)
+
+    # roofline of the dominant kernel (decode: one launch per layer-token)
+    flops, dec_bytes_per_token = algorithmic_work(windows, B, N, T, s, d, CFG.group)
+    peaks, peak_src = load_peaks()
+    dk_avg_ms = sum(dk_ms) / (K_steps * n_ev)
+    dec_bytes_per_launch = dec_bytes_per_token / L
+    achieved_gbs = dec_bytes_per_launch / (dk_avg_ms / 1e3) / 1e9
+    pk_total_s = sum(pk_ms) / 1e3 / K_steps
+    achieved_tf = flops / pk_total_s / 1e12
+    clocks = clk.summary()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+
+    # ---------------- e2e: host buffers through the public API, H2D/D2H inside the timed region
+    e2e = run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, desc = cpu_oracle_decode_rate()
+        cpu = dict(desc, value=rate, unit="tokens/s")
+
+    if rank == 0:
+        line = {
+            "metric": "decode tokens/s", "value": decode_tps, "unit": "tokens/s", "n_gpus": world,
+            "steps": K_steps, "warmup": args.warmup, "ms_per_step": tot / K_steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": config_block(world),
+            "prefill": {"value": prefill_tps, "unit": "tokens/s", "ms_per_step": pre / K_steps,
+                        "roofline": {"bound": "tensor", "achieved": achieved_tf,
+                                     "peak": peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+                                     "unit": "TFLOP/s",
+                                     "frac": achieved_tf / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
+                                     "peak_source": peak_src + ", sustained bf16",
+                                     "note": "in-window FLOPs 4*d*sum|V| over moa_prefill call time "
+                                             "(tcgen05 attention kernel + cache fill)"}},
+            "decode_ms_per_step": dec / K_steps,
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic,
+                         "kernel": "moa decode_kernel (fused append + split-KV + last-CTA combine)",
+                         "bytes_per_launch": dec_bytes_per_launch, "avg_launch_ms": dk_avg_ms,
+                         "peak_source": peak_src},
+            "e2e": e2e,
+            "gpu_launches": K_steps * (2 * L + T * L),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
+    """Decode tokens/s through MoAContext with pinned HOST inputs: every layer-token copies
+    q, k_new, v_new host->device and o device->host inside the timed region (prefill inputs of
+    one layer are staged from host per layer as well)."""
+    L, B, N, T, d = CFG.layers, CFG.batch, CFG.N, CFG.decode_steps, CFG.head_dim
+    stream = torch.cuda.current_stream()
+    hq, hk, hv = (x.cpu().pin_memory() for x in (qd, kd, vd))
+    hQ, hK, hV = (x.cpu().pin_memory() for x in (Q[0], K[0], V[0]))
+    hO = torch.empty(Q[0].shape, dtype=Q[0].dtype).pin_memory()
+    ho = torch.empty((T, L) + tuple(qd.shape[1:]), dtype=qd.dtype).pin_memory()
+    dQ, dK, dV, dO = (torch.empty_like(x) for x in (Q[0], K[0], V[0], Q[0]))
+    dq, dk, dv, do = (torch.empty(x.shape[1:], dtype=x.dtype, device=dev) for x in (qd, kd, vd, qd))
+    h2d = d2h = 0
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record(stream)
+    for l in range(L):
+        dQ.copy_(hQ, non_blocking=True), dK.copy_(hK, non_blocking=True), dV.copy_(hV, non_blocking=True)
+        h2d += 3 * hQ.numel() * 2
+        ctx.prefill(l, dQ, dK, dV, dO, scale)
+        hO.copy_(dO, non_blocking=True)
+        d2h += hO.numel() * 2
+    e1.record(stream)
+    for t in range(T):
+        for l in range(L):
+            dq.copy_(hq[t], non_blocking=True), dk.copy_(hk[t], non_blocking=True), dv.copy_(hv[t], non_blocking=True)
+            h2d += (hq[t].numel() + 2 * hk[t].numel()) * 2
+            ctx.decode_step_fused(l, dq, dk, dv, do, N + t, scale, ws)
+            ho[t, l].copy_(do, non_blocking=True)
+            d2h += do.numel() * 2
+    e2.record(stream)
+    torch.cuda.synchronize()
+    dec_ms = e1.elapsed_time(e2)
+    if world > 1:
+        x = torch.tensor([dec_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+        dec_ms = x.item()
+    return {"value": B * T * world / (dec_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "prefill_ms": e0.elapsed_time(e1), "decode_ms": dec_ms,
+            "note": "1 step; prefill inputs of one layer staged host->device per layer; per layer-token "
+                    "q/k_new/v_new H2D and o D2H from pinned memory"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group(backend)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
