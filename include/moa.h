@@ -131,7 +131,9 @@ moa_status moa_layer_cache_bytes(const moa_ctx *ctx, int layer, int batch, size_
 moa_status moa_workspace_bytes(const moa_ctx *ctx, int batch, size_t *bytes);
 
 /* Bind caller-owned device memory as the cache of every layer (layer l at
- * byte offset sum_{l'<l} layer bytes) or of one layer.  256-byte aligned. */
+ * byte offset sum_{l'<l} layer bytes) or of one layer.  256-byte aligned.
+ * Binding zero-fills the layer caches (synchronously) and resets the layer's
+ * next position to 0. */
 moa_status moa_bind_cache(moa_ctx *ctx, void *k_cache, void *v_cache, int batch);
 moa_status moa_bind_layer_cache(moa_ctx *ctx, int layer, void *k_cache, void *v_cache, int batch);
 

@@ -1,5 +1,6 @@
 // decode.cu -- MoA decode attention over the compact per-group ring cache
-// (SURVEY §8(a) a7 split-KV + a8 combine, optionally a6 append fused in).
+// (SURVEY §8(a) a7 split-KV + a8 combine, optionally a6 append fused in),
+// fp32 I/O specialisation (FFMA; the bf16 path is decode_mma.cu).
 //
 // One new query per sequence at absolute position `pos` attends over its
 // kv-group's cache region: sink rows [0, s) and ring rows [s, s + W_g)
@@ -305,11 +306,9 @@ size_t decode_ws_bytes(int batch, int n_chunks, int G, int d) {
   return (b + 255) & ~size_t(255);
 }
 
+// fp32 I/O only (config C1, 1e-5 bar); bf16 decode runs on decode_mma.cu.
 int launch_decode(const DecodeArgs &a, moa_dtype dtype, bool fused, void *stream) {
-  if (dtype == MOA_BF16) {
-    if (a.d == 128) return launch_g<__nv_bfloat16, 128>(a, fused, stream);
-    return launch_g<__nv_bfloat16, 64>(a, fused, stream);
-  }
+  if (dtype != MOA_FP32) return (int)cudaErrorInvalidValue;
   if (a.d == 128) return launch_g<float, 128>(a, fused, stream);
   return launch_g<float, 64>(a, fused, stream);
 }

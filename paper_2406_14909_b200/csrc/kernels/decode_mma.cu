@@ -1,0 +1,494 @@
+// decode_mma.cu -- bf16 MoA decode over the compact ring cache on B200
+// (SURVEY §8(a) a7 split-KV + a8 combine [+ a6 append fused]).
+//
+// One query token per sequence at position `pos` attends over its kv-group's
+// cache region (sinks + ring; PAPER.md:704 fixed span, oldest entry
+// replaced).  q-head h masks ring rows older than its own window W_h
+// (reading c10), so one pass over a group's rows serves its G heads.
+//
+// HBM-bound design:
+//  * Balanced split: the layer cache is one contiguous row space
+//    [b][g][s + W_g rows]; CTA c streams rows [c*R/n, (c+1)*R/n) -- every CTA
+//    moves the same number of bytes whatever the per-head spans are.  A CTA
+//    range is cut into segments at region (b, g) boundaries; each segment
+//    yields one partial (m, l, o) per consumer warp.
+//  * A producer warp streams 64-row K/V tiles with TMA (cp.async.bulk.tensor,
+//    128B swizzle) into a 3-stage shared-memory ring (mbarrier full/empty).
+//  * 4 consumer warps, 16 keys each per tile, compute S = Q K^T and O += P V
+//    with mma.sync m16n8k16 (bf16 in, fp32 accumulate): the G heads of the
+//    group are the M rows (zero-padded to 16), keys the N columns, so K/V
+//    bytes are read once for all heads and the instruction count per row is
+//    independent of G.  Online softmax in base 2 with a lazy running max.
+//  * The last CTA of a region (atomic ticket, self-resetting) merges the
+//    partials by LSE and writes o (and lse).
+//  * Fused append: the cache row of `pos` is masked in the tile path; the CTA
+//    owning it folds (k_new, v_new) into its state and writes it to the cache.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "../moa_internal.h"
+#include "common.cuh"
+#include "ptx_sm100.cuh"
+
+namespace moa {
+namespace {
+
+using namespace ptx;
+
+constexpr int kCW = 4;                    // consumer warps
+constexpr int kThreads = (kCW + 1) * 32;  // + producer warp
+constexpr int kRows = 16 * kCW;           // rows per tile
+constexpr int kCtasPerSm = 2;
+constexpr float kRescale = 8.0f;
+
+template <int D>
+constexpr int part_stride() { return D + 4; }  // per-head partial: o[D], lse2, pad (16-B aligned)
+
+template <int D>
+struct DCfg {
+  static constexpr int kSlabs = D / 64;
+  static constexpr int kSlabBytes = kRows * 128;
+  static constexpr int kTileBytes = kRows * D * 2;            // K or V
+  static constexpr int kStages = D == 128 ? 3 : 6;
+  static constexpr int kSmem = kStages * 2 * kTileBytes + 1024;
+};
+
+struct MParams {
+  const __nv_bfloat16 *q;
+  __nv_bfloat16 *o;
+  int64_t q_bs, o_bs;
+  const __nv_bfloat16 *k_new, *v_new;
+  int64_t kv_bs;
+  __nv_bfloat16 *kc, *vc;
+  int64_t rows_per_seq, R, rpc;  // total rows, rows per CTA
+  const int64_t *g_off;
+  const int32_t *win_g, *win_q;
+  int ngl, G, n_sink, batch;
+  int64_t pos;
+  float scale_log2;
+  float *lse;
+  float *part;
+  int *counters;
+};
+
+struct Region {
+  int b, g, Wg;
+  int64_t start, end;  // absolute rows [start, end)
+};
+
+__device__ __forceinline__ Region region_of(const MParams &p, int64_t x) {
+  Region r;
+  r.b = (int)(x / p.rows_per_seq);
+  const int64_t within = x - (int64_t)r.b * p.rows_per_seq;
+  int g = 0;
+  while (g + 1 < p.ngl && p.g_off[g + 1] <= within) ++g;
+  r.g = g;
+  r.Wg = p.win_g[g];
+  r.start = (int64_t)r.b * p.rows_per_seq + p.g_off[g];
+  r.end = r.start + p.n_sink + r.Wg;
+  return r;
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *m, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    decode_mma_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                      const MParams p) {
+  using C = DCfg<D>;
+  constexpr int NT = D / 8;   // output n-tiles (8 dims each)
+  constexpr int KS = D / 16;  // k-steps over the head dim
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t full_bar[C::kStages], empty_bar[C::kStages];
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const int64_t X0 = (int64_t)blockIdx.x * p.rpc;
+  const int64_t X1 = X0 + p.rpc < p.R ? X0 + p.rpc : p.R;
+
+  if (tid == 0) {
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(smem_u32(&full_bar[i]), 1);
+      mbar_init(smem_u32(&empty_bar[i]), kCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (X0 >= X1) return;
+
+  if (warp == kCW) {
+    // ------------------------------------------------------------ producer: TMA K/V tiles
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      int T = 0;
+      for (int64_t x = X0; x < X1;) {
+        const Region rg = region_of(p, x);
+        const int64_t seg_end = rg.end < X1 ? rg.end : X1;
+        for (int64_t t0 = x; t0 < seg_end; t0 += kRows, ++T) {
+          const int st = T % C::kStages;
+          if (T >= C::kStages) mbar_wait(smem_u32(&empty_bar[st]), ((T - C::kStages) / C::kStages) & 1);
+          const uint32_t fb = smem_u32(&full_bar[st]);
+          mbar_expect_tx(fb, 2 * C::kTileBytes);
+          const uint32_t kd = base + st * 2 * C::kTileBytes, vd = kd + C::kTileBytes;
+          for (int sl = 0; sl < C::kSlabs; ++sl) {
+            tma_load_2d(kd + sl * C::kSlabBytes, &tm_k, fb, sl * 64, (int)t0);
+            tma_load_2d(vd + sl * C::kSlabBytes, &tm_v, fb, sl * 64, (int)t0);
+          }
+        }
+        x = seg_end;
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers (warps 0..3)
+  const int qr = lane >> 2, qc = lane & 3;  // fragment row (head) / column-pair index
+  const int h0 = qr, h1 = qr + 8;           // the two head rows this lane holds
+  const int s = p.n_sink;
+  const int64_t pos = p.pos;
+  int T = 0;
+  for (int64_t x = X0; x < X1;) {
+    const Region rg = region_of(p, x);
+    const int64_t seg_end = rg.end < X1 ? rg.end : X1;
+    const int G = p.G;
+    const int W0 = h0 < G ? p.win_q[rg.g * G + h0] : rg.Wg;
+    const int W1 = h1 < G ? p.win_q[rg.g * G + h1] : rg.Wg;
+    const bool ring_live = pos >= s && rg.Wg > 0;
+    const int pm = ring_live ? (int)((pos - s) % rg.Wg) : 0;
+    const int64_t slot_p = (p.k_new != nullptr) ? slot_of(pos, s, rg.Wg) : -1;
+
+    // Q fragments (A operand, 16 x D, rows >= G are zero), unscaled bf16
+    uint32_t qa[KS][4];
+    {
+      const __nv_bfloat16 *qb = p.q + (int64_t)rg.b * p.q_bs + (int64_t)rg.g * G * D;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int c = ks * 16 + qc * 2;
+        qa[ks][0] = h0 < G ? *reinterpret_cast<const uint32_t *>(qb + h0 * D + c) : 0u;
+        qa[ks][1] = h1 < G ? *reinterpret_cast<const uint32_t *>(qb + h1 * D + c) : 0u;
+        qa[ks][2] = h0 < G ? *reinterpret_cast<const uint32_t *>(qb + h0 * D + c + 8) : 0u;
+        qa[ks][3] = h1 < G ? *reinterpret_cast<const uint32_t *>(qb + h1 * D + c + 8) : 0u;
+      }
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+    for (int64_t t0 = x; t0 < seg_end; t0 += kRows, ++T) {
+      const int st = T % C::kStages;
+      const int nrows = (int)((seg_end - t0) < kRows ? (seg_end - t0) : kRows);
+      mbar_wait(smem_u32(&full_bar[st]), (T / C::kStages) & 1);
+      const uint32_t kb = base + st * 2 * C::kTileBytes, vb = kb + C::kTileBytes;
+      const int k0 = warp * 16;  // this warp's first key row in the tile
+
+      // ---- S = Q K^T  (16 heads x 16 keys)
+      float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      {
+        const int mi = lane >> 3, rr = lane & 7;
+        const int key = k0 + rr + (mi >> 1) * 8;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int chunk = 2 * ks + (mi & 1);
+          const uint32_t addr = kb + (chunk >> 3) * C::kSlabBytes + key * 128 + (((chunk & 7) ^ (key & 7)) << 4);
+          uint32_t b00, b01, b10, b11;
+          ldsm_x4(addr, b00, b01, b10, b11);
+          mma16816(sacc[0], qa[ks], b00, b01);
+          mma16816(sacc[1], qa[ks], b10, b11);
+        }
+      }
+      // ---- visibility of this lane's 4 keys for its 2 head rows
+      float sv[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int kk = k0 + nt * 8 + qc * 2 + e;  // key index in tile
+          const int64_t r = t0 + kk - rg.start;     // row in region
+          bool valid = kk < nrows, sink = false;
+          int age = 0;
+          if (valid) {
+            if (r < s) {
+              sink = true;
+              valid = r <= pos;
+            } else if (ring_live) {
+              int mm = pm - (int)(r - s);
+              if (mm < 0) mm += rg.Wg;
+              age = mm;
+              valid = (int64_t)mm <= pos - s;
+            } else {
+              valid = false;
+            }
+            if (r == slot_p) valid = false;  // fused: the new token is folded in separately
+          }
+          const bool v0 = valid && (sink || age < W0);
+          const bool v1 = valid && (sink || age < W1);
+          sv[nt][e] = v0 ? sacc[nt][e] * p.scale_log2 : -INFINITY;
+          sv[nt][2 + e] = v1 ? sacc[nt][2 + e] * p.scale_log2 : -INFINITY;
+        }
+      }
+      // ---- lazy online softmax per head row (quad-reduced max)
+      float mt0 = fmaxf(fmaxf(sv[0][0], sv[0][1]), fmaxf(sv[1][0], sv[1][1]));
+      float mt1 = fmaxf(fmaxf(sv[0][2], sv[0][3]), fmaxf(sv[1][2], sv[1][3]));
+      mt0 = fmaxf(mt0, __shfl_xor_sync(0xffffffffu, mt0, 1));
+      mt0 = fmaxf(mt0, __shfl_xor_sync(0xffffffffu, mt0, 2));
+      mt1 = fmaxf(mt1, __shfl_xor_sync(0xffffffffu, mt1, 1));
+      mt1 = fmaxf(mt1, __shfl_xor_sync(0xffffffffu, mt1, 2));
+      if (m0 == -INFINITY) {
+        m0 = mt0;
+      } else if (mt0 > m0 + kRescale) {
+        const float a = fast_exp2(m0 - mt0);
+        l0 *= a;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) o[j][0] *= a, o[j][1] *= a;
+        m0 = mt0;
+      }
+      if (m1 == -INFINITY) {
+        m1 = mt1;
+      } else if (mt1 > m1 + kRescale) {
+        const float a = fast_exp2(m1 - mt1);
+        l1 *= a;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) o[j][2] *= a, o[j][3] *= a;
+        m1 = mt1;
+      }
+      const float r0 = m0 == -INFINITY ? 0.f : m0, r1 = m1 == -INFINITY ? 0.f : m1;
+      uint32_t pa[4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const float e0 = fast_exp2(sv[nt][0] - r0), e1 = fast_exp2(sv[nt][1] - r0);
+        const float e2 = fast_exp2(sv[nt][2] - r1), e3 = fast_exp2(sv[nt][3] - r1);
+        l0 += e0 + e1;
+        l1 += e2 + e3;
+        pa[2 * nt + 0] = pack_bf16x2(e0, e1);
+        pa[2 * nt + 1] = pack_bf16x2(e2, e3);
+      }
+      // ---- O += P V  (16 heads x D)
+      {
+        const int mi = lane >> 3, rr = lane & 7;
+        const int key = k0 + rr + (mi & 1) * 8;
+#pragma unroll
+        for (int j2 = 0; j2 < NT / 2; ++j2) {
+          const int chunk = 2 * j2 + (mi >> 1);
+          const uint32_t addr = vb + (chunk >> 3) * C::kSlabBytes + key * 128 + (((chunk & 7) ^ (key & 7)) << 4);
+          uint32_t b0a, b1a, b0b, b1b;
+          ldsm_x4_t(addr, b0a, b1a, b0b, b1b);
+          mma16816(o[2 * j2], pa, b0a, b1a);
+          mma16816(o[2 * j2 + 1], pa, b0b, b1b);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
+    }
+
+    // ---- fused append: fold the new token into warp 0 of the CTA owning slot_p
+    if (slot_p >= 0 && warp == 0) {
+      const int64_t xr = rg.start + slot_p;
+      if (xr >= x && xr < seg_end) {
+        const __nv_bfloat16 *kn = p.k_new + (int64_t)rg.b * p.kv_bs + (int64_t)rg.g * D;
+        const __nv_bfloat16 *vn = p.v_new + (int64_t)rg.b * p.kv_bs + (int64_t)rg.g * D;
+        const __nv_bfloat16 *qb = p.q + (int64_t)rg.b * p.q_bs + (int64_t)rg.g * G * D;
+        float d0 = 0.f, d1 = 0.f;
+        for (int e = qc * (D / 4); e < (qc + 1) * (D / 4); ++e) {
+          const float kf = __bfloat162float(kn[e]);
+          if (h0 < G) d0 = fmaf(__bfloat162float(qb[h0 * D + e]), kf, d0);
+          if (h1 < G) d1 = fmaf(__bfloat162float(qb[h1 * D + e]), kf, d1);
+        }
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
+        // the new token (age 0) is visible to a head iff W_h >= 1 or it is a sink position
+        const bool nsink = pos < s;
+        const float x0 = (nsink || W0 >= 1) ? d0 * p.scale_log2 : -INFINITY;
+        const float x1 = (nsink || W1 >= 1) ? d1 * p.scale_log2 : -INFINITY;
+        const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+        const float a0 = (m0 == -INFINITY) ? 0.f : fast_exp2(m0 - n0);
+        const float a1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - n1);
+        const float p0 = x0 == -INFINITY ? 0.f : fast_exp2(x0 - n0);
+        const float p1 = x1 == -INFINITY ? 0.f : fast_exp2(x1 - n1);
+        if (n0 != -INFINITY) {
+          l0 = l0 * a0 + (qc == 0 ? p0 : 0.f);
+          m0 = n0;
+        }
+        if (n1 != -INFINITY) {
+          l1 = l1 * a1 + (qc == 0 ? p1 : 0.f);
+          m1 = n1;
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const int c = 8 * j + qc * 2;
+          const float v0 = __bfloat162float(vn[c]), v1 = __bfloat162float(vn[c + 1]);
+          if (n0 != -INFINITY) {
+            o[j][0] = o[j][0] * a0 + p0 * v0;
+            o[j][1] = o[j][1] * a0 + p0 * v1;
+          }
+          if (n1 != -INFINITY) {
+            o[j][2] = o[j][2] * a1 + p1 * v0;
+            o[j][3] = o[j][3] * a1 + p1 * v1;
+          }
+        }
+        // write the token into its cache row (nothing reads this row in this launch)
+        const int64_t row = xr;
+        for (int e = lane * 8; e < D; e += 32 * 8) {
+          *reinterpret_cast<uint4 *>(p.kc + row * D + e) = *reinterpret_cast<const uint4 *>(kn + e);
+          *reinterpret_cast<uint4 *>(p.vc + row * D + e) = *reinterpret_cast<const uint4 *>(vn + e);
+        }
+      }
+    }
+
+    // ---- per-warp partial of this segment: o / l and lse2
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    const int ridx = rg.b * p.ngl + rg.g;
+    const int64_t slot = ((int64_t)blockIdx.x + ridx) * kCW + warp;
+    constexpr int PS = part_stride<D>();
+    float *part = p.part + slot * G * PS;
+    {
+      const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int c = 8 * j + qc * 2;
+        if (h0 < G) *reinterpret_cast<float2 *>(part + h0 * PS + c) = make_float2(o[j][0] * i0, o[j][1] * i0);
+        if (h1 < G) *reinterpret_cast<float2 *>(part + h1 * PS + c) = make_float2(o[j][2] * i1, o[j][3] * i1);
+      }
+      if (qc == 0) {
+        if (h0 < G) part[h0 * PS + D] = l0 > 0.f ? m0 + __log2f(l0) : -INFINITY;
+        if (h1 < G) part[h1 * PS + D] = l1 > 0.f ? m1 + __log2f(l1) : -INFINITY;
+      }
+    }
+    __threadfence();
+    named_bar_sync(1, kCW * 32);
+    if (tid == 0) {
+      const int64_t c_first = rg.start / p.rpc, c_last = (rg.end - 1) / p.rpc;
+      int *ctr = p.counters + ridx;
+      const int ticket = atomicAdd(ctr, 1);
+      const bool last = ticket == (int)(c_last - c_first);
+      if (last) *ctr = 0;
+      s_last = last;
+    }
+    named_bar_sync(1, kCW * 32);
+    if (s_last) {
+      __threadfence();
+      const int64_t c_first = rg.start / p.rpc, c_last = (rg.end - 1) / p.rpc;
+      const int64_t sl0 = (c_first + ridx) * kCW, sl1 = (c_last + ridx + 1) * kCW;
+      for (int t = tid; t < G * D; t += kCW * 32) {
+        const int j = t / D, e = t - j * D;
+        float mx = -INFINITY;
+        for (int64_t sl = sl0; sl < sl1; ++sl) mx = fmaxf(mx, __ldcg(p.part + (sl * G + j) * PS + D));
+        float L = 0.f, O = 0.f;
+        for (int64_t sl = sl0; sl < sl1; ++sl) {
+          const float *pc = p.part + (sl * G + j) * PS;
+          const float ls = __ldcg(pc + D);
+          if (ls == -INFINITY) continue;
+          const float w = fast_exp2(ls - mx);
+          L += w;
+          O += w * __ldcg(pc + e);
+        }
+        p.o[(int64_t)rg.b * p.o_bs + (int64_t)(rg.g * G + j) * D + e] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+        if (p.lse && e == 0)
+          p.lse[(int64_t)rg.b * p.ngl * G + rg.g * G + j] = L > 0.f ? (mx + __log2f(L)) * kLn2 : -INFINITY;
+      }
+    }
+    x = seg_end;
+  }
+}
+
+int num_sms_dev() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+int ctas_for(int64_t R) {
+  int64_t n = (int64_t)num_sms_dev() * kCtasPerSm;
+  int64_t by_rows = (R + kRows - 1) / kRows;
+  return (int)(n < by_rows ? n : by_rows);
+}
+
+template <int D>
+int launch_d(const DecodeMmaArgs &a, void *stream) {
+  using C = DCfg<D>;
+  MParams p;
+  p.q = static_cast<const __nv_bfloat16 *>(a.q);
+  p.o = static_cast<__nv_bfloat16 *>(a.o);
+  p.q_bs = a.q_bs;
+  p.o_bs = a.o_bs;
+  p.k_new = static_cast<const __nv_bfloat16 *>(a.k_new);
+  p.v_new = static_cast<const __nv_bfloat16 *>(a.v_new);
+  p.kv_bs = a.kv_bs;
+  p.kc = static_cast<__nv_bfloat16 *>(a.k_cache);
+  p.vc = static_cast<__nv_bfloat16 *>(a.v_cache);
+  p.rows_per_seq = a.rows_per_seq;
+  p.R = (int64_t)a.batch * a.rows_per_seq;
+  const int n = ctas_for(p.R);
+  p.rpc = (p.R + n - 1) / n;
+  p.g_off = a.d_g_off;
+  p.win_g = a.d_win_g;
+  p.win_q = a.d_win_q;
+  p.ngl = a.ngl;
+  p.G = a.G;
+  p.n_sink = a.n_sink;
+  p.batch = a.batch;
+  p.pos = a.pos;
+  p.scale_log2 = a.scale * kLog2e;
+  p.lse = a.lse;
+  p.part = a.ws_part;
+  p.counters = a.counters;
+  cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  if (e != cudaSuccess) return (int)e;
+  const CUtensorMap *km = static_cast<const CUtensorMap *>(a.kmap);
+  const CUtensorMap *vm = static_cast<const CUtensorMap *>(a.vmap);
+  decode_mma_kernel<D><<<n, kThreads, C::kSmem, (cudaStream_t)stream>>>(*km, *vm, p);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d) {
+  const size_t slots = ((size_t)num_sms_dev() * kCtasPerSm + (size_t)batch * ngl + 1) * kCW;
+  return ((slots * G * (d + 4) * 4) + 255) & ~size_t(255);
+}
+
+int launch_decode_mma(const DecodeMmaArgs &a, void *stream) {
+  if (a.d == 128) return launch_d<128>(a, stream);
+  return launch_d<64>(a, stream);
+}
+
+}  // namespace moa

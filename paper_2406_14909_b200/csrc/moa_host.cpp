@@ -352,6 +352,10 @@ moa_status moa_workspace_bytes(const moa_ctx *ctx, int batch, size_t *bytes) {
   for (const auto &p : ctx->layers)
     if (p.set)
       mx = std::max(mx, moa::decode_ws_bytes(batch, (int)(p.chunks.size() / 3), ctx->G, ctx->d));
+  if (ctx->dtype == MOA_BF16 && ctx->device >= 0) {
+    DeviceGuard dg(ctx->device);
+    mx = std::max(mx, moa::decode_mma_ws_bytes(batch, ctx->ngl, ctx->G, ctx->d));
+  }
   *bytes = mx;
   return ok();
 }
@@ -369,6 +373,23 @@ moa_status moa_bind_layer_cache(moa_ctx *ctx, int layer, void *k_cache, void *v_
   p.v_cache = v_cache;
   p.bound_batch = batch;
   p.next_pos = 0;
+  p.maps_ok = false;
+  if (ctx->device >= 0) {
+    // rows not yet reached by the sequence must hold finite values: the tensor-core decode
+    // multiplies masked rows by a zero probability, and 0 * NaN would poison the sum
+    DeviceGuard dg(ctx->device);
+    const size_t bytes = layer_bytes(ctx, p, batch);
+    cudaError_t e = cudaMemset(k_cache, 0, bytes);
+    if (e == cudaSuccess) e = cudaMemset(v_cache, 0, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(cache)");
+  }
+  if (ctx->device >= 0 && ctx->dtype == MOA_BF16) {
+    DeviceGuard dg(ctx->device);
+    const int64_t rows = (int64_t)batch * p.rows_per_seq;
+    if (!moa::encode_cache_map(p.kmap, k_cache, ctx->d, rows) || !moa::encode_cache_map(p.vmap, v_cache, ctx->d, rows))
+      return fail(MOA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the layer %d cache", layer);
+    p.maps_ok = true;
+  }
   return ok();
 }
 
@@ -517,11 +538,28 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
     return fail(MOA_ERR_INVALID_ARG, "decode pointers and batch strides must be 16-byte aligned");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(MOA_ERR_INVALID_ARG, "scale must be finite > 0");
   const int n_chunks = (int)(p.chunks.size() / 3);
-  size_t need = moa::decode_ws_bytes(batch, n_chunks, ctx->G, ctx->d);
+  const bool mma_path = ctx->dtype == MOA_BF16;
+  size_t need = mma_path ? moa::decode_mma_ws_bytes(batch, ctx->ngl, ctx->G, ctx->d)
+                         : moa::decode_ws_bytes(batch, n_chunks, ctx->G, ctx->d);
   if (!workspace || ws_bytes < need)
     return fail(MOA_ERR_OOM, "workspace of %zu bytes < %zu needed", ws_bytes, need);
   if (!aligned16(workspace)) return fail(MOA_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
   DeviceGuard dg(ctx->device);
+  if (mma_path) {
+    if (!p.maps_ok) return fail(MOA_ERR_STATE, "layer %d cache has no tensor maps (re-bind the cache)", layer);
+    moa::DecodeMmaArgs m{};
+    m.kmap = p.kmap; m.vmap = p.vmap; m.q = q; m.o = o; m.q_bs = q_batch_stride; m.o_bs = o_batch_stride;
+    m.k_new = fused ? k_new : nullptr; m.v_new = fused ? v_new : nullptr; m.kv_bs = kv_batch_stride;
+    m.k_cache = p.k_cache; m.v_cache = p.v_cache; m.rows_per_seq = p.rows_per_seq;
+    m.d_g_off = p.d_g_off; m.d_win_g = p.d_win_g; m.d_win_q = p.d_win_q;
+    m.ngl = ctx->ngl; m.G = ctx->G; m.d = ctx->d; m.n_sink = p.n_sink; m.batch = batch;
+    m.pos = pos; m.scale = scale; m.lse = lse_out; m.ws_part = static_cast<float *>(workspace);
+    m.counters = p.d_counters;
+    int e = moa::launch_decode_mma(m, stream);
+    if (e) return cuda_fail((cudaError_t)e, "decode launch");
+    if (fused) p.next_pos = pos + 1;
+    return ok();
+  }
   moa::DecodeArgs a{};
   a.q = q; a.o = o; a.q_batch_stride = q_batch_stride; a.o_batch_stride = o_batch_stride;
   a.k_new = fused ? k_new : nullptr; a.v_new = fused ? v_new : nullptr; a.kv_batch_stride = kv_batch_stride;

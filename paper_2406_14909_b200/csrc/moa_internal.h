@@ -111,6 +111,11 @@ struct LayerPlan {
   const int32_t *d_chunks = nullptr;
   const int32_t *d_g_chunk = nullptr;
   int *d_counters = nullptr;     // [max_batch, ngl] decode combine tickets (zeroed at upload)
+  // TMA tensor maps (CUtensorMap, 128 B) over the bound K / V cache of this layer:
+  // 2D [bound_batch * rows_per_seq rows, d], 64-row x 64-col boxes, 128B swizzle
+  alignas(64) unsigned char kmap[128] = {};
+  alignas(64) unsigned char vmap[128] = {};
+  bool maps_ok = false;
   // bound cache
   void *k_cache = nullptr;
   void *v_cache = nullptr;
@@ -185,5 +190,30 @@ struct DecodeArgs {
 int launch_decode(const DecodeArgs &a, moa_dtype dtype, bool fused, void *stream);
 
 size_t decode_ws_bytes(int batch, int n_chunks, int G, int d);
+
+// bf16 decode on mma.sync with TMA-staged swizzled cache tiles (decode_mma.cu)
+struct DecodeMmaArgs {
+  const void *kmap, *vmap;     // host CUtensorMap images
+  const void *q;
+  void *o;
+  int64_t q_bs, o_bs;
+  const void *k_new, *v_new;   // fused append (nullable)
+  int64_t kv_bs;
+  void *k_cache, *v_cache;     // for the fused append's global write
+  int64_t rows_per_seq;
+  const int64_t *d_g_off;
+  const int32_t *d_win_g, *d_win_q;
+  int ngl, G, d, n_sink, batch;
+  int64_t pos;
+  float scale;
+  float *lse;
+  float *ws_part;
+  int *counters;
+};
+int launch_decode_mma(const DecodeMmaArgs &a, void *stream);
+size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d);
+
+// TMA tensor map over a [rows, d] bf16 cache (box 64 rows x 64 cols, 128B swizzle).
+bool encode_cache_map(void *map_out, const void *ptr, int d, int64_t rows);
 
 }  // namespace moa

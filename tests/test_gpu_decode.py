@@ -91,11 +91,22 @@ def test_group_sizes_bf16(moa, G):
     _decode_run(moa, torch.bfloat16, 3, G * Hkv, Hkv, 128, 3, W, 90, 31 + G, check_every=11)
 
 
-def test_fused_append_decode_is_bitwise_equal_to_two_calls(moa):
+def test_fused_append_decode_matches_two_calls(moa):
+    """moa_decode_step_fused == moa_kv_append + moa_decode_step: both are
+    checked against the oracle every step (and the cache image bitwise); the
+    fused kernel folds the new token in fp32 outside the tensor-core tile path,
+    so the two agree to rounding, not bit for bit (bf16)."""
     W = [9, 33, 2, 70]
     a = _decode_run(moa, torch.bfloat16, 2, 4, 2, 128, 5, W, 120, 41, fused=False, check_every=13)
     b = _decode_run(moa, torch.bfloat16, 2, 4, 2, 128, 5, W, 120, 41, fused=True, check_every=13)
-    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    assert (a.float() - b.float()).abs().max().item() < 2e-2
+
+
+def test_fused_append_fp32_is_bitwise_equal_to_two_calls(moa):
+    W = [9, 33, 2, 70]
+    a = _decode_run(moa, torch.float32, 1, 4, 2, 64, 5, W, 90, 43, fused=False, check_every=13)
+    b = _decode_run(moa, torch.float32, 1, 4, 2, 64, 5, W, 90, 43, fused=True, check_every=13)
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
 
 
 def test_cache_fill_then_decode_with_wraps(moa):
