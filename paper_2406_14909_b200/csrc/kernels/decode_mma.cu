@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "../moa_internal.h"
 #include "common.cuh"
@@ -46,12 +47,12 @@ constexpr float kRescale = 8.0f;
 template <int D>
 constexpr int part_stride() { return D + 4; }  // per-head partial: o[D], lse2, pad (16-B aligned)
 
-template <int D>
+template <int D, int STAGES>
 struct DCfg {
   static constexpr int kSlabs = D / 64;
   static constexpr int kSlabBytes = kRows * 128;
   static constexpr int kTileBytes = kRows * D * 2;            // K or V
-  static constexpr int kStages = D == 128 ? 3 : 6;
+  static constexpr int kStages = STAGES;
   static constexpr int kSmem = kStages * 2 * kTileBytes + 1024;
 };
 
@@ -78,15 +79,22 @@ struct Region {
   int64_t start, end;  // absolute rows [start, end)
 };
 
-__device__ __forceinline__ Region region_of(const MParams &p, int64_t x) {
+constexpr int kMaxGroups = 128;
+constexpr int kMaxPend = 256;
+
+// region (b, g) holding absolute row x; g_off / win_g are staged in shared memory
+__device__ __forceinline__ Region region_of(const MParams &p, const int64_t *g_off, const int *win_g, int64_t x) {
   Region r;
   r.b = (int)(x / p.rows_per_seq);
   const int64_t within = x - (int64_t)r.b * p.rows_per_seq;
-  int g = 0;
-  while (g + 1 < p.ngl && p.g_off[g + 1] <= within) ++g;
-  r.g = g;
-  r.Wg = p.win_g[g];
-  r.start = (int64_t)r.b * p.rows_per_seq + p.g_off[g];
+  int lo = 0, hi = p.ngl - 1;  // last g with g_off[g] <= within
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (g_off[mid] <= within) lo = mid; else hi = mid - 1;
+  }
+  r.g = lo;
+  r.Wg = win_g[lo];
+  r.start = (int64_t)r.b * p.rows_per_seq + g_off[lo];
   r.end = r.start + p.n_sink + r.Wg;
   return r;
 }
@@ -119,16 +127,48 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// merge the partials of region ridx (slots of every CTA x warp that touched it) by LSE
 template <int D>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+__device__ __forceinline__ void combine_region(const MParams &p, const int64_t *g_off, const int *win_g, int ridx,
+                                               int t0, int tstep) {
+  constexpr int PS = part_stride<D>();
+  const int b = ridx / p.ngl, g = ridx - b * p.ngl;
+  const int G = p.G;
+  const int64_t start = (int64_t)b * p.rows_per_seq + g_off[g];
+  const int64_t end = start + p.n_sink + win_g[g];
+  const int64_t c_first = start / p.rpc, c_last = (end - 1) / p.rpc;
+  const int64_t sl0 = (c_first + ridx) * kCW, sl1 = (c_last + ridx + 1) * kCW;
+  for (int t = t0; t < G * D; t += tstep) {
+    const int j = t / D, e = t - j * D;
+    float mx = -INFINITY;
+    for (int64_t sl = sl0; sl < sl1; ++sl) mx = fmaxf(mx, __ldcg(p.part + (sl * G + j) * PS + D));
+    float L = 0.f, O = 0.f;
+    for (int64_t sl = sl0; sl < sl1; ++sl) {
+      const float *pc = p.part + (sl * G + j) * PS;
+      const float ls = __ldcg(pc + D);
+      if (ls == -INFINITY) continue;
+      const float w = fast_exp2(ls - mx);
+      L += w;
+      O += w * __ldcg(pc + e);
+    }
+    p.o[(int64_t)b * p.o_bs + (int64_t)(g * G + j) * D + e] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+    if (p.lse && e == 0) p.lse[(int64_t)b * p.ngl * G + g * G + j] = L > 0.f ? (mx + __log2f(L)) * kLn2 : -INFINITY;
+  }
+}
+
+template <int D, int STAGES, int CPS>
+__global__ void __launch_bounds__(kThreads, CPS)
     decode_mma_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                       const MParams p) {
-  using C = DCfg<D>;
+  using C = DCfg<D, STAGES>;
   constexpr int NT = D / 8;   // output n-tiles (8 dims each)
   constexpr int KS = D / 16;  // k-steps over the head dim
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full_bar[C::kStages], empty_bar[C::kStages];
-  __shared__ int s_last;
+  __shared__ int64_t s_goff[kMaxGroups];
+  __shared__ int s_wing[kMaxGroups];
+  __shared__ int s_pend[kMaxPend];  // regions whose combine this CTA owes (deferred to the end)
+  __shared__ int s_npend;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -142,7 +182,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     }
     fence_mbar_init();
   }
+  if (tid == 0) s_npend = 0;
+  for (int g = tid; g < p.ngl; g += kThreads) {
+    s_goff[g] = p.g_off[g];
+    s_wing[g] = p.win_g[g];
+  }
   __syncthreads();
+  // programmatic dependent launch: everything above overlapped the previous kernel's tail;
+  // q / k_new / the cache / the tickets may be written by stream predecessors
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (X0 >= X1) return;
 
   if (warp == kCW) {
@@ -152,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       tma_prefetch_desc(&tm_v);
       int T = 0;
       for (int64_t x = X0; x < X1;) {
-        const Region rg = region_of(p, x);
+        const Region rg = region_of(p, s_goff, s_wing, x);
         const int64_t seg_end = rg.end < X1 ? rg.end : X1;
         for (int64_t t0 = x; t0 < seg_end; t0 += kRows, ++T) {
           const int st = T % C::kStages;
@@ -178,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const int64_t pos = p.pos;
   int T = 0;
   for (int64_t x = X0; x < X1;) {
-    const Region rg = region_of(p, x);
+    const Region rg = region_of(p, s_goff, s_wing, x);
     const int64_t seg_end = rg.end < X1 ? rg.end : X1;
     const int G = p.G;
     const int W0 = h0 < G ? p.win_q[rg.g * G + h0] : rg.Wg;
@@ -186,6 +234,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const bool ring_live = pos >= s && rg.Wg > 0;
     const int pm = ring_live ? (int)((pos - s) % rg.Wg) : 0;
     const int64_t slot_p = (p.k_new != nullptr) ? slot_of(pos, s, rg.Wg) : -1;
+    const int slot_r = (int)slot_p;  // region row of the fused token (-1: none)
+    const int pos32 = pos < (int64_t)0x7fffffff ? (int)pos : 0x7fffffff;
+    const int ring_age_max = (int)((pos - s) < (int64_t)0x7fffffff ? (pos - s) : (int64_t)0x7fffffff);
+    // every sink and ring row holds a position and every real head sees the whole ring
+    const int minW = (W0 < W1 ? W0 : W1);
+    const bool seg_full = pos - s >= (int64_t)rg.Wg - 1 && pos >= s &&
+                          __reduce_min_sync(0xffffffffu, (unsigned)minW) >= (unsigned)rg.Wg;
 
     // Q fragments (A operand, 16 x D, rows >= G are zero), unscaled bf16
     uint32_t qa[KS][4];
@@ -212,8 +267,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const uint32_t kb = base + st * 2 * C::kTileBytes, vb = kb + C::kTileBytes;
       const int k0 = warp * 16;  // this warp's first key row in the tile
 
-      // ---- S = Q K^T  (16 heads x 16 keys)
-      float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      // ---- S = Q K^T  (16 heads x 16 keys); two accumulators per n-tile halve the HMMA chain
+      float sacc[2][4], sacc2[2][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sacc[0][i] = sacc[1][i] = sacc2[0][i] = sacc2[1][i] = 0.f;
       {
         const int mi = lane >> 3, rr = lane & 7;
         const int key = k0 + rr + (mi >> 1) * 8;
@@ -223,38 +280,49 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           const uint32_t addr = kb + (chunk >> 3) * C::kSlabBytes + key * 128 + (((chunk & 7) ^ (key & 7)) << 4);
           uint32_t b00, b01, b10, b11;
           ldsm_x4(addr, b00, b01, b10, b11);
-          mma16816(sacc[0], qa[ks], b00, b01);
-          mma16816(sacc[1], qa[ks], b10, b11);
+          if (ks & 1) {
+            mma16816(sacc2[0], qa[ks], b00, b01);
+            mma16816(sacc2[1], qa[ks], b10, b11);
+          } else {
+            mma16816(sacc[0], qa[ks], b00, b01);
+            mma16816(sacc[1], qa[ks], b10, b11);
+          }
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sacc[0][i] += sacc2[0][i], sacc[1][i] += sacc2[1][i];
       }
       // ---- visibility of this lane's 4 keys for its 2 head rows
+      const int r_first = (int)(t0 - rg.start) + k0;  // region row of this warp's first key
+      const bool fast = seg_full && k0 + 16 <= nrows && !(slot_r >= r_first && slot_r < r_first + 16);
       float sv[2][4];
+      if (fast) {  // every key valid and inside every head's window: no mask arithmetic
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+        for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int kk = k0 + nt * 8 + qc * 2 + e;  // key index in tile
-          const int64_t r = t0 + kk - rg.start;     // row in region
-          bool valid = kk < nrows, sink = false;
-          int age = 0;
-          if (valid) {
+          for (int i = 0; i < 4; ++i) sv[nt][i] = sacc[nt][i] * p.scale_log2;
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int kk = k0 + nt * 8 + qc * 2 + e;  // key index in tile
+            const int r = r_first - k0 + kk;          // row in region
+            bool valid = kk < nrows && r != slot_r, sink = false;
+            int age = 0;
             if (r < s) {
               sink = true;
-              valid = r <= pos;
-            } else if (ring_live) {
-              int mm = pm - (int)(r - s);
+              valid = valid && r <= pos32;
+            } else {
+              int mm = pm - (r - s);
               if (mm < 0) mm += rg.Wg;
               age = mm;
-              valid = (int64_t)mm <= pos - s;
-            } else {
-              valid = false;
+              valid = valid && ring_live && mm <= ring_age_max;
             }
-            if (r == slot_p) valid = false;  // fused: the new token is folded in separately
+            const bool v0 = valid && (sink || age < W0);
+            const bool v1 = valid && (sink || age < W1);
+            sv[nt][e] = v0 ? sacc[nt][e] * p.scale_log2 : -INFINITY;
+            sv[nt][2 + e] = v1 ? sacc[nt][2 + e] * p.scale_log2 : -INFINITY;
           }
-          const bool v0 = valid && (sink || age < W0);
-          const bool v1 = valid && (sink || age < W1);
-          sv[nt][e] = v0 ? sacc[nt][e] * p.scale_log2 : -INFINITY;
-          sv[nt][2 + e] = v1 ? sacc[nt][2 + e] * p.scale_log2 : -INFINITY;
         }
       }
       // ---- lazy online softmax per head row (quad-reduced max)
@@ -389,41 +457,30 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         if (h1 < G) part[h1 * PS + D] = l1 > 0.f ? m1 + __log2f(l1) : -INFINITY;
       }
     }
-    __threadfence();
     named_bar_sync(1, kCW * 32);
     if (tid == 0) {
+      __threadfence();  // cumulative: orders every consumer's partial (seen via bar.sync) before the ticket
       const int64_t c_first = rg.start / p.rpc, c_last = (rg.end - 1) / p.rpc;
       int *ctr = p.counters + ridx;
       const int ticket = atomicAdd(ctr, 1);
-      const bool last = ticket == (int)(c_last - c_first);
-      if (last) *ctr = 0;
-      s_last = last;
-    }
-    named_bar_sync(1, kCW * 32);
-    if (s_last) {
-      __threadfence();
-      const int64_t c_first = rg.start / p.rpc, c_last = (rg.end - 1) / p.rpc;
-      const int64_t sl0 = (c_first + ridx) * kCW, sl1 = (c_last + ridx + 1) * kCW;
-      for (int t = tid; t < G * D; t += kCW * 32) {
-        const int j = t / D, e = t - j * D;
-        float mx = -INFINITY;
-        for (int64_t sl = sl0; sl < sl1; ++sl) mx = fmaxf(mx, __ldcg(p.part + (sl * G + j) * PS + D));
-        float L = 0.f, O = 0.f;
-        for (int64_t sl = sl0; sl < sl1; ++sl) {
-          const float *pc = p.part + (sl * G + j) * PS;
-          const float ls = __ldcg(pc + D);
-          if (ls == -INFINITY) continue;
-          const float w = fast_exp2(ls - mx);
-          L += w;
-          O += w * __ldcg(pc + e);
+      if (ticket == (int)(c_last - c_first)) {  // last contributor: combine later (deferred)
+        *ctr = 0;                                // self-reset for the next launch
+        if (s_npend < kMaxPend) {
+          s_pend[s_npend++] = ridx;
+        } else {  // (only with very many tiny regions) merge right away, single-threaded
+          __threadfence();
+          combine_region<D>(p, s_goff, s_wing, ridx, 0, 1);
         }
-        p.o[(int64_t)rg.b * p.o_bs + (int64_t)(rg.g * G + j) * D + e] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
-        if (p.lse && e == 0)
-          p.lse[(int64_t)rg.b * p.ngl * G + rg.g * G + j] = L > 0.f ? (mx + __log2f(L)) * kLn2 : -INFINITY;
       }
     }
     x = seg_end;
   }
+
+  // ---- deferred combines of the regions this CTA completed last
+  named_bar_sync(1, kCW * 32);
+  const int npend = s_npend;
+  if (npend > 0) __threadfence();
+  for (int k = 0; k < npend; ++k) combine_region<D>(p, s_goff, s_wing, s_pend[k], tid, kCW * 32);
 }
 
 int num_sms_dev() {
@@ -436,15 +493,15 @@ int num_sms_dev() {
   return n;
 }
 
-int ctas_for(int64_t R) {
-  int64_t n = (int64_t)num_sms_dev() * kCtasPerSm;
+int ctas_for(int64_t R, int cps) {
+  int64_t n = (int64_t)num_sms_dev() * cps;
   int64_t by_rows = (R + kRows - 1) / kRows;
   return (int)(n < by_rows ? n : by_rows);
 }
 
-template <int D>
-int launch_d(const DecodeMmaArgs &a, void *stream) {
-  using C = DCfg<D>;
+template <int D, int STAGES, int CPS>
+int launch_v(const DecodeMmaArgs &a, void *stream) {
+  using C = DCfg<D, STAGES>;
   MParams p;
   p.q = static_cast<const __nv_bfloat16 *>(a.q);
   p.o = static_cast<__nv_bfloat16 *>(a.o);
@@ -457,7 +514,7 @@ int launch_d(const DecodeMmaArgs &a, void *stream) {
   p.vc = static_cast<__nv_bfloat16 *>(a.v_cache);
   p.rows_per_seq = a.rows_per_seq;
   p.R = (int64_t)a.batch * a.rows_per_seq;
-  const int n = ctas_for(p.R);
+  const int n = ctas_for(p.R, CPS);
   p.rpc = (p.R + n - 1) / n;
   p.g_off = a.d_g_off;
   p.win_g = a.d_win_g;
@@ -471,12 +528,39 @@ int launch_d(const DecodeMmaArgs &a, void *stream) {
   p.lse = a.lse;
   p.part = a.ws_part;
   p.counters = a.counters;
-  cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D, STAGES, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return (int)e;
   const CUtensorMap *km = static_cast<const CUtensorMap *>(a.kmap);
   const CUtensorMap *vm = static_cast<const CUtensorMap *>(a.vmap);
-  decode_mma_kernel<D><<<n, kThreads, C::kSmem, (cudaStream_t)stream>>>(*km, *vm, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)n);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, decode_mma_kernel<D, STAGES, CPS>, *km, *vm, p);
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
+}
+
+template <int D>
+int launch_d(const DecodeMmaArgs &a, void *stream) {
+  static int variant = [] {
+    const char *e = std::getenv("MOA_DEC_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (D == 128) {
+    switch (variant) {
+      case 1: return launch_v<D, 3, 2>(a, stream);
+      case 2: return launch_v<D, 4, 1>(a, stream);
+      default: return launch_v<D, 2, 2>(a, stream);
+    }
+  }
+  return launch_v<D, 6, 2>(a, stream);
 }
 
 }  // namespace

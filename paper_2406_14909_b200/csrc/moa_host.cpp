@@ -546,6 +546,7 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
   if (!aligned16(workspace)) return fail(MOA_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
   DeviceGuard dg(ctx->device);
   if (mma_path) {
+    if (ctx->ngl > 128) return fail(MOA_ERR_UNSUPPORTED, "more than 128 local kv-groups");
     if (!p.maps_ok) return fail(MOA_ERR_STATE, "layer %d cache has no tensor maps (re-bind the cache)", layer);
     moa::DecodeMmaArgs m{};
     m.kmap = p.kmap; m.vmap = p.vmap; m.q = q; m.o = o; m.q_bs = q_batch_stride; m.o_bs = o_batch_stride;
