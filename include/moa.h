@@ -206,8 +206,10 @@ moa_status moa_layer_offset(const moa_ctx *ctx, int layer, int batch, size_t *by
 #define MOA_TILE 128
 moa_status moa_prefill_tiles(const moa_ctx *ctx, int layer, int q_head_local, int q_tile,
                              int32_t *tiles, uint8_t *edge, int max_tiles, int32_t *n_tiles);
-/* Work-item order of the prefill kernel: n_items (q_head_local, q_tile) pairs,
- * longest first (LPT).  items: 2 * max_items int32. */
+/* Work-item order of the prefill kernels: n_items (q_head_local, q_tile) pairs.
+ * Heads by total kv-tile count, heaviest first; the q tiles of one head are
+ * consecutive (concurrent CTAs share that head's K/V tiles in L2), heaviest
+ * first.  items: 2 * max_items int32. */
 moa_status moa_prefill_items(const moa_ctx *ctx, int layer, int32_t *items, int max_items,
                              int32_t *n_items);
 /* Decode work list: n chunks of (group_local, row_begin, row_end). */

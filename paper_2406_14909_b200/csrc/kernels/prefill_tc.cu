@@ -9,23 +9,22 @@
 // apply the token-granular predicate.  Within a visited tile the work is a
 // dense contraction, so QK^T and PV run on tcgen05 with TMEM accumulators.
 //
-// Work item = two adjacent 128-row q tiles (Q0, Q1) of one (b, head): their kv
-// tile lists differ by at most one tile at each end, so one TMA stream of K/V
-// tiles (the union) feeds both.  Persistent CTAs (one per SM) walk a static
-// round-robin slice of the LPT-sorted item list.  Warp roles (384 threads):
-//   warps 0-3   softmax of Q0 (thread t owns row t = TMEM lane t)
-//   warps 4-7   softmax of Q1
-//   warp 8      TMA producer of Q0/Q1 and the K ring; warp 10: producer of the V ring
-//   warp 9      TMEM allocator + single-thread MMA issuer
-// TMEM (512 columns): S0 (128 fp32, P0 aliased as 64 packed bf16x2 columns) |
-// O0 (D) | S1/P1 | O1.  The MMA issue order S0(k) S1(k) | PV0(k) S0(k+1) |
-// PV1(k) S1(k+1) | ... keeps the tensor pipe busy with one Q tile while the
-// other tile's softmax runs (ping-pong).  tcgen05 ops of one thread complete in
-// issue order and a commit tracks all earlier ops, so "S_q(k+1) complete"
-// implies "PV_q(k) complete": P may overwrite S and O may be rescaled without
-// extra barriers.  The running max is refreshed (and O rescaled in TMEM) only
-// when it grows by more than 2^8; a share of the exponentials runs as a
-// polynomial on the FMA pipe (MUFU ex2 is as slow as the tensor core here).
+// Persistent CTAs (one per SM) walk a static round-robin slice of the
+// LPT-sorted (q-head, 128-row q tile) x batch work list.  Warp roles (384 threads):
+//   warps 0-3   softmax of S columns [0, 64)   (thread t owns row t = TMEM lane t)
+//   warps 4-7   softmax of S columns [64, 128) (same rows; the two halves exchange the
+//               row max through shared memory once per tile)
+//   warp 8      TMA producer: Q (double-buffered per item) and the K ring
+//   warp 9      TMEM allocator + MMA issuer (whole warp, one elected lane issues)
+//   warp 10     TMA producer: the V ring
+// TMEM (512 columns): S0 | S1 (fp32 128x128) | P0 | P1 (bf16 128x128 packed, 64 columns
+// each) | O (fp32 128xD).  S is double-buffered, so QK^T of tile T+1 runs on the tensor
+// core while the softmax of tile T executes; P is double-buffered, so PV of tile T
+// overlaps the softmax of tile T+1.  tcgen05 ops of one thread complete in issue order
+// and a commit tracks every earlier op, so "S(T) complete" implies "PV(T-2) complete"
+// (P[T%2] is free).  The running max is refreshed (and O rescaled in TMEM) only when it
+// grows by more than 2^8; a share of the exponentials runs as a polynomial on the FMA
+// pipe (MUFU ex2, 16/clk/SM, is as slow as the tensor core on a 128x128 tile).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -45,20 +44,17 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kM = 128;                // q rows per tile (MMA M)
-constexpr int kN = 128;                // keys per tile (MMA N of QK^T, K of PV)
-constexpr int kSoftmaxThreads = 128;   // one warpgroup per q tile
-constexpr int kThreads = 3 * 128;
+constexpr int kM = 128;               // q rows per tile (MMA M)
+constexpr int kN = 128;               // keys per tile (MMA N of QK^T, K of PV)
+constexpr int kHalf = kN / 2;         // S columns per softmax warpgroup
+constexpr int kSoftmaxThreads = 256;  // two warpgroups, one per column half
+constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
-constexpr int kRegsSoftmax = 208, kRegsOther = 88;
-// setmaxnreg.inc blocks until the CTA's pool (launch allocation: 168 x 384) has the registers
-static_assert(256 * kRegsSoftmax + 128 * kRegsOther <= 168 * 384, "register split exceeds the CTA pool");
+constexpr uint32_t kColS0 = 0, kColS1 = 128, kColP0 = 256, kColP1 = 320, kColO = 384;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only if the max grows by > 2^8
 // exponentials of pairs c with (c & kPolyMask) == kPolyMask use the FMA-pipe polynomial
 constexpr int kPolyMask = 1;
-
-__host__ __device__ constexpr uint32_t col_s(int q) { return q ? 256u : 0u; }
-__host__ __device__ constexpr uint32_t col_o(int q) { return q ? 384u : 128u; }
+constexpr int kBarSoftmax = 1;  // named barrier of the 8 softmax warps
 
 // 2^y on the FMA/ALU pipes: y = n + f, n = round(y), |f| <= 1/2, 2^f by a degree-3
 // polynomial fitted for relative error (7.7e-5 max, far below bf16's 3.9e-3), 2^n by
@@ -83,14 +79,19 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t *r) {
       : "memory");
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 template <int D>
 struct Cfg {
   static constexpr int kSlabs = D / 64;                  // 128-byte swizzle slabs per row
   static constexpr int kTileBytes = kM * D * 2;          // one Q / K / V tile in smem
   static constexpr int kSlabBytes = kM * 128;            // 128 rows x 128 B
   static constexpr int kNK = D == 128 ? 2 : 3;           // K ring stages
-  static constexpr int kNV = D == 128 ? 3 : 3;           // V ring stages
-  static constexpr int kSmemBytes = (2 + kNK + kNV) * kTileBytes + 1024;
+  static constexpr int kNV = D == 128 ? 2 : 3;           // V ring stages
+  static constexpr int kNQ = 2;                          // Q buffers (items in flight)
+  static constexpr int kSmemBytes = (kNQ + kNK + kNV) * kTileBytes + 1024;
 };
 
 struct TcParams {
@@ -101,19 +102,18 @@ struct TcParams {
   int batch, n_items, nql, G, n_sink;
   float scale_log2;
   const int32_t *win_q;
-  const int32_t *items;  // (q-head, q-tile pair) LPT order
+  const int32_t *items;  // (q-head, q-tile) LPT order
 };
 
 // debug tracing (env MOA_PREFILL_TRACE=1): (clock << 8 | event code) of CTA 0
 __device__ unsigned long long *g_trace = nullptr;
-__shared__ unsigned int s_trace_n[3];  // per role (MMA, softmax 0, softmax 1) event counters
-__device__ __forceinline__ void trace_ev(int code) {
+__shared__ unsigned int s_trace_n[5];
+__device__ __forceinline__ void trace_ev(int role, int code) {
   unsigned long long *tr = g_trace;
   if (tr && blockIdx.x == 0) {
     const unsigned long long t = clock64();
-    const int role = code >= 30 && code < 50 ? 1 + (code & 1) : 0;
     const unsigned int k = s_trace_n[role]++;
-    if (k < 20000) tr[1 + role * 20000 + k] = (t << 8) | (unsigned long long)code;
+    if (k < 12000) tr[1 + role * 12000 + k] = (t << 8) | (unsigned long long)code;
   }
 }
 
@@ -121,223 +121,155 @@ struct Bars {
   uint64_t q_full[2], q_empty[2];
   uint64_t k_full[4], k_empty[4];
   uint64_t v_full[4], v_empty[4];
-  uint64_t s_full[2], p_full[2];
-  uint64_t o_full[2], o_empty[2];
+  uint64_t s_full[2], p_full[2], pv_done[2];
+  uint64_t o_full, o_empty;
   uint32_t tmem_base;
 };
 
 struct Item {
   int b, h;
-  bool has[2];          // q tile present
-  int64_t i0[2], i1[2]; // first / last real row of each q tile
+  int64_t i0, i1;
   int W;
-  TileRanges tq[2];     // per q tile kv lists
-  TileRanges tu;        // union (the K/V stream)
+  TileRanges tr;
 };
-
-__device__ __forceinline__ bool in_ranges(const TileRanges &r, int t) {
-  return (t >= r.a0 && t < r.a1) || (t >= r.b0 && t < r.b1);
-}
 
 __device__ __forceinline__ Item get_item(const TcParams &p, int idx) {
   Item it;
   const int wi = idx / p.batch;
   it.b = idx - wi * p.batch;
   it.h = p.items[2 * wi];
-  const int qp = p.items[2 * wi + 1];
+  const int qt = p.items[2 * wi + 1];
+  it.i0 = (int64_t)qt * kM;
+  it.i1 = (p.N < it.i0 + kM ? p.N : it.i0 + kM) - 1;
   it.W = p.win_q[it.h];
-  for (int q = 0; q < 2; ++q) {
-    it.i0[q] = (int64_t)(2 * qp + q) * kM;
-    it.has[q] = it.i0[q] < p.N;
-    it.i1[q] = (p.N < it.i0[q] + kM ? p.N : it.i0[q] + kM) - 1;
-    if (it.has[q]) {
-      it.tq[q] = kv_tile_ranges(it.i0[q], it.i1[q], it.W, p.n_sink);
-    } else {
-      it.tq[q].a0 = it.tq[q].a1 = it.tq[q].b0 = it.tq[q].b1 = 0;
-    }
-  }
-  it.tu = kv_tile_ranges(it.i0[0], it.has[1] ? it.i1[1] : it.i1[0], it.W, p.n_sink);
+  it.tr = kv_tile_ranges(it.i0, it.i1, it.W, p.n_sink);
   return it;
 }
 
-
 // ------------------------------------------------------------------------------------------
-// MMA issuer (one thread).  Per q tile: S_q(list[k]) then, once P_q(k) is in TMEM, PV_q(k)
-// followed by S_q(k+1).  Both q tiles interleave: S0 S1 | PV0 S0' | PV1 S1' | ...
+// MMA issuer: whole warp 9 walks the schedule, one elected lane issues tcgen05 ops.
+// Order per item: S(t) [then PV(t-1)] for each tile, PV(last).
 // ------------------------------------------------------------------------------------------
-struct MmaQ {
-  int n = 0;        // tiles of this q tile in the current item
-  int s_next = 0;   // next S to issue
-  int pv_next = 0;  // next PV to issue
-  int pcnt = 0;     // P handoffs consumed (global)
-  int ocnt = 0;     // items finished (global)
-  int qcnt = 0;     // Q loads consumed (global)
-};
-
-template <int D, int Q>
-__device__ __forceinline__ int union_index(const Item &it, int k) {
-  const int t = it.tq[Q].at(k);
-  return t < it.tu.a1 ? t - it.tu.a0 : (it.tu.a1 - it.tu.a0) + (t - it.tu.b0);
-}
-
-__device__ __forceinline__ uint32_t users_of(const Item &it, int u) {
-  const int t = it.tu.at(u);
-  return (in_ranges(it.tq[0], t) ? 1u : 0u) | (in_ranges(it.tq[1], t) ? 2u : 0u);
-}
-
-template <int D, int Q>
-__device__ __forceinline__ void issue_s(const Item &it, MmaQ &st, int T0, uint32_t &kbits, Bars &bars,
-                                        uint32_t tmem, uint64_t qdesc, uint64_t kdesc0) {
-  using C = Cfg<D>;
-  constexpr uint32_t idesc_s = idesc_bf16_f32(kM, kN, false);
-  const int u = union_index<D, Q>(it, st.s_next);
-  const int Tu = T0 + u, ks = Tu % C::kNK;
-  mbar_wait(smem_u32(&bars.k_full[ks]), (Tu / C::kNK) & 1);
-  if ((threadIdx.x & 31) == 0) trace_ev(60 + Q);
-  tc_fence_after();
-  // descriptors: the 14-bit start-address field advances by (byte offset >> 4)
-  const uint64_t kdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
-  kbits |= (1u << Q) << (2 * ks);
-  const bool k_done = ((kbits >> (2 * ks)) & 3u) == users_of(it, u);  // every user of this K stage issued
-  if (k_done) kbits &= ~(3u << (2 * ks));
-  const bool q_done = ++st.s_next == st.n;
-  if (elect_one()) {
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      const uint32_t off = ((kk >> 2) * C::kSlabBytes + (kk & 3) * 32) >> 4;
-      mma_ss(tmem + col_s(Q), qdesc + off, kdesc + off, idesc_s, kk > 0 ? 1u : 0u);
-    }
-    mma_commit(smem_u32(&bars.s_full[Q]));
-    if (k_done) mma_commit(smem_u32(&bars.k_empty[ks]));
-    if (q_done) mma_commit(smem_u32(&bars.q_empty[Q]));
-    trace_ev(10 + Q);
-  }
-  __syncwarp();
-}
-
-template <int D, int Q>
-__device__ __forceinline__ void issue_pv(const Item &it, MmaQ &st, int T0, uint32_t &vbits, Bars &bars,
-                                         uint32_t tmem, uint64_t vdesc0) {
-  using C = Cfg<D>;
-  constexpr uint32_t idesc_o = idesc_bf16_f32(kM, D, true);
-  const int u = union_index<D, Q>(it, st.pv_next);
-  const int Tu = T0 + u, vs = Tu % C::kNV;
-  mbar_wait(smem_u32(&bars.v_full[vs]), (Tu / C::kNV) & 1);
-  mbar_wait(smem_u32(&bars.p_full[Q]), st.pcnt & 1);
-  if ((threadIdx.x & 31) == 0) trace_ev(50 + Q);
-  ++st.pcnt;
-  if (st.pv_next == 0 && st.ocnt > 0) mbar_wait(smem_u32(&bars.o_empty[Q]), (st.ocnt - 1) & 1);
-  tc_fence_after();
-  // B = V tile, MN-major SW128: 16 keys = two 8-row groups of 1024 B; N slabs 16 KB apart
-  const uint64_t vdesc = vdesc0 + (uint64_t)((vs * C::kTileBytes) >> 4);
-  const uint32_t acc0 = st.pv_next == 0 ? 0u : 1u;
-  vbits |= (1u << Q) << (2 * vs);
-  const bool v_done = ((vbits >> (2 * vs)) & 3u) == users_of(it, u);
-  if (v_done) vbits &= ~(3u << (2 * vs));
-  const bool o_done = ++st.pv_next == st.n;
-  if (o_done) ++st.ocnt;
-  if (elect_one()) {
-#pragma unroll
-    for (int kk = 0; kk < kN / 16; ++kk)
-      mma_ts(tmem + col_o(Q), tmem + col_s(Q) + kk * 8, vdesc + (uint64_t)((kk * 2048) >> 4), idesc_o,
-             kk == 0 ? acc0 : 1u);
-    if (v_done) mma_commit(smem_u32(&bars.v_empty[vs]));
-    if (o_done) mma_commit(smem_u32(&bars.o_full[Q]));
-    trace_ev(20 + Q);
-  }
-  __syncwarp();
-}
-
 template <int D>
 __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t tmem, uint32_t q_smem,
-                                        uint32_t k_smem, uint32_t v_smem, int total) {
+                                         uint32_t k_smem, uint32_t v_smem, int total) {
   using C = Cfg<D>;
+  constexpr uint32_t idesc_s = idesc_bf16_f32(kM, kN, false);
+  constexpr uint32_t idesc_o = idesc_bf16_f32(kM, D, true);
   const uint64_t qdesc0 = smem_desc_sw128(q_smem, 16, 1024);
-  const uint64_t qdesc1 = smem_desc_sw128(q_smem + C::kTileBytes, 16, 1024);
   const uint64_t kdesc0 = smem_desc_sw128(k_smem, 16, 1024);
   const uint64_t vdesc0 = smem_desc_sw128(v_smem, C::kSlabBytes, 1024);
-  MmaQ q0, q1;
-  uint32_t kbits = 0, vbits = 0;
-  int T = 0;
-  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-    const Item it = get_item(p, idx);
-    const int T0 = T;
-    q0.n = it.tq[0].count();
-    q1.n = it.tq[1].count();
-    q0.s_next = q0.pv_next = q1.s_next = q1.pv_next = 0;
-    if (q0.n) mbar_wait(smem_u32(&bars.q_full[0]), q0.qcnt++ & 1);
-    if (q1.n) mbar_wait(smem_u32(&bars.q_full[1]), q1.qcnt++ & 1);
-    if (q0.n) issue_s<D, 0>(it, q0, T0, kbits, bars, tmem, qdesc0, kdesc0);
-    if (q1.n) issue_s<D, 1>(it, q1, T0, kbits, bars, tmem, qdesc1, kdesc0);
-    while (q0.pv_next < q0.n || q1.pv_next < q1.n) {
-      if (q0.pv_next < q0.n) {
-        issue_pv<D, 0>(it, q0, T0, vbits, bars, tmem, vdesc0);
-        if (q0.s_next < q0.n) issue_s<D, 0>(it, q0, T0, kbits, bars, tmem, qdesc0, kdesc0);
-      }
-      if (q1.pv_next < q1.n) {
-        issue_pv<D, 1>(it, q1, T0, vbits, bars, tmem, vdesc0);
-        if (q1.s_next < q1.n) issue_s<D, 1>(it, q1, T0, kbits, bars, tmem, qdesc1, kdesc0);
-      }
+  int n = 0, T = 0;
+  auto issue_pv = [&](int Tp, bool first_of_item, bool last_of_item, int item_n) {
+    const int vs = Tp % C::kNV, pb = Tp & 1;
+    mbar_wait(smem_u32(&bars.v_full[vs]), (Tp / C::kNV) & 1);
+    mbar_wait(smem_u32(&bars.p_full[pb]), (Tp >> 1) & 1);
+    if ((threadIdx.x & 31) == 0) trace_ev(0, 50);
+    if (first_of_item && item_n > 0) mbar_wait(smem_u32(&bars.o_empty), (item_n - 1) & 1);
+    tc_fence_after();
+    // B = V tile, MN-major SW128: 16 keys = two 8-row groups of 1024 B; N slabs 16 KB apart
+    const uint64_t vdesc = vdesc0 + (uint64_t)((vs * C::kTileBytes) >> 4);
+    const uint32_t pcol = tmem + (pb ? kColP1 : kColP0);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < kN / 16; ++kk)
+        mma_ts(tmem + kColO, pcol + kk * 8, vdesc + (uint64_t)((kk * 2048) >> 4), idesc_o,
+               (first_of_item && kk == 0) ? 0u : 1u);
+      mma_commit(smem_u32(&bars.v_empty[vs]));
+      mma_commit(smem_u32(&bars.pv_done[pb]));
+      if (last_of_item) mma_commit(smem_u32(&bars.o_full));
+      trace_ev(0, 20);
     }
-    T = T0 + it.tu.count();
+    __syncwarp();
+  };
+  for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++n) {
+    const Item it = get_item(p, idx);
+    const int qb = n % C::kNQ;
+    mbar_wait(smem_u32(&bars.q_full[qb]), (n / C::kNQ) & 1);
+    const uint64_t qdesc = qdesc0 + (uint64_t)((qb * C::kTileBytes) >> 4);
+    const int nt = it.tr.count();
+    for (int t = 0; t < nt; ++t, ++T) {
+      const int ks = T % C::kNK, sb = T & 1;
+      mbar_wait(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
+      if ((threadIdx.x & 31) == 0) trace_ev(0, 60);
+      if (T >= 2) mbar_wait(smem_u32(&bars.p_full[sb]), ((T - 2) >> 1) & 1);  // S[sb] consumed
+      if ((threadIdx.x & 31) == 0) trace_ev(0, 61);
+      tc_fence_after();
+      const uint64_t kdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * C::kSlabBytes + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + (sb ? kColS1 : kColS0), qdesc + off, kdesc + off, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(smem_u32(&bars.s_full[sb]));
+        mma_commit(smem_u32(&bars.k_empty[ks]));
+        if (t == nt - 1) mma_commit(smem_u32(&bars.q_empty[qb]));
+        trace_ev(0, 10);
+      }
+      __syncwarp();
+      if (t > 0) issue_pv(T - 1, t == 1, false, n);
+    }
+    issue_pv(T - 1, nt == 1, true, n);
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// softmax warpgroup of q tile Q: thread t owns row t (TMEM lane t)
+// softmax warpgroup W (column half W of S); thread owns row = TMEM lane
 // ------------------------------------------------------------------------------------------
-template <int D, int Q>
+template <int D, int W>
 __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint32_t tmem, int total, int tid,
-                                             int warp) {
+                                             int warp, float (*red_max)[2][kM], float (*red_l)[kM]) {
   const int row = tid & 127;
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-  int scnt = 0, ocnt = 0;
-  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+  constexpr int c0 = W * kHalf;        // first S column of this half
+  constexpr int oc0 = W * (D / 2);     // first O column of this half
+  int n = 0, T = 0;
+  for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++n) {
     const Item it = get_item(p, idx);
-    if (!it.has[Q]) continue;
-    const int64_t i0 = it.i0[Q], i1 = it.i1[Q];
-    const TileRanges tr = it.tq[Q];
-    const int64_t i = i0 + row;
-    const int nt = tr.count();
+    const int64_t i = it.i0 + row;
+    const int nt = it.tr.count();
     float m_used = -INFINITY, l = 0.f;
-    for (int t = 0; t < nt; ++t, ++scnt) {
-      const int kt = tr.at(t);
+    for (int t = 0; t < nt; ++t, ++T) {
+      const int sb = T & 1;
+      const int kt = it.tr.at(t);
       const int64_t j0 = (int64_t)kt * kN;
-      const bool full = kv_tile_full(i0, i1, kt, it.W, p.n_sink);
-      mbar_wait(smem_u32(&bars.s_full[Q]), scnt & 1);
+      const bool full = kv_tile_full(it.i0, it.i1, kt, it.W, p.n_sink);
+      mbar_wait(smem_u32(&bars.s_full[sb]), (T >> 1) & 1);
       tc_fence_after();
-      if (row == 0) trace_ev(30 + Q);
-      // S row -> registers: four 32-column TMEM loads in flight, one wait
-      uint32_t sr[kN];
+      if (row == 0) trace_ev(1 + W, 30 + W);
+      uint32_t sr[kHalf];
       {
-        const uint32_t sa = tmem + lane_off + col_s(Q);
-#pragma unroll
-        for (int c = 0; c < kN / 32; ++c) tmem_ld32(sa + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+        const uint32_t sa = tmem + lane_off + (sb ? kColS1 : kColS0) + c0;
+        tmem_ld32(sa, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        tmem_ld32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
         tmem_wait_ld();
       }
-      float x[kN];
+      float x[kHalf];
 #pragma unroll
-      for (int c = 0; c < kN; ++c) x[c] = __uint_as_float(sr[c]);
+      for (int c = 0; c < kHalf; ++c) x[c] = __uint_as_float(sr[c]);
       if (!full) {
         // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  c > i-j0-W)
-        const int dd = (int)(i - j0), sl = (int)(p.n_sink - j0), lo = dd - it.W;
+        const int dd = (int)(i - j0) - c0, sl = (int)(p.n_sink - j0) - c0, lo = dd - it.W;
 #pragma unroll
-        for (int c = 0; c < kN; ++c) {
+        for (int c = 0; c < kHalf; ++c) {
           const bool vis = c <= dd && (c < sl || c > lo);
           if (!vis) x[c] = -INFINITY;
         }
       }
-      // row max of the raw scores (tree), scaled to log2 units (scale > 0 commutes with max)
       float mx[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        mx[k] = fmaxf(fmaxf(fmaxf(x[k], x[k + 16]), fmaxf(x[k + 32], x[k + 48])),
-                      fmaxf(fmaxf(x[k + 64], x[k + 80]), fmaxf(x[k + 96], x[k + 112])));
+      for (int k = 0; k < 16; ++k) mx[k] = fmaxf(fmaxf(x[k], x[k + 16]), fmaxf(x[k + 32], x[k + 48]));
 #pragma unroll
       for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
         for (int k = 0; k < w; ++k) mx[k] = fmaxf(mx[k], mx[k + w]);
-      const float mt = mx[0] * p.scale_log2;
+      // row max of both halves (raw scores; scale > 0 commutes with max)
+      red_max[sb][W][row] = mx[0];
+      if (row == 0) trace_ev(1 + W, 70 + W);
+      named_bar_sync(kBarSoftmax, kSoftmaxThreads);
+      if (row == 0) trace_ev(1 + W, 72 + W);
+      const float mt = fmaxf(mx[0], red_max[sb][1 - W][row]) * p.scale_log2;
       bool rescale = false;
       float alpha = 1.f;
       if (m_used == -INFINITY) {
@@ -348,11 +280,13 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
         m_used = mt;
       }
       if (__any_sync(0xffffffffu, rescale)) {
-        // S_Q(t) complete => PV_Q(t-1) complete (in-order tcgen05): O is final for t-1
+        // O must hold PV(T-1) before it is rescaled (this half of its columns)
+        mbar_wait(smem_u32(&bars.pv_done[(T - 1) & 1]), ((T - 1) >> 1) & 1);
+        tc_fence_after();
         uint32_t r[32];
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          const uint32_t oa = tmem + lane_off + col_o(Q) + c * 32;
+        for (int c = 0; c < D / 64; ++c) {
+          const uint32_t oa = tmem + lane_off + kColO + oc0 + c * 32;
           tmem_ld32(oa, r);
           tmem_wait_ld();
 #pragma unroll
@@ -363,9 +297,9 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
       l *= alpha;
       const float nmref = m_used == -INFINITY ? 0.f : -m_used;
       float ps[4] = {0.f, 0.f, 0.f, 0.f};
-      const uint32_t pa = tmem + lane_off + col_s(Q);  // P aliases the first 64 S columns
+      const uint32_t pa = tmem + lane_off + (sb ? kColP1 : kColP0) + W * (kHalf / 2);
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
+      for (int ch = 0; ch < 2; ++ch) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -383,22 +317,24 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
       l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
       tmem_wait_st();
       tc_fence_before();
-      if (row == 0) trace_ev(40 + Q);
-      mbar_arrive(smem_u32(&bars.p_full[Q]));
+      if (row == 0) trace_ev(1 + W, 40 + W);
+      mbar_arrive(smem_u32(&bars.p_full[sb]));
     }
-    // epilogue: O / l -> bf16 rows, lse
-    mbar_wait(smem_u32(&bars.o_full[Q]), ocnt & 1);
-    ++ocnt;
+    // epilogue: O / l -> bf16 rows (this half of the columns), lse
+    red_l[W][row] = l;
+    mbar_wait(smem_u32(&bars.o_full), n & 1);
+    named_bar_sync(kBarSoftmax, kSoftmaxThreads);
+    const float lt = l + red_l[1 - W][row];
     tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16 *orow =
-        static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride + (int64_t)it.h * D;
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    __nv_bfloat16 *orow = static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride +
+                          (int64_t)it.h * D + oc0;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < D / 64; ++c) {
       uint32_t r[32];
-      tmem_ld32(tmem + lane_off + col_o(Q) + c * 32, r);
+      tmem_ld32(tmem + lane_off + kColO + oc0 + c * 32, r);
       tmem_wait_ld();
-      if (i <= i1) {
+      if (i <= it.i1) {
         uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
 #pragma unroll
         for (int v4 = 0; v4 < 4; ++v4) {
@@ -411,10 +347,10 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
         }
       }
     }
-    if (p.lse && i <= i1)
-      p.lse[((int64_t)it.b * p.nql + it.h) * p.N + i] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
+    if (W == 0 && p.lse && i <= it.i1)
+      p.lse[((int64_t)it.b * p.nql + it.h) * p.N + i] = lt > 0.f ? (m_used + __log2f(lt)) * kLn2 : -INFINITY;
     tc_fence_before();
-    mbar_arrive(smem_u32(&bars.o_empty[Q]));
+    mbar_arrive(smem_u32(&bars.o_empty));
   }
 }
 
@@ -425,23 +361,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ Bars bars;
+  __shared__ float red_max[2][2][kM];  // [tile parity][half][row]
+  __shared__ float red_l[2][kM];       // [half][row]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t q_smem = smem_base;                                   // Q0, Q1
-  const uint32_t k_smem = q_smem + 2 * C::kTileBytes;                  // kNK tiles
-  const uint32_t v_smem = k_smem + C::kNK * C::kTileBytes;             // kNV tiles
+  const uint32_t q_smem = smem_base;                        // 2 tiles
+  const uint32_t k_smem = q_smem + C::kNQ * C::kTileBytes;  // kNK tiles
+  const uint32_t v_smem = k_smem + C::kNK * C::kTileBytes;  // kNV tiles
   const int total = p.n_items * p.batch;
 
   if (tid == 0) {
-    s_trace_n[0] = s_trace_n[1] = s_trace_n[2] = 0;
+    s_trace_n[0] = s_trace_n[1] = s_trace_n[2] = s_trace_n[3] = s_trace_n[4] = 0;
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&bars.q_full[i]), 1);
       mbar_init(smem_u32(&bars.q_empty[i]), 1);
       mbar_init(smem_u32(&bars.s_full[i]), 1);
       mbar_init(smem_u32(&bars.p_full[i]), kSoftmaxThreads);
-      mbar_init(smem_u32(&bars.o_full[i]), 1);
-      mbar_init(smem_u32(&bars.o_empty[i]), kSoftmaxThreads);
+      mbar_init(smem_u32(&bars.pv_done[i]), 1);
     }
     for (int i = 0; i < C::kNK; ++i) {
       mbar_init(smem_u32(&bars.k_full[i]), 1);
@@ -451,6 +388,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&bars.v_full[i]), 1);
       mbar_init(smem_u32(&bars.v_empty[i]), 1);
     }
+    mbar_init(smem_u32(&bars.o_full), 1);
+    mbar_init(smem_u32(&bars.o_empty), kSoftmaxThreads);
     fence_mbar_init();
   }
   if (warp == 9) tmem_alloc<kTmemCols>(smem_u32(&bars.tmem_base));
@@ -463,42 +402,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
-  // register budget: the producer / MMA warpgroup gives registers to the softmax warpgroups
-  if (warp >= 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsOther) : "memory");
+
   if (warp == 8 || warp == 10) {
     // ------------------------------------------------------------------ TMA producers
-    // warp 8: Q tiles + K ring; warp 10: V ring (a V stage waits for the later PV of the
-    // two q tiles, which must not hold back the next K loads)
     if (lane == 0) {
       const bool kq = warp == 8;
-      int T = 0;
-      int qcnt[2] = {0, 0};  // Q tile loads per slot
-      for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      int n = 0, T = 0;
+      for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++n) {
         const Item it = get_item(p, idx);
         const int g = it.h / p.G;
         if (kq) {
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            if (!it.has[q]) continue;
-            // Q_q of this item may overwrite the previous Q_q once its last S_q completed
-            if (qcnt[q] >= 1) mbar_wait(smem_u32(&bars.q_empty[q]), (qcnt[q] - 1) & 1);
-            ++qcnt[q];
-            const uint32_t qbar = smem_u32(&bars.q_full[q]);
-            mbar_expect_tx(qbar, C::kTileBytes);
-            for (int sl = 0; sl < C::kSlabs; ++sl)
-              tma_load_4d(q_smem + q * C::kTileBytes + sl * C::kSlabBytes, &tm_q, qbar, sl * 64, it.h,
-                          (int)it.i0[q], it.b);
-          }
+          const int qb = n % C::kNQ;
+          if (n >= C::kNQ) mbar_wait(smem_u32(&bars.q_empty[qb]), ((n - C::kNQ) / C::kNQ) & 1);
+          const uint32_t qbar = smem_u32(&bars.q_full[qb]);
+          mbar_expect_tx(qbar, C::kTileBytes);
+          for (int sl = 0; sl < C::kSlabs; ++sl)
+            tma_load_4d(q_smem + qb * C::kTileBytes + sl * C::kSlabBytes, &tm_q, qbar, sl * 64, it.h, (int)it.i0,
+                        it.b);
         }
-        const int nu = it.tu.count();
-        for (int u = 0; u < nu; ++u, ++T) {
-          const int j0 = it.tu.at(u) * kN;
+        const int nt = it.tr.count();
+        for (int t = 0; t < nt; ++t, ++T) {
+          const int j0 = it.tr.at(t) * kN;
           if (kq) {
             const int ks = T % C::kNK;
             if (T >= C::kNK) mbar_wait(smem_u32(&bars.k_empty[ks]), ((T - C::kNK) / C::kNK) & 1);
             const uint32_t kbar = smem_u32(&bars.k_full[ks]);
             mbar_expect_tx(kbar, C::kTileBytes);
+            trace_ev(3, 80);
             for (int sl = 0; sl < C::kSlabs; ++sl)
               tma_load_4d(k_smem + ks * C::kTileBytes + sl * C::kSlabBytes, &tm_k, kbar, sl * 64, g, j0, it.b);
           } else {
@@ -506,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (T >= C::kNV) mbar_wait(smem_u32(&bars.v_empty[vs]), ((T - C::kNV) / C::kNV) & 1);
             const uint32_t vbar = smem_u32(&bars.v_full[vs]);
             mbar_expect_tx(vbar, C::kTileBytes);
+            trace_ev(4, 81);
             for (int sl = 0; sl < C::kSlabs; ++sl)
               tma_load_4d(v_smem + vs * C::kTileBytes + sl * C::kSlabBytes, &tm_v, vbar, sl * 64, g, j0, it.b);
           }
@@ -513,14 +444,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 9) {
-    mma_role<D>(p, bars, tmem, q_smem, k_smem, v_smem, total);  // whole warp; one elected lane issues
-  }  // warp 11: idle
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax) : "memory");
-    if (warp < 4)
-      softmax_role<D, 0>(p, bars, tmem, total, tid, warp);
-    else
-      softmax_role<D, 1>(p, bars, tmem, total, tid, warp);
+    mma_role<D>(p, bars, tmem, q_smem, k_smem, v_smem, total);
+  } else if (warp < 4) {
+    softmax_role<D, 0>(p, bars, tmem, total, tid, warp, red_max, red_l);
+  } else if (warp < 8) {
+    softmax_role<D, 1>(p, bars, tmem, total, tid, warp, red_max, red_l);
   }
 
   tc_fence_before();
@@ -601,17 +529,17 @@ int launch_d(const PrefillArgs &a, void *stream) {
   p.o_row_stride = a.o_row_stride;
   p.N = a.N;
   p.batch = a.batch;
-  p.n_items = a.n_pairs;
+  p.n_items = a.n_items;
   p.nql = a.nql;
   p.G = a.G;
   p.n_sink = a.n_sink;
   p.scale_log2 = a.scale * kLog2e;
   p.win_q = a.d_win_q;
-  p.items = a.d_pairs;
+  p.items = a.d_items;
   cudaError_t e = cudaFuncSetAttribute(prefill_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        C::kSmemBytes);
   if (e != cudaSuccess) return (int)e;
-  const int total = a.n_pairs * a.batch;
+  const int total = a.n_items * a.batch;
   static unsigned long long *trace_buf = nullptr;
   static bool trace_on = std::getenv("MOA_PREFILL_TRACE") != nullptr;
   if (trace_on) {
@@ -619,6 +547,7 @@ int launch_d(const PrefillArgs &a, void *stream) {
     cudaMemsetAsync(trace_buf, 0, 65536 * 8, (cudaStream_t)stream);
     cudaMemcpyToSymbolAsync(g_trace, &trace_buf, sizeof(trace_buf), 0, cudaMemcpyHostToDevice, (cudaStream_t)stream);
   }
+
   const int grid = total < num_sms() ? total : num_sms();
   prefill_tc_kernel<D><<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, p);
   if (trace_on) {
@@ -626,8 +555,6 @@ int launch_d(const PrefillArgs &a, void *stream) {
     cudaMemcpy(h.data(), trace_buf, 65536 * 8, cudaMemcpyDeviceToHost);
     FILE *f = fopen("gpurun_out/prefill_trace.txt", "w");
     if (f) {
-      const unsigned n = (unsigned)(h[0] & 0xffffffffu);
-      (void)n;
       for (unsigned k = 0; k < 60000; ++k)
         if (h[1 + k]) fprintf(f, "%llu %llu\n", h[1 + k] >> 8, h[1 + k] & 255);
       fclose(f);

@@ -81,7 +81,7 @@ void free_tables(LayerPlan &p) {
   p.d_tables = nullptr;
   p.d_win_q = p.d_win_g = nullptr;
   p.d_g_off = nullptr;
-  p.d_items = p.d_pairs = p.d_chunks = p.d_g_chunk = nullptr;
+  p.d_items = p.d_chunks = p.d_g_chunk = nullptr;
   p.d_counters = nullptr;
 }
 
@@ -93,8 +93,7 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   size_t o_wing = align16(o_winq + p.win_q.size() * 4);
   size_t o_goff = align16(o_wing + p.win_g.size() * 4);
   size_t o_items = align16(o_goff + p.g_off.size() * 8);
-  size_t o_pairs = align16(o_items + p.items.size() * 4);
-  size_t o_chunks = align16(o_pairs + p.pairs.size() * 4);
+  size_t o_chunks = align16(o_items + p.items.size() * 4);
   size_t o_gch = align16(o_chunks + p.chunks.size() * 4);
   size_t o_cnt = align16(o_gch + p.g_chunk.size() * 4);
   size_t total = align16(o_cnt + (size_t)ctx->max_batch * ctx->ngl * 4);
@@ -103,7 +102,6 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   std::memcpy(host.data() + o_wing, p.win_g.data(), p.win_g.size() * 4);
   std::memcpy(host.data() + o_goff, p.g_off.data(), p.g_off.size() * 8);
   std::memcpy(host.data() + o_items, p.items.data(), p.items.size() * 4);
-  std::memcpy(host.data() + o_pairs, p.pairs.data(), p.pairs.size() * 4);
   std::memcpy(host.data() + o_chunks, p.chunks.data(), p.chunks.size() * 4);
   std::memcpy(host.data() + o_gch, p.g_chunk.data(), p.g_chunk.size() * 4);
   DeviceGuard dg(ctx->device);
@@ -122,7 +120,6 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   p.d_win_g = reinterpret_cast<const int32_t *>(b + o_wing);
   p.d_g_off = reinterpret_cast<const int64_t *>(b + o_goff);
   p.d_items = reinterpret_cast<const int32_t *>(b + o_items);
-  p.d_pairs = reinterpret_cast<const int32_t *>(b + o_pairs);
   p.d_chunks = reinterpret_cast<const int32_t *>(b + o_chunks);
   p.d_g_chunk = reinterpret_cast<const int32_t *>(b + o_gch);
   p.d_counters = reinterpret_cast<int *>(b + o_cnt);
@@ -252,41 +249,34 @@ moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_he
   }
   np.rows_per_seq = off;
 
-  // prefill work items, longest (most kv tiles) first
+  // prefill work items (h_local, q_tile).  Order: heads by total kv-tile count, heaviest
+  // first (so the kernel tail holds light work), and the q tiles of one head consecutively,
+  // heaviest first: CTAs running concurrently then share their heads' K/V tiles in L2.
   const int nqt = (int)((N + moa::kTile - 1) / moa::kTile);
-  struct It { int h, qt, cnt; };
+  struct It { int h, qt, cnt; int64_t hcost; };
   std::vector<It> its;
   its.reserve((size_t)ctx->nql * nqt);
-  for (int h = 0; h < ctx->nql; ++h)
+  for (int h = 0; h < ctx->nql; ++h) {
+    const size_t first = its.size();
+    int64_t hc = 0;
     for (int qt = 0; qt < nqt; ++qt) {
       int64_t i0 = (int64_t)qt * moa::kTile;
       int64_t i1 = std::min<int64_t>(N, i0 + moa::kTile) - 1;
-      its.push_back({h, qt, moa::kv_tile_ranges(i0, i1, np.win_q[h], n_sink).count()});
+      const int c = moa::kv_tile_ranges(i0, i1, np.win_q[h], n_sink).count();
+      hc += c;
+      its.push_back({h, qt, c, 0});
     }
-  std::stable_sort(its.begin(), its.end(), [](const It &a, const It &b) { return a.cnt > b.cnt; });
+    for (size_t k = first; k < its.size(); ++k) its[k].hcost = hc;
+  }
+  std::stable_sort(its.begin(), its.end(), [](const It &a, const It &b) {
+    if (a.hcost != b.hcost) return a.hcost > b.hcost;
+    if (a.h != b.h) return a.h < b.h;
+    return a.cnt > b.cnt;
+  });
   np.items.resize(its.size() * 2);
   for (size_t i = 0; i < its.size(); ++i) {
     np.items[2 * i] = its[i].h;
     np.items[2 * i + 1] = its[i].qt;
-  }
-  // tensor-core kernel: two adjacent q tiles share one K/V stream (the union of their lists)
-  const int nqp = (nqt + 1) / 2;
-  its.clear();
-  for (int h = 0; h < ctx->nql; ++h)
-    for (int qp = 0; qp < nqp; ++qp) {
-      int64_t i0 = (int64_t)qp * 2 * moa::kTile;
-      int64_t i1 = std::min<int64_t>(N, i0 + 2 * moa::kTile) - 1;
-      int64_t i1a = std::min<int64_t>(N, i0 + moa::kTile) - 1;
-      int cnt = moa::kv_tile_ranges(i0, i1a, np.win_q[h], n_sink).count();
-      if (i1 > i1a) cnt += moa::kv_tile_ranges(i1a + 1, i1, np.win_q[h], n_sink).count();
-      (void)i1;
-      its.push_back({h, qp, cnt});
-    }
-  std::stable_sort(its.begin(), its.end(), [](const It &a, const It &b) { return a.cnt > b.cnt; });
-  np.pairs.resize(its.size() * 2);
-  for (size_t i = 0; i < its.size(); ++i) {
-    np.pairs[2 * i] = its[i].h;
-    np.pairs[2 * i + 1] = its[i].qt;
   }
 
   // decode work list: split every group region into chunks of ~chunk_rows rows
@@ -474,7 +464,6 @@ moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, co
   a.batch = batch; a.N = N; a.scale = scale; a.lse = lse_out; a.n_sink = p.n_sink;
   a.nql = ctx->nql; a.G = ctx->G; a.d = ctx->d;
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
-  a.d_pairs = p.d_pairs; a.n_pairs = (int)(p.pairs.size() / 2);
   int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_tc(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
   moa::CacheArgs c{};

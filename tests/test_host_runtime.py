@@ -111,7 +111,9 @@ def test_prefill_tile_schedule_is_exact(moa, N, s):
                 assert e == (not full[t]), (h, W, qt, t)
 
 
-def test_prefill_items_lpt_permutation(moa):
+def test_prefill_items_head_grouped_order(moa):
+    """A permutation of every (head, q tile); heads heaviest first, each head's
+    q tiles consecutive and heaviest first."""
     N, s = 1000, 64
     windows = [5, 900, 300, 64, 1000, 0]
     c = _ctx(moa, Hq=6, Hkv=6, B=1)
@@ -119,8 +121,14 @@ def test_prefill_items_lpt_permutation(moa):
     items = c.prefill_items(0)
     nqt = (N + 127) // 128
     assert sorted(items) == [(h, q) for h in range(6) for q in range(nqt)]
-    counts = [len(c.prefill_tiles(0, h, q)[0]) for h, q in items]
-    assert counts == sorted(counts, reverse=True)
+    cnt = {(h, q): len(c.prefill_tiles(0, h, q)[0]) for h, q in items}
+    heads = [h for i, (h, q) in enumerate(items) if i == 0 or items[i - 1][0] != h]
+    assert sorted(heads) == list(range(6))          # each head appears as one run
+    hcost = [sum(cnt[(h, q)] for q in range(nqt)) for h in heads]
+    assert hcost == sorted(hcost, reverse=True)
+    for h in heads:
+        run = [cnt[(hh, q)] for hh, q in items if hh == h]
+        assert run == sorted(run, reverse=True)
 
 
 def test_decode_chunks_cover_each_region_once(moa):
