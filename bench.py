@@ -275,11 +275,15 @@ def run_ours(args, rank, world, local_rank):
     pk_total_s = sum(pk_ms) / 1e3 / K_steps
     achieved_tf = flops / pk_total_s / 1e12
     clocks = clk.summary()
-    traffic = None
+    traffic, traffic_note = None, None
     tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("bytes_per_launch")
+        traffic_note = (f"dram read+write of one {tj.get('launch')} launch ({tj.get('source')}); "
+                        f"its algorithmic bytes {tj.get('algorithmic_bytes_same_launch')}, "
+                        f"ratio {tj.get('traffic_over_algorithmic'):.3f}")
 
     # ---------------- e2e: host buffers through the public API, H2D/D2H inside the timed region
     e2e = run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev)
@@ -305,7 +309,7 @@ def run_ours(args, rank, world, local_rank):
                                              "(tcgen05 attention kernel + cache fill)"}},
             "decode_ms_per_step": dec / K_steps,
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic,
+                         "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic, "traffic_note": traffic_note,
                          "kernel": "moa decode_kernel (fused append + split-KV + last-CTA combine)",
                          "bytes_per_launch": dec_bytes_per_launch, "avg_launch_ms": dk_avg_ms,
                          "peak_source": peak_src},
