@@ -176,3 +176,39 @@ def test_c3_gqa_prefill_slice(moa):
 
 def test_c4_full_layer_prefill(moa):
     _full_layer_prefill(moa, "C4", 33)
+
+
+def test_kv_sharded_contexts_on_one_gpu(moa):
+    """Two contexts serving kv-groups [0,2) and [2,4) on head-sliced views of
+    full tensors (row strides of the full layout): prefill and decode outputs
+    of the shards, concatenated by heads, equal the oracle for all heads."""
+    from paper_2406_14909_b200 import dist as mdist
+    dev = torch.device("cuda")
+    B, N, Hq, Hkv, d, s = 2, 300, 8, 4, 128, 4
+    W = [3, 200, 0, 77, 128, 129, 1, 300]
+    G = Hq // Hkv
+    q = normal((B, N, Hq, d), 301, torch.bfloat16)
+    k = normal((B, N, Hkv, d), 302, torch.bfloat16)
+    v = normal((B, N, Hkv, d), 303, torch.bfloat16)
+    qd = normal((B, Hq, d), 304, torch.bfloat16)
+    kd = normal((B, Hkv, d), 305, torch.bfloat16)
+    vd = normal((B, Hkv, d), 306, torch.bfloat16)
+    qg, kg, vg, qdg, kdg, vdg = (x.to(dev) for x in (q, k, v, qd, kd, vd))
+    o = torch.empty_like(qg)
+    od = torch.empty_like(qdg)
+    scale = 1 / math.sqrt(d)
+    for sh in mdist.plan_shards(2, Hkv, B, "kv"):
+        ctx = mdist.make_context(sh, 1, Hq, Hkv, d, device=0)
+        ctx.set_spans(0, W, s, N)
+        ctx.alloc_cache(B)
+        ws = ctx.alloc_workspace(B)
+        ctx.prefill(0, mdist.local_slice_q(qg, sh, G), mdist.local_slice_kv(kg, sh), mdist.local_slice_kv(vg, sh),
+                    mdist.local_slice_q(o, sh, G), scale)
+        ctx.decode_step_fused(0, mdist.local_slice_q(qdg, sh, G), mdist.local_slice_kv(kdg, sh),
+                              mdist.local_slice_kv(vdg, sh), mdist.local_slice_q(od, sh, G), N, scale, ws)
+    torch.cuda.synchronize()
+    O, _ = oracle.prefill(f64(q), f64(k), f64(v), W, s, scale)
+    assert np.abs(f64(o) - O).max() < 2e-2
+    Kh, Vh = torch.cat([k, kd[:, None]], 1), torch.cat([v, vd[:, None]], 1)
+    Od, _ = oracle.decode(f64(qd), f64(Kh), f64(Vh), N, W, s, scale)
+    assert np.abs(f64(od) - Od).max() < 2e-2
