@@ -124,6 +124,7 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *m, 
       : "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
     for (int64_t t0 = x; t0 < seg_end; t0 += kRows, ++T) {
       const int st = T % C::kStages;
       const int nrows = (int)((seg_end - t0) < kRows ? (seg_end - t0) : kRows);
-      mbar_wait(smem_u32(&full_bar[st]), (T / C::kStages) & 1);
+      mbar_wait_warp(smem_u32(&full_bar[st]), (T / C::kStages) & 1);
       const uint32_t kb = base + st * 2 * C::kTileBytes, vb = kb + C::kTileBytes;
       const int k0 = warp * 16;  // this warp's first key row in the tile
 

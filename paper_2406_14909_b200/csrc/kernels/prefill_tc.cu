@@ -80,6 +80,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t *r) {
 }
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
@@ -162,10 +163,10 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
   int n = 0, T = 0;
   auto issue_pv = [&](int Tp, bool first_of_item, bool last_of_item, int item_n) {
     const int vs = Tp % C::kNV, pb = Tp & 1;
-    mbar_wait(smem_u32(&bars.v_full[vs]), (Tp / C::kNV) & 1);
-    mbar_wait(smem_u32(&bars.p_full[pb]), (Tp >> 1) & 1);
+    mbar_wait_warp(smem_u32(&bars.v_full[vs]), (Tp / C::kNV) & 1);
+    mbar_wait_warp(smem_u32(&bars.p_full[pb]), (Tp >> 1) & 1);
     if ((threadIdx.x & 31) == 0) trace_ev(0, 50);
-    if (first_of_item && item_n > 0) mbar_wait(smem_u32(&bars.o_empty), (item_n - 1) & 1);
+    if (first_of_item && item_n > 0) mbar_wait_warp(smem_u32(&bars.o_empty), (item_n - 1) & 1);
     tc_fence_after();
     // B = V tile, MN-major SW128: 16 keys = two 8-row groups of 1024 B; N slabs 16 KB apart
     const uint64_t vdesc = vdesc0 + (uint64_t)((vs * C::kTileBytes) >> 4);
@@ -185,14 +186,14 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++n) {
     const Item it = get_item(p, idx);
     const int qb = n % C::kNQ;
-    mbar_wait(smem_u32(&bars.q_full[qb]), (n / C::kNQ) & 1);
+    mbar_wait_warp(smem_u32(&bars.q_full[qb]), (n / C::kNQ) & 1);
     const uint64_t qdesc = qdesc0 + (uint64_t)((qb * C::kTileBytes) >> 4);
     const int nt = it.tr.count();
     for (int t = 0; t < nt; ++t, ++T) {
       const int ks = T % C::kNK, sb = T & 1;
-      mbar_wait(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
+      mbar_wait_warp(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
       if ((threadIdx.x & 31) == 0) trace_ev(0, 60);
-      if (T >= 2) mbar_wait(smem_u32(&bars.p_full[sb]), ((T - 2) >> 1) & 1);  // S[sb] consumed
+      if (T >= 2) mbar_wait_warp(smem_u32(&bars.p_full[sb]), ((T - 2) >> 1) & 1);  // S[sb] consumed
       if ((threadIdx.x & 31) == 0) trace_ev(0, 61);
       tc_fence_after();
       const uint64_t kdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
@@ -217,13 +218,16 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
 // ------------------------------------------------------------------------------------------
 // softmax warpgroup W (column half W of S); thread owns row = TMEM lane
 // ------------------------------------------------------------------------------------------
-template <int D, int W>
+// (W is a runtime value so that both warpgroups execute one code path: the named
+// barrier they share is then a single program point)
+template <int D>
 __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint32_t tmem, int total, int tid,
                                              int warp, float (*red_max)[2][kM], float (*red_l)[kM]) {
+  const int W = warp >> 2;             // column half of this warpgroup
   const int row = tid & 127;
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-  constexpr int c0 = W * kHalf;        // first S column of this half
-  constexpr int oc0 = W * (D / 2);     // first O column of this half
+  const int c0 = W * kHalf;            // first S column of this half
+  const int oc0 = W * (D / 2);         // first O column of this half
   int n = 0, T = 0;
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++n) {
     const Item it = get_item(p, idx);
@@ -235,7 +239,7 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
       const int kt = it.tr.at(t);
       const int64_t j0 = (int64_t)kt * kN;
       const bool full = kv_tile_full(it.i0, it.i1, kt, it.W, p.n_sink);
-      mbar_wait(smem_u32(&bars.s_full[sb]), (T >> 1) & 1);
+      mbar_wait_warp(smem_u32(&bars.s_full[sb]), (T >> 1) & 1);
       tc_fence_after();
       if (row == 0) trace_ev(1 + W, 30 + W);
       uint32_t sr[kHalf];
@@ -281,7 +285,7 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
       }
       if (__any_sync(0xffffffffu, rescale)) {
         // O must hold PV(T-1) before it is rescaled (this half of its columns)
-        mbar_wait(smem_u32(&bars.pv_done[(T - 1) & 1]), ((T - 1) >> 1) & 1);
+        mbar_wait_warp(smem_u32(&bars.pv_done[(T - 1) & 1]), ((T - 1) >> 1) & 1);
         tc_fence_after();
         uint32_t r[32];
 #pragma unroll
@@ -322,7 +326,7 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
     }
     // epilogue: O / l -> bf16 rows (this half of the columns), lse
     red_l[W][row] = l;
-    mbar_wait(smem_u32(&bars.o_full), n & 1);
+    mbar_wait_warp(smem_u32(&bars.o_full), n & 1);
     named_bar_sync(kBarSoftmax, kSoftmaxThreads);
     const float lt = l + red_l[1 - W][row];
     tc_fence_after();
@@ -445,10 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 9) {
     mma_role<D>(p, bars, tmem, q_smem, k_smem, v_smem, total);
-  } else if (warp < 4) {
-    softmax_role<D, 0>(p, bars, tmem, total, tid, warp, red_max, red_l);
   } else if (warp < 8) {
-    softmax_role<D, 1>(p, bars, tmem, total, tid, warp, red_max, red_l);
+    softmax_role<D>(p, bars, tmem, total, tid, warp, red_max, red_l);
   }
 
   tc_fence_before();
