@@ -491,6 +491,20 @@ bool make_map(CUtensorMap *m, const void *ptr, int D, int H, int64_t N, int B, i
 
 }  // namespace
 
+// [B, N, H, D] bf16 tensor map with 64-column x box_rows boxes (128-byte swizzle)
+bool make_tile_map(void *m, const void *ptr, int D, int H, int64_t N, int B, int64_t row_stride, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)row_stride * 2, (cuuint64_t)(N * row_stride * 2)};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(static_cast<CUtensorMap *>(m), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool encode_cache_map(void *map_out, const void *ptr, int D, int64_t rows) {
   auto enc = get_encode();
   if (!enc) return false;
@@ -568,7 +582,7 @@ int launch_d(const PrefillArgs &a, void *stream) {
 }  // namespace
 
 int launch_prefill_bf16_tc(const PrefillArgs &a, void *stream) {
-  if (a.d == 128) return launch_d<128>(a, stream);
+  if (a.d == 128) return launch_prefill_bf16_tc2(a, stream);  // CTA-pair kernel (prefill_tc2.cu)
   return launch_d<64>(a, stream);
 }
 
