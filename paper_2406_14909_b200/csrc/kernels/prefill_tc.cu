@@ -582,7 +582,7 @@ int launch_d(const PrefillArgs &a, void *stream) {
 }  // namespace
 
 int launch_prefill_bf16_tc(const PrefillArgs &a, void *stream) {
-  if (a.d == 128) return launch_prefill_bf16_tc2(a, stream);  // CTA-pair kernel (prefill_tc2.cu)
+  if (a.d == 128) return launch_d<128>(a, stream);
   return launch_d<64>(a, stream);
 }
 

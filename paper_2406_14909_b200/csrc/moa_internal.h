@@ -157,7 +157,6 @@ struct PrefillArgs {
 };
 int launch_prefill_f32(const PrefillArgs &a, void *stream);
 int launch_prefill_bf16_tc(const PrefillArgs &a, void *stream);
-int launch_prefill_bf16_tc2(const PrefillArgs &a, void *stream);
 
 struct CacheArgs {
   const void *k, *v;  // prompt K/V (fill) or new token (append)
