@@ -81,7 +81,7 @@ void free_tables(LayerPlan &p) {
   p.d_tables = nullptr;
   p.d_win_q = p.d_win_g = nullptr;
   p.d_g_off = nullptr;
-  p.d_items = p.d_pairs = p.d_chunks = p.d_g_chunk = nullptr;
+  p.d_items = p.d_chunks = p.d_g_chunk = nullptr;
   p.d_counters = nullptr;
 }
 
@@ -93,8 +93,7 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   size_t o_wing = align16(o_winq + p.win_q.size() * 4);
   size_t o_goff = align16(o_wing + p.win_g.size() * 4);
   size_t o_items = align16(o_goff + p.g_off.size() * 8);
-  size_t o_pairs = align16(o_items + p.items.size() * 4);
-  size_t o_chunks = align16(o_pairs + p.pairs.size() * 4);
+  size_t o_chunks = align16(o_items + p.items.size() * 4);
   size_t o_gch = align16(o_chunks + p.chunks.size() * 4);
   size_t o_cnt = align16(o_gch + p.g_chunk.size() * 4);
   size_t total = align16(o_cnt + (size_t)ctx->max_batch * ctx->ngl * 4);
@@ -103,7 +102,6 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   std::memcpy(host.data() + o_wing, p.win_g.data(), p.win_g.size() * 4);
   std::memcpy(host.data() + o_goff, p.g_off.data(), p.g_off.size() * 8);
   std::memcpy(host.data() + o_items, p.items.data(), p.items.size() * 4);
-  std::memcpy(host.data() + o_pairs, p.pairs.data(), p.pairs.size() * 4);
   std::memcpy(host.data() + o_chunks, p.chunks.data(), p.chunks.size() * 4);
   std::memcpy(host.data() + o_gch, p.g_chunk.data(), p.g_chunk.size() * 4);
   DeviceGuard dg(ctx->device);
@@ -122,7 +120,6 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   p.d_win_g = reinterpret_cast<const int32_t *>(b + o_wing);
   p.d_g_off = reinterpret_cast<const int64_t *>(b + o_goff);
   p.d_items = reinterpret_cast<const int32_t *>(b + o_items);
-  p.d_pairs = reinterpret_cast<const int32_t *>(b + o_pairs);
   p.d_chunks = reinterpret_cast<const int32_t *>(b + o_chunks);
   p.d_g_chunk = reinterpret_cast<const int32_t *>(b + o_gch);
   p.d_counters = reinterpret_cast<int *>(b + o_cnt);
@@ -280,33 +277,6 @@ moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_he
   for (size_t i = 0; i < its.size(); ++i) {
     np.items[2 * i] = its[i].h;
     np.items[2 * i + 1] = its[i].qt;
-  }
-  // CTA-pair kernel: two adjacent q tiles walk the union of their kv lists
-  {
-    const int nqp = (nqt + 1) / 2;
-    std::vector<It> ps;
-    for (int h = 0; h < ctx->nql; ++h) {
-      const size_t first = ps.size();
-      int64_t hc = 0;
-      for (int qp = 0; qp < nqp; ++qp) {
-        int64_t i0 = (int64_t)qp * 2 * moa::kTile;
-        int64_t i1 = std::min<int64_t>(N, i0 + 2 * moa::kTile) - 1;
-        const int c = moa::kv_tile_ranges(i0, i1, np.win_q[h], n_sink).count();
-        hc += c;
-        ps.push_back({h, qp, c, 0});
-      }
-      for (size_t k = first; k < ps.size(); ++k) ps[k].hcost = hc;
-    }
-    std::stable_sort(ps.begin(), ps.end(), [](const It &a, const It &b) {
-      if (a.hcost != b.hcost) return a.hcost > b.hcost;
-      if (a.h != b.h) return a.h < b.h;
-      return a.cnt > b.cnt;
-    });
-    np.pairs.resize(ps.size() * 2);
-    for (size_t i = 0; i < ps.size(); ++i) {
-      np.pairs[2 * i] = ps[i].h;
-      np.pairs[2 * i + 1] = ps[i].qt;
-    }
   }
 
   // decode work list: split every group region into chunks of ~chunk_rows rows
@@ -494,7 +464,6 @@ moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, co
   a.batch = batch; a.N = N; a.scale = scale; a.lse = lse_out; a.n_sink = p.n_sink;
   a.nql = ctx->nql; a.G = ctx->G; a.d = ctx->d;
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
-  a.d_pairs = p.d_pairs; a.n_pairs = (int)(p.pairs.size() / 2);
   int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_tc(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
   moa::CacheArgs c{};

@@ -99,7 +99,6 @@ struct LayerPlan {
   int64_t rows_per_seq = 0;      // sum_g (s + W_g)
   std::vector<int32_t> items;    // prefill work items (h_local, q_tile): heads heaviest first, q tiles of a
                                  // head consecutive (L2 sharing of its K/V), heaviest first
-  std::vector<int32_t> pairs;    // same order over (h_local, q_tile pair) for the CTA-pair kernel
   std::vector<int32_t> chunks;   // decode chunks: (g_local, row_begin, row_end) triples
   std::vector<int32_t> g_chunk;  // first chunk of each group, size ngl + 1
   int chunk_rows = 0;
@@ -110,7 +109,6 @@ struct LayerPlan {
   const int32_t *d_win_g = nullptr;
   const int64_t *d_g_off = nullptr;
   const int32_t *d_items = nullptr;
-  const int32_t *d_pairs = nullptr;
   const int32_t *d_chunks = nullptr;
   const int32_t *d_g_chunk = nullptr;
   int *d_counters = nullptr;     // [max_batch, ngl] decode combine tickets (zeroed at upload)
@@ -152,8 +150,6 @@ struct PrefillArgs {
   const int32_t *d_win_q;
   const int32_t *d_items;
   int n_items;
-  const int32_t *d_pairs;  // (q-head, q-tile pair) items of the CTA-pair kernel
-  int n_pairs;
 };
 int launch_prefill_f32(const PrefillArgs &a, void *stream);
 int launch_prefill_bf16_tc(const PrefillArgs &a, void *stream);
