@@ -50,11 +50,13 @@ constexpr int kHalf = kN / 2;         // S columns per softmax warpgroup
 constexpr int kSoftmaxThreads = 256;  // two warpgroups, one per column half
 constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColS0 = 0, kColS1 = 128, kColP0 = 256, kColP1 = 320, kColO = 384;
+// TMEM: S (fp32 128x128) | P0 | P1 (bf16 packed, 64 cols each) | O (fp32 128xD) | Q0 | Q1 (bf16 packed)
+constexpr uint32_t kColS = 0, kColP0 = 128, kColP1 = 192, kColO = 256, kColQ0 = 384, kColQ1 = 448;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only if the max grows by > 2^8
 // exponentials of pairs c with (c & kPolyMask) == kPolyMask use the FMA-pipe polynomial
 constexpr int kPolyMask = 1;
 constexpr int kBarSoftmax = 1;  // named barrier of the 8 softmax warps
+constexpr int kSoftmaxWarps = 8;  // mbarrier arrivals from the softmax side (one per warp)
 
 // 2^y on the FMA/ALU pipes: y = n + f, n = round(y), |f| <= 1/2, 2^f by a degree-3
 // polynomial fitted for relative error (7.7e-5 max, far below bf16's 3.9e-3), 2^n by
@@ -89,9 +91,9 @@ struct Cfg {
   static constexpr int kSlabs = D / 64;                  // 128-byte swizzle slabs per row
   static constexpr int kTileBytes = kM * D * 2;          // one Q / K / V tile in smem
   static constexpr int kSlabBytes = kM * 128;            // 128 rows x 128 B
-  static constexpr int kNK = D == 128 ? 2 : 3;           // K ring stages
-  static constexpr int kNV = D == 128 ? 2 : 3;           // V ring stages
-  static constexpr int kNQ = 2;                          // Q buffers (items in flight)
+  static constexpr int kNK = D == 128 ? 3 : 4;           // K ring stages (K(T+3) streams during S(T+1..T+2))
+  static constexpr int kNV = D == 128 ? 2 : 3;           // V ring stages (V is consumed a softmax later)
+  static constexpr int kNQ = 1;                          // Q staging buffer (copied to TMEM at item start)
   static constexpr int kSmemBytes = (kNQ + kNK + kNV) * kTileBytes + 1024;
 };
 
@@ -122,7 +124,9 @@ struct Bars {
   uint64_t q_full[2], q_empty[2];
   uint64_t k_full[4], k_empty[4];
   uint64_t v_full[4], v_empty[4];
-  uint64_t s_full[2], p_full[2], pv_done[2];
+  uint64_t s_full, s_free;          // S(T) computed / S(T) loaded into softmax registers
+  uint64_t p_full[2], pv_done[2];
+  uint64_t qt_full[2];              // Q of an item copied smem -> TMEM by the softmax warps
   uint64_t o_full, o_empty;
   uint32_t tmem_base;
 };
@@ -149,15 +153,17 @@ __device__ __forceinline__ Item get_item(const TcParams &p, int idx) {
 
 // ------------------------------------------------------------------------------------------
 // MMA issuer: whole warp 9 walks the schedule, one elected lane issues tcgen05 ops.
-// Order per item: S(t) [then PV(t-1)] for each tile, PV(last).
+// Order per item: S(t) [then PV(t-1)] for each tile, PV(last).  S = Q K^T takes Q from
+// TMEM (copied there by the softmax warps) and K from shared memory, so the QK^T MMA reads
+// only K through the shared-memory port; S(t+1) reuses the single S buffer as soon as the
+// softmax has loaded S(t) into registers (s_free), P is double-buffered.
 // ------------------------------------------------------------------------------------------
 template <int D>
-__device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t tmem, uint32_t q_smem,
-                                         uint32_t k_smem, uint32_t v_smem, int total) {
+__device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t tmem, uint32_t k_smem,
+                                         uint32_t v_smem, int total) {
   using C = Cfg<D>;
   constexpr uint32_t idesc_s = idesc_bf16_f32(kM, kN, false);
   constexpr uint32_t idesc_o = idesc_bf16_f32(kM, D, true);
-  const uint64_t qdesc0 = smem_desc_sw128(q_smem, 16, 1024);
   const uint64_t kdesc0 = smem_desc_sw128(k_smem, 16, 1024);
   const uint64_t vdesc0 = smem_desc_sw128(v_smem, C::kSlabBytes, 1024);
   int n = 0, T = 0;
@@ -185,27 +191,26 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
   };
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++n) {
     const Item it = get_item(p, idx);
-    const int qb = n % C::kNQ;
-    mbar_wait_warp(smem_u32(&bars.q_full[qb]), (n / C::kNQ) & 1);
-    const uint64_t qdesc = qdesc0 + (uint64_t)((qb * C::kTileBytes) >> 4);
+    const int qb = n & 1;
+    mbar_wait_warp(smem_u32(&bars.qt_full[qb]), (n >> 1) & 1);  // Q(n) in TMEM
+    const uint32_t qcol = tmem + (qb ? kColQ1 : kColQ0);
     const int nt = it.tr.count();
     for (int t = 0; t < nt; ++t, ++T) {
-      const int ks = T % C::kNK, sb = T & 1;
+      const int ks = T % C::kNK;
       mbar_wait_warp(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
       if ((threadIdx.x & 31) == 0) trace_ev(0, 60);
-      if (T >= 2) mbar_wait_warp(smem_u32(&bars.p_full[sb]), ((T - 2) >> 1) & 1);  // S[sb] consumed
+      if (T >= 1) mbar_wait_warp(smem_u32(&bars.s_free), (T - 1) & 1);  // S(T-1) read by the softmax
       if ((threadIdx.x & 31) == 0) trace_ev(0, 61);
       tc_fence_after();
       const uint64_t kdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * C::kSlabBytes + (kk & 3) * 32) >> 4;
-          mma_ss(tmem + (sb ? kColS1 : kColS0), qdesc + off, kdesc + off, idesc_s, kk > 0 ? 1u : 0u);
+          const uint32_t koff = ((kk >> 2) * C::kSlabBytes + (kk & 3) * 32) >> 4;
+          mma_ts(tmem + kColS, qcol + kk * 8, kdesc + koff, idesc_s, kk > 0 ? 1u : 0u);
         }
-        mma_commit(smem_u32(&bars.s_full[sb]));
+        mma_commit(smem_u32(&bars.s_full));
         mma_commit(smem_u32(&bars.k_empty[ks]));
-        if (t == nt - 1) mma_commit(smem_u32(&bars.q_empty[qb]));
         trace_ev(0, 10);
       }
       __syncwarp();
@@ -216,39 +221,75 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
 }
 
 // ------------------------------------------------------------------------------------------
-// softmax warpgroup W (column half W of S); thread owns row = TMEM lane
+// softmax warpgroups: warps 0-3 take S columns [0, 64), warps 4-7 columns [64, 128) of the
+// same rows (thread owns row = TMEM lane).  W is a runtime value so both warpgroups run one
+// code path (the named barrier they share is a single program point).  At each item start
+// they also copy the item's Q tile from shared memory (TMA, 128B swizzle) into TMEM.
 // ------------------------------------------------------------------------------------------
-// (W is a runtime value so that both warpgroups execute one code path: the named
-// barrier they share is then a single program point)
 template <int D>
-__device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint32_t tmem, int total, int tid,
-                                             int warp, float (*red_max)[2][kM], float (*red_l)[kM]) {
+__device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint32_t tmem, uint32_t q_smem,
+                                             int total, int tid, int warp, float (*red_max)[2][kM],
+                                             float (*red_l)[kM]) {
+  using C = Cfg<D>;
   const int W = warp >> 2;             // column half of this warpgroup
   const int row = tid & 127;
+  const int lane = tid & 31;
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const int c0 = W * kHalf;            // first S column of this half
-  const int oc0 = W * (D / 2);         // first O column of this half
+  const int oc0 = W * (D / 2);         // first O / Q column of this half
   int n = 0, T = 0;
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x, ++n) {
     const Item it = get_item(p, idx);
     const int64_t i = it.i0 + row;
     const int nt = it.tr.count();
+    // ---- Q(n): smem (swizzled rows) -> TMEM columns of this half, packed bf16 pairs
+    {
+      const int qb = n & 1;                       // TMEM Q buffer
+      const int sq = n % C::kNQ;                  // smem staging buffer
+      mbar_wait_warp(smem_u32(&bars.q_full[sq]), (n / C::kNQ) & 1);
+      const uint32_t qs = q_smem + sq * C::kTileBytes;
+      constexpr int kChunks = D / 16;  // 16-byte chunks of this half row
+      uint32_t qr[D / 4];
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c) {
+        const int gc = (oc0 / 8) + c;            // chunk index in the full row
+        const int sl = gc >> 3, cc = gc & 7;     // 128-byte slab, chunk within the swizzle row
+        const uint32_t addr = qs + sl * C::kSlabBytes + row * 128 + ((cc ^ (row & 7)) << 4);
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(qr[4 * c]), "=r"(qr[4 * c + 1]), "=r"(qr[4 * c + 2]), "=r"(qr[4 * c + 3])
+                     : "r"(addr));
+      }
+      const uint32_t qa = tmem + lane_off + (qb ? kColQ1 : kColQ0) + oc0 / 2;
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) tmem_st16(qa + c * 16, &qr[16 * c]);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(smem_u32(&bars.qt_full[qb]));
+        mbar_arrive(smem_u32(&bars.q_empty[sq]));  // the smem Q buffer may be refilled
+      }
+    }
     float m_used = -INFINITY, l = 0.f;
     for (int t = 0; t < nt; ++t, ++T) {
       const int sb = T & 1;
       const int kt = it.tr.at(t);
       const int64_t j0 = (int64_t)kt * kN;
       const bool full = kv_tile_full(it.i0, it.i1, kt, it.W, p.n_sink);
-      mbar_wait_warp(smem_u32(&bars.s_full[sb]), (T >> 1) & 1);
+      mbar_wait_warp(smem_u32(&bars.s_full), T & 1);
       tc_fence_after();
       if (row == 0) trace_ev(1 + W, 30 + W);
       uint32_t sr[kHalf];
       {
-        const uint32_t sa = tmem + lane_off + (sb ? kColS1 : kColS0) + c0;
+        const uint32_t sa = tmem + lane_off + kColS + c0;
         tmem_ld32(sa, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
         tmem_ld32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
         tmem_wait_ld();
       }
+      // S is in registers: the tensor core may overwrite it with S(T+1)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars.s_free));
       float x[kHalf];
 #pragma unroll
       for (int c = 0; c < kHalf; ++c) x[c] = __uint_as_float(sr[c]);
@@ -301,6 +342,7 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
       l *= alpha;
       const float nmref = m_used == -INFINITY ? 0.f : -m_used;
       float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      // P[sb] was last read by PV(T-2), complete since S(T) completed (in-order tcgen05)
       const uint32_t pa = tmem + lane_off + (sb ? kColP1 : kColP0) + W * (kHalf / 2);
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
@@ -322,7 +364,8 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
       tmem_wait_st();
       tc_fence_before();
       if (row == 0) trace_ev(1 + W, 40 + W);
-      mbar_arrive(smem_u32(&bars.p_full[sb]));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars.p_full[sb]));
     }
     // epilogue: O / l -> bf16 rows (this half of the columns), lse
     red_l[W][row] = l;
@@ -354,7 +397,8 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
     if (W == 0 && p.lse && i <= it.i1)
       p.lse[((int64_t)it.b * p.nql + it.h) * p.N + i] = lt > 0.f ? (m_used + __log2f(lt)) * kLn2 : -INFINITY;
     tc_fence_before();
-    mbar_arrive(smem_u32(&bars.o_empty));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&bars.o_empty));
   }
 }
 
@@ -379,11 +423,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     s_trace_n[0] = s_trace_n[1] = s_trace_n[2] = s_trace_n[3] = s_trace_n[4] = 0;
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&bars.q_full[i]), 1);
-      mbar_init(smem_u32(&bars.q_empty[i]), 1);
-      mbar_init(smem_u32(&bars.s_full[i]), 1);
-      mbar_init(smem_u32(&bars.p_full[i]), kSoftmaxThreads);
+      mbar_init(smem_u32(&bars.q_empty[i]), kSoftmaxWarps);
+      mbar_init(smem_u32(&bars.p_full[i]), kSoftmaxWarps);
       mbar_init(smem_u32(&bars.pv_done[i]), 1);
+      mbar_init(smem_u32(&bars.qt_full[i]), kSoftmaxWarps);
     }
+    mbar_init(smem_u32(&bars.s_full), 1);
+    mbar_init(smem_u32(&bars.s_free), kSoftmaxWarps);
     for (int i = 0; i < C::kNK; ++i) {
       mbar_init(smem_u32(&bars.k_full[i]), 1);
       mbar_init(smem_u32(&bars.k_empty[i]), 1);
@@ -393,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&bars.v_empty[i]), 1);
     }
     mbar_init(smem_u32(&bars.o_full), 1);
-    mbar_init(smem_u32(&bars.o_empty), kSoftmaxThreads);
+    mbar_init(smem_u32(&bars.o_empty), kSoftmaxWarps);
     fence_mbar_init();
   }
   if (warp == 9) tmem_alloc<kTmemCols>(smem_u32(&bars.tmem_base));
@@ -448,9 +494,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 9) {
-    mma_role<D>(p, bars, tmem, q_smem, k_smem, v_smem, total);
+    mma_role<D>(p, bars, tmem, k_smem, v_smem, total);
   } else if (warp < 8) {
-    softmax_role<D>(p, bars, tmem, total, tid, warp, red_max, red_l);
+    softmax_role<D>(p, bars, tmem, q_smem, total, tid, warp, red_max, red_l);
   }
 
   tc_fence_before();
