@@ -108,18 +108,6 @@ struct TcParams {
   const int32_t *items;  // (q-head, q-tile) LPT order
 };
 
-// debug tracing (env MOA_PREFILL_TRACE=1): (clock << 8 | event code) of CTA 0
-__device__ unsigned long long *g_trace = nullptr;
-__shared__ unsigned int s_trace_n[5];
-__device__ __forceinline__ void trace_ev(int role, int code) {
-  unsigned long long *tr = g_trace;
-  if (tr && blockIdx.x == 0) {
-    const unsigned long long t = clock64();
-    const unsigned int k = s_trace_n[role]++;
-    if (k < 12000) tr[1 + role * 12000 + k] = (t << 8) | (unsigned long long)code;
-  }
-}
-
 struct Bars {
   uint64_t q_full[2], q_empty[2];
   uint64_t k_full[4], k_empty[4];
@@ -171,7 +159,6 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
     const int vs = Tp % C::kNV, pb = Tp & 1;
     mbar_wait_warp(smem_u32(&bars.v_full[vs]), (Tp / C::kNV) & 1);
     mbar_wait_warp(smem_u32(&bars.p_full[pb]), (Tp >> 1) & 1);
-    if ((threadIdx.x & 31) == 0) trace_ev(0, 50);
     if (first_of_item && item_n > 0) mbar_wait_warp(smem_u32(&bars.o_empty), (item_n - 1) & 1);
     tc_fence_after();
     // B = V tile, MN-major SW128: 16 keys = two 8-row groups of 1024 B; N slabs 16 KB apart
@@ -185,7 +172,6 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
       mma_commit(smem_u32(&bars.v_empty[vs]));
       mma_commit(smem_u32(&bars.pv_done[pb]));
       if (last_of_item) mma_commit(smem_u32(&bars.o_full));
-      trace_ev(0, 20);
     }
     __syncwarp();
   };
@@ -198,9 +184,7 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
     for (int t = 0; t < nt; ++t, ++T) {
       const int ks = T % C::kNK;
       mbar_wait_warp(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
-      if ((threadIdx.x & 31) == 0) trace_ev(0, 60);
       if (T >= 1) mbar_wait_warp(smem_u32(&bars.s_free), (T - 1) & 1);  // S(T-1) read by the softmax
-      if ((threadIdx.x & 31) == 0) trace_ev(0, 61);
       tc_fence_after();
       const uint64_t kdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
       if (elect_one()) {
@@ -211,7 +195,6 @@ __device__ __forceinline__ void mma_role(const TcParams &p, Bars &bars, uint32_t
         }
         mma_commit(smem_u32(&bars.s_full));
         mma_commit(smem_u32(&bars.k_empty[ks]));
-        trace_ev(0, 10);
       }
       __syncwarp();
       if (t > 0) issue_pv(T - 1, t == 1, false, n);
@@ -278,7 +261,6 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
       const bool full = kv_tile_full(it.i0, it.i1, kt, it.W, p.n_sink);
       mbar_wait_warp(smem_u32(&bars.s_full), T & 1);
       tc_fence_after();
-      if (row == 0) trace_ev(1 + W, 30 + W);
       uint32_t sr[kHalf];
       {
         const uint32_t sa = tmem + lane_off + kColS + c0;
@@ -311,9 +293,7 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
         for (int k = 0; k < w; ++k) mx[k] = fmaxf(mx[k], mx[k + w]);
       // row max of both halves (raw scores; scale > 0 commutes with max)
       red_max[sb][W][row] = mx[0];
-      if (row == 0) trace_ev(1 + W, 70 + W);
       named_bar_sync(kBarSoftmax, kSoftmaxThreads);
-      if (row == 0) trace_ev(1 + W, 72 + W);
       const float mt = fmaxf(mx[0], red_max[sb][1 - W][row]) * p.scale_log2;
       bool rescale = false;
       float alpha = 1.f;
@@ -363,7 +343,6 @@ __device__ __forceinline__ void softmax_role(const TcParams &p, Bars &bars, uint
       l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
       tmem_wait_st();
       tc_fence_before();
-      if (row == 0) trace_ev(1 + W, 40 + W);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&bars.p_full[sb]));
     }
@@ -420,7 +399,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total = p.n_items * p.batch;
 
   if (tid == 0) {
-    s_trace_n[0] = s_trace_n[1] = s_trace_n[2] = s_trace_n[3] = s_trace_n[4] = 0;
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&bars.q_full[i]), 1);
       mbar_init(smem_u32(&bars.q_empty[i]), kSoftmaxWarps);
@@ -478,7 +456,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (T >= C::kNK) mbar_wait(smem_u32(&bars.k_empty[ks]), ((T - C::kNK) / C::kNK) & 1);
             const uint32_t kbar = smem_u32(&bars.k_full[ks]);
             mbar_expect_tx(kbar, C::kTileBytes);
-            trace_ev(3, 80);
             for (int sl = 0; sl < C::kSlabs; ++sl)
               tma_load_4d(k_smem + ks * C::kTileBytes + sl * C::kSlabBytes, &tm_k, kbar, sl * 64, g, j0, it.b);
           } else {
@@ -486,7 +463,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (T >= C::kNV) mbar_wait(smem_u32(&bars.v_empty[vs]), ((T - C::kNV) / C::kNV) & 1);
             const uint32_t vbar = smem_u32(&bars.v_full[vs]);
             mbar_expect_tx(vbar, C::kTileBytes);
-            trace_ev(4, 81);
             for (int sl = 0; sl < C::kSlabs; ++sl)
               tma_load_4d(v_smem + vs * C::kTileBytes + sl * C::kSlabBytes, &tm_v, vbar, sl * 64, g, j0, it.b);
           }
@@ -602,26 +578,8 @@ int launch_d(const PrefillArgs &a, void *stream) {
                                        C::kSmemBytes);
   if (e != cudaSuccess) return (int)e;
   const int total = a.n_items * a.batch;
-  static unsigned long long *trace_buf = nullptr;
-  static bool trace_on = std::getenv("MOA_PREFILL_TRACE") != nullptr;
-  if (trace_on) {
-    if (!trace_buf) cudaMalloc(&trace_buf, 65536 * 8);
-    cudaMemsetAsync(trace_buf, 0, 65536 * 8, (cudaStream_t)stream);
-    cudaMemcpyToSymbolAsync(g_trace, &trace_buf, sizeof(trace_buf), 0, cudaMemcpyHostToDevice, (cudaStream_t)stream);
-  }
-
   const int grid = total < num_sms() ? total : num_sms();
   prefill_tc_kernel<D><<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, p);
-  if (trace_on) {
-    static std::vector<unsigned long long> h(65536);
-    cudaMemcpy(h.data(), trace_buf, 65536 * 8, cudaMemcpyDeviceToHost);
-    FILE *f = fopen("gpurun_out/prefill_trace.txt", "w");
-    if (f) {
-      for (unsigned k = 0; k < 60000; ++k)
-        if (h[1 + k]) fprintf(f, "%llu %llu\n", h[1 + k] >> 8, h[1 + k] & 255);
-      fclose(f);
-    }
-  }
   return (int)cudaGetLastError();
 }
 
