@@ -151,6 +151,14 @@ moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, co
                        int64_t o_row_stride, int batch, int64_t N, float scale, float *lse_out,
                        void *workspace, size_t ws_bytes, moa_stream_t stream);
 
+/* The attention of moa_prefill alone (a4): no cache is read or written and
+ * none needs to be bound; the layer's decode position is unchanged.  Together
+ * with moa_cache_fill it is exactly moa_prefill. */
+moa_status moa_prefill_attn(moa_ctx *ctx, int layer, const void *q, const void *k, const void *v,
+                            void *o, int64_t q_row_stride, int64_t kv_row_stride,
+                            int64_t o_row_stride, int batch, int64_t N, float scale, float *lse_out,
+                            moa_stream_t stream);
+
 /* Cache fill alone (a5): write the resident rows of a prompt of length N
  * (K/V as in moa_prefill) into the layer's cache; next position = N. */
 moa_status moa_cache_fill(moa_ctx *ctx, int layer, const void *k, const void *v,

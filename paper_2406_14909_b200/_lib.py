@@ -36,6 +36,8 @@ _SIGS = [
     ("moa_bind_layer_cache", c_int, [_P, c_int, _P, _P, c_int]),
     ("moa_prefill", c_int, [_P, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int, c_int64, c_float,
                             _P, _P, c_size_t, _P]),
+    ("moa_prefill_attn", c_int, [_P, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int, c_int64, c_float,
+                                 _P, _P]),
     ("moa_cache_fill", c_int, [_P, c_int, _P, _P, c_int64, c_int, c_int64, _P]),
     ("moa_kv_append", c_int, [_P, c_int, _P, _P, c_int64, c_int, c_int64, _P]),
     ("moa_decode_step", c_int, [_P, c_int, _P, _P, c_int64, c_int64, c_int, c_int64, c_float, _P, _P,

@@ -437,15 +437,18 @@ static moa_status check_launch_common(const moa_ctx *ctx, int layer, int batch) 
 
 static bool aligned16(const void *ptr) { return ((uintptr_t)ptr & 15) == 0; }
 
-moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, const void *v,
-                       void *o, int64_t q_row_stride, int64_t kv_row_stride,
-                       int64_t o_row_stride, int batch, int64_t N, float scale, float *lse_out,
-                       void *workspace, size_t ws_bytes, moa_stream_t stream) {
-  (void)workspace;
-  (void)ws_bytes;
-  moa_status st = check_launch_common(ctx, layer, batch);
+static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const void *k, const void *v, void *o,
+                                 int64_t q_row_stride, int64_t kv_row_stride, int64_t o_row_stride, int batch,
+                                 int64_t N, float scale, float *lse_out, moa_stream_t stream, bool fill) {
+  moa_status st = check_layer(ctx, layer, true);
   if (st) return st;
+  if (ctx->device < 0) return fail(MOA_ERR_STATE, "planning context (device -1) cannot launch");
   LayerPlan &p = ctx->layers[layer];
+  if (fill && !p.k_cache) return fail(MOA_ERR_STATE, "no cache bound for layer %d", layer);
+  const int max_b = fill ? p.bound_batch : ctx->max_batch;
+  if (batch < 1 || batch > max_b) return fail(MOA_ERR_INVALID_ARG, "batch %d not in [1, %d]", batch, max_b);
+  st = check_sticky(ctx);
+  if (st) return st;
   if (!q || !k || !v || !o) return fail(MOA_ERR_INVALID_ARG, "q/k/v/o must be non-NULL");
   if (N != p.N)
     return fail(MOA_ERR_SHAPE, "prefill N=%lld but spans were set for N=%lld", (long long)N, (long long)p.N);
@@ -466,6 +469,7 @@ moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, co
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
   int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_tc(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
+  if (!fill) return ok();
   moa::CacheArgs c{};
   c.k = k; c.v = v; c.row_stride = kv_row_stride; c.k_cache = p.k_cache; c.v_cache = p.v_cache;
   c.rows_per_seq = p.rows_per_seq; c.d_g_off = p.d_g_off; c.d_win_g = p.d_win_g;
@@ -476,6 +480,23 @@ moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, co
   if (e) return cuda_fail((cudaError_t)e, "cache fill launch");
   p.next_pos = N;
   return ok();
+}
+
+moa_status moa_prefill(moa_ctx *ctx, int layer, const void *q, const void *k, const void *v,
+                       void *o, int64_t q_row_stride, int64_t kv_row_stride,
+                       int64_t o_row_stride, int batch, int64_t N, float scale, float *lse_out,
+                       void *workspace, size_t ws_bytes, moa_stream_t stream) {
+  (void)workspace;
+  (void)ws_bytes;
+  return prefill_common(ctx, layer, q, k, v, o, q_row_stride, kv_row_stride, o_row_stride, batch, N, scale,
+                        lse_out, stream, true);
+}
+
+moa_status moa_prefill_attn(moa_ctx *ctx, int layer, const void *q, const void *k, const void *v, void *o,
+                            int64_t q_row_stride, int64_t kv_row_stride, int64_t o_row_stride, int batch,
+                            int64_t N, float scale, float *lse_out, moa_stream_t stream) {
+  return prefill_common(ctx, layer, q, k, v, o, q_row_stride, kv_row_stride, o_row_stride, batch, N, scale,
+                        lse_out, stream, false);
 }
 
 moa_status moa_cache_fill(moa_ctx *ctx, int layer, const void *k, const void *v,

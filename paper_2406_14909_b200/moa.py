@@ -185,6 +185,14 @@ class MoAContext:
                                    0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)),
               "moa_prefill")
 
+    def prefill_attn(self, layer: int, q, k, v, o, scale: float, lse=None, stream=None):
+        B, N = q.shape[0], q.shape[1]
+        for t in (q, k, v, o):
+            assert t.stride(-1) == 1 and t.stride(-2) == self.d and t.stride(0) == N * t.stride(1)
+        check(self.lib.moa_prefill_attn(self.ctx, layer, _ptr(q), _ptr(k), _ptr(v), _ptr(o), q.stride(1),
+                                        k.stride(1), o.stride(1), B, N, float(scale), _ptr(lse), _stream(stream)),
+              "moa_prefill_attn")
+
     def cache_fill(self, layer: int, k, v, stream=None):
         B, N = k.shape[0], k.shape[1]
         check(self.lib.moa_cache_fill(self.ctx, layer, _ptr(k), _ptr(v), k.stride(1), B, N, _stream(stream)),

@@ -212,3 +212,28 @@ def test_kv_sharded_contexts_on_one_gpu(moa):
     Kh, Vh = torch.cat([k, kd[:, None]], 1), torch.cat([v, vd[:, None]], 1)
     Od, _ = oracle.decode(f64(qd), f64(Kh), f64(Vh), N, W, s, scale)
     assert np.abs(f64(od) - Od).max() < 2e-2
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_prefill_attn_plus_cache_fill_equals_prefill(moa, dtype):
+    """moa_prefill_attn + moa_cache_fill is moa_prefill (include/moa.h): the same
+    kernel, so outputs are bitwise equal; prefill_attn needs no bound cache and
+    leaves the decode position alone."""
+    B, N, Hq, Hkv, d, s = 2, 300, 4, 2, 128, 4
+    W = [3, 140, 0, 290]
+    q, k, v = (normal((B, N, h, d), 300 + i, dtype).cuda() for i, h in enumerate((Hq, Hkv, Hkv)))
+    _, ref, _, scale = _prefill(moa, q.cpu(), k.cpu(), v.cpu(), W, s, dtype)
+    ctx = moa.MoAContext(1, Hq, Hkv, d, B, dtype=dtype)
+    ctx.set_spans(0, W, s, N)
+    o = torch.full_like(q, float("nan"))
+    ctx.prefill_attn(0, q, k, v, o, scale)         # no cache bound: allowed
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o), bits(ref))
+    ctx.alloc_cache(B)
+    assert ctx.next_pos(0) == 0
+    ctx.prefill_attn(0, q, k, v, o, scale)
+    assert ctx.next_pos(0) == 0
+    ctx.cache_fill(0, k, v)
+    torch.cuda.synchronize()
+    assert ctx.next_pos(0) == N
+    check_cache_image(ctx, 0, k.cpu(), v.cpu(), N - 1, W, s, B, 2)
