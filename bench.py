@@ -210,7 +210,6 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     n_ev = T * L
-    ev_d = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_ev)]
     ev_p = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
 
     def step(record=False):
@@ -223,13 +222,12 @@ def run_ours(args, rank, world, local_rank):
             ctx.cache_fill(l, K[l], V[l])     # = moa_prefill split in two so the attention kernel is timed alone
         ph = torch.cuda.Event(enable_timing=True)
         ph.record(stream)
+        # decode: no event between launches -- an event record between two PDL launches stops the
+        # next kernel's prologue from overlapping the previous one's tail (measured 60.0 vs 52.6 us
+        # per launch, tools/time_decode.py); the phase events bracket the launches instead.
         for t in range(T):
             for l in range(L):
-                if record:
-                    ev_d[t * L + l][0].record(stream)
                 ctx.decode_step_fused(l, qd[t], kd[t], vd[t], od, N + t, scale, ws)
-                if record:
-                    ev_d[t * L + l][1].record(stream)
         return ph
 
     for _ in range(args.warmup):
@@ -240,7 +238,7 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()
 
-    pre_ms, dec_ms, tot_ms, pk_ms, dk_ms = [], [], [], [], []
+    pre_ms, dec_ms, tot_ms, pk_ms = [], [], [], []
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
             barrier()
@@ -255,7 +253,6 @@ def run_ours(args, rank, world, local_rank):
             pre_ms.append(e0.elapsed_time(ph))
             dec_ms.append(ph.elapsed_time(e2))
             pk_ms.append(sum(a.elapsed_time(b) for a, b in ev_p))
-            dk_ms.append(sum(a.elapsed_time(b) for a, b in ev_d))
     tot = sum(tot_ms)
     pre = sum(pre_ms)
     dec = sum(dec_ms)
@@ -270,7 +267,7 @@ def run_ours(args, rank, world, local_rank):
     # roofline of the dominant kernel (decode: one launch per layer-token)
     flops, dec_bytes_per_token = algorithmic_work(windows, B, N, T, s, d, CFG.group)
     peaks, peak_src = load_peaks()
-    dk_avg_ms = sum(dk_ms) / (K_steps * n_ev)
+    dk_avg_ms = dec / (K_steps * n_ev)   # decode phase (max over ranks) / launches, gaps included
     dec_bytes_per_launch = dec_bytes_per_token / L
     achieved_gbs = dec_bytes_per_launch / (dk_avg_ms / 1e3) / 1e9
     pk_total_s = sum(pk_ms) / 1e3 / K_steps
@@ -315,6 +312,8 @@ def run_ours(args, rank, world, local_rank):
                          "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic, "traffic_note": traffic_note,
                          "kernel": "moa decode_kernel (fused append + split-KV + last-CTA combine)",
                          "bytes_per_launch": dec_bytes_per_launch, "avg_launch_ms": dk_avg_ms,
+                         "avg_launch_note": "decode phase time (CUDA events on the launch stream, timed "
+                                            "steps) / launches; inter-launch gaps count against the kernel",
                          "peak_source": peak_src},
             "e2e": e2e,
             "gpu_launches": K_steps * (2 * L + T * L),
@@ -325,17 +324,30 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
-    """Decode tokens/s through MoAContext with pinned HOST inputs: every layer-token copies
-    q, k_new, v_new host->device and o device->host inside the timed region (prefill inputs of
-    one layer are staged from host per layer as well)."""
+    """Decode tokens/s through MoAContext with pinned HOST inputs and outputs.
+
+    Every token's inputs (q, k_new, v_new of all layers, packed in one pinned buffer) are
+    copied host->device and every token's outputs (o of all layers) device->host inside the
+    timed region, on a copy stream double-buffered against the compute stream: the H2D of
+    token t+1 and the D2H of token t-1 overlap the decode launches of token t.  The prefill
+    inputs of each layer are staged from host as well (reported as prefill_ms)."""
     L, B, N, T, d = CFG.layers, CFG.batch, CFG.N, CFG.decode_steps, CFG.head_dim
+    hq_, hkv_ = qd.shape[2], kd.shape[2]
+    nq, nk = B * hq_ * d, B * hkv_ * d
+    per_layer = nq + 2 * nk
     stream = torch.cuda.current_stream()
-    hq, hk, hv = (x.cpu().pin_memory() for x in (qd, kd, vd))
+    cs = torch.cuda.Stream(device=dev)
+    # host: [T, L, q|k|v] packed, pinned
+    hin = torch.empty(T, L, per_layer, dtype=qd.dtype).pin_memory()
+    hin[:, :, :nq] = qd.reshape(T, 1, nq).cpu()
+    hin[:, :, nq:nq + nk] = kd.reshape(T, 1, nk).cpu()
+    hin[:, :, nq + nk:] = vd.reshape(T, 1, nk).cpu()
+    hout = torch.empty(T, L, B, hq_, d, dtype=qd.dtype).pin_memory()
+    din = [torch.empty(L, per_layer, dtype=qd.dtype, device=dev) for _ in range(2)]
+    dout = [torch.empty(L, B, hq_, d, dtype=qd.dtype, device=dev) for _ in range(2)]
     hQ, hK, hV = (x.cpu().pin_memory() for x in (Q[0], K[0], V[0]))
     hO = torch.empty(Q[0].shape, dtype=Q[0].dtype).pin_memory()
-    ho = torch.empty((T, L) + tuple(qd.shape[1:]), dtype=qd.dtype).pin_memory()
     dQ, dK, dV, dO = (torch.empty_like(x) for x in (Q[0], K[0], V[0], Q[0]))
-    dq, dk, dv, do = (torch.empty(x.shape[1:], dtype=x.dtype, device=dev) for x in (qd, kd, vd, qd))
     h2d = d2h = 0
     if world > 1:
         torch.distributed.barrier()
@@ -349,13 +361,39 @@ def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
         hO.copy_(dO, non_blocking=True)
         d2h += hO.numel() * 2
     e1.record(stream)
+    ev_in = [torch.cuda.Event() for _ in range(T)]
+    ev_done = [torch.cuda.Event() for _ in range(T)]
+    ev_out = [torch.cuda.Event() for _ in range(T)]
+    cs.wait_event(e1)
+
+    def h2d_token(t):
+        nonlocal h2d
+        with torch.cuda.stream(cs):
+            din[t % 2].copy_(hin[t], non_blocking=True)
+            ev_in[t].record(cs)
+        h2d += hin[t].numel() * 2
+
+    h2d_token(0)
+    if T > 1:
+        h2d_token(1)
     for t in range(T):
+        stream.wait_event(ev_in[t])
+        if t >= 2:
+            stream.wait_event(ev_out[t - 2])       # dout[t % 2] drained to host
+        buf, ob = din[t % 2], dout[t % 2]
         for l in range(L):
-            dq.copy_(hq[t], non_blocking=True), dk.copy_(hk[t], non_blocking=True), dv.copy_(hv[t], non_blocking=True)
-            h2d += (hq[t].numel() + 2 * hk[t].numel()) * 2
-            ctx.decode_step_fused(l, dq, dk, dv, do, N + t, scale, ws)
-            ho[t, l].copy_(do, non_blocking=True)
-            d2h += do.numel() * 2
+            row = buf[l]
+            ctx.decode_step_fused(l, row[:nq].view(B, hq_, d), row[nq:nq + nk].view(B, hkv_, d),
+                                  row[nq + nk:].view(B, hkv_, d), ob[l], N + t, scale, ws)
+        ev_done[t].record(stream)
+        cs.wait_event(ev_done[t])
+        with torch.cuda.stream(cs):
+            hout[t].copy_(ob, non_blocking=True)
+            ev_out[t].record(cs)
+        d2h += ob.numel() * 2
+        if t + 2 < T:
+            h2d_token(t + 2)                        # din[t % 2] is free once token t is done
+    stream.wait_event(ev_out[T - 1])
     e2.record(stream)
     torch.cuda.synchronize()
     dec_ms = e1.elapsed_time(e2)
@@ -365,8 +403,9 @@ def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
         dec_ms = x.item()
     return {"value": B * T * world / (dec_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "prefill_ms": e0.elapsed_time(e1), "decode_ms": dec_ms,
-            "note": "1 step; prefill inputs of one layer staged host->device per layer; per layer-token "
-                    "q/k_new/v_new H2D and o D2H from pinned memory"}
+            "note": "1 step; prefill inputs of one layer staged host->device per layer (o read back); "
+                    "decode: per token one pinned H2D of q/k_new/v_new for all layers and one D2H of o "
+                    "for all layers, on a copy stream double-buffered against the decode launches"}
 
 
 def main():
