@@ -65,6 +65,7 @@ class MoAError(RuntimeError):
 
 
 def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    path = os.environ.get("MOA_LIB", path)  # diagnostic builds (tools/build_trace.py)
     if not os.path.exists(path):
         raise ImportError(
             f"libmoa.so not found at {path}: build it with `python -m paper_2406_14909_b200.build` "

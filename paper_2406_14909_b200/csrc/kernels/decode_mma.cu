@@ -19,8 +19,11 @@
 //    group are the M rows (zero-padded to 16), keys the N columns, so K/V
 //    bytes are read once for all heads and the instruction count per row is
 //    independent of G.  Online softmax in base 2 with a lazy running max.
-//  * The last CTA of a region (atomic ticket, self-resetting) merges the
-//    partials by LSE and writes o (and lse).
+//  * An epilogue warp keeps the consumers free of latency: it stages each
+//    segment's q rows in shared memory two segments ahead, takes the region's
+//    ticket (atomic, self-resetting) when the consumers finish a segment, and,
+//    if this CTA contributed last, merges the region's partials by LSE and
+//    writes o (and lse) while the consumers stream the next segment.
 //  * Fused append: the cache row of `pos` is masked in the tile path; the CTA
 //    owning it folds (k_new, v_new) into its state and writes it to the cache.
 #include <cuda.h>
@@ -38,14 +41,36 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kCW = 4;                    // consumer warps
-constexpr int kThreads = (kCW + 1) * 32;  // + producer warp
-constexpr int kRows = 16 * kCW;           // rows per tile
+#ifdef MOA_DEC_TRACE
+// diagnostic build only (tools/build_trace.sh): per-CTA %globaltimer stamps of two consecutive launches
+constexpr int kTraceCtas = 1024, kTraceFields = 8;
+__device__ unsigned long long g_trace[2][kTraceCtas][kTraceFields];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(f) \
+  if (blockIdx.x < kTraceCtas) g_trace[p.trace_slot][blockIdx.x][f] = gtime()
+#define TRACE_V(f, v) \
+  if (blockIdx.x < kTraceCtas) g_trace[p.trace_slot][blockIdx.x][f] = (v)
+#else
+#define TRACE(f)
+#define TRACE_V(f, v)
+#endif
+
+constexpr int kCW = 4;                      // consumer warps
+constexpr int kProd = kCW;                  // producer warp (TMA)
+constexpr int kEpi = kCW + 1;               // epilogue warp (q staging, tickets, combines)
+constexpr int kThreads = (kCW + 2) * 32;
+constexpr int kRows = 16 * kCW;             // rows per tile
 constexpr int kCtasPerSm = 2;
 constexpr float kRescale = 8.0f;
 
 template <int D>
 constexpr int part_stride() { return D + 4; }  // per-head partial: o[D], lse2, pad (16-B aligned)
+template <int D>
+constexpr int q_stride() { return D + 8; }     // staged q row (padding spreads the fragment reads over banks)
 
 template <int D, int STAGES>
 struct DCfg {
@@ -72,6 +97,10 @@ struct MParams {
   float *lse;
   float *part;
   int *counters;
+  int early;  // 1: the producer may stream the cache before the stream predecessor completes
+#ifdef MOA_DEC_TRACE
+  int trace_slot;
+#endif
 };
 
 struct Region {
@@ -80,7 +109,6 @@ struct Region {
 };
 
 constexpr int kMaxGroups = 128;
-constexpr int kMaxPend = 256;
 
 // region (b, g) holding absolute row x; g_off / win_g are staged in shared memory
 __device__ __forceinline__ Region region_of(const MParams &p, const int64_t *g_off, const int *win_g, int64_t x) {
@@ -123,95 +151,162 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *m, 
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  __syncwarp();
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// merge the partials of region ridx (slots of every CTA x warp that touched it) by LSE
+// Merge the partials of region ridx by LSE, one warp: one slot per CTA whose range touched
+// the region.  Lane l owns output elements l, l+32, ...;
+// the slot LSEs and partial vectors are read in batches of 8 independent loads, so the
+// merge costs ~ceil(slots/8) L2 round trips per head.
 template <int D>
-__device__ __forceinline__ void combine_region(const MParams &p, const int64_t *g_off, const int *win_g, int ridx,
-                                               int t0, int tstep) {
+__device__ __forceinline__ void combine_region_warp(const MParams &p, const int64_t *g_off, const int *win_g,
+                                                    int ridx, int lane) {
   constexpr int PS = part_stride<D>();
+  constexpr int NE = D / 32;
+  constexpr int KB = 8;
   const int b = ridx / p.ngl, g = ridx - b * p.ngl;
   const int G = p.G;
   const int64_t start = (int64_t)b * p.rows_per_seq + g_off[g];
   const int64_t end = start + p.n_sink + win_g[g];
   const int64_t c_first = start / p.rpc, c_last = (end - 1) / p.rpc;
-  const int64_t sl0 = (c_first + ridx) * kCW, sl1 = (c_last + ridx + 1) * kCW;
-  for (int t = t0; t < G * D; t += tstep) {
-    const int j = t / D, e = t - j * D;
-    float mx = -INFINITY;
-    for (int64_t sl = sl0; sl < sl1; ++sl) mx = fmaxf(mx, __ldcg(p.part + (sl * G + j) * PS + D));
-    float L = 0.f, O = 0.f;
-    for (int64_t sl = sl0; sl < sl1; ++sl) {
-      const float *pc = p.part + (sl * G + j) * PS;
-      const float ls = __ldcg(pc + D);
-      if (ls == -INFINITY) continue;
-      const float w = fast_exp2(ls - mx);
-      L += w;
-      O += w * __ldcg(pc + e);
+  const int64_t sl0 = c_first + ridx;
+  const int nsl = (int)(c_last - c_first + 1);
+  for (int j = 0; j < G; ++j) {
+    const float *base = p.part + (sl0 * G + j) * PS;
+    float mx = -INFINITY, L = 0.f, O[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) O[i] = 0.f;
+    for (int c0 = 0; c0 < nsl; c0 += KB) {
+      float ls[KB], v[KB][NE];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const bool in = c0 + k < nsl;
+        const float *pc = base + (int64_t)(c0 + k) * G * PS;
+        ls[k] = in ? __ldcg(pc + D) : -INFINITY;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) v[k][i] = in ? __ldcg(pc + lane + 32 * i) : 0.f;
+      }
+      float cm = ls[0];
+#pragma unroll
+      for (int k = 1; k < KB; ++k) cm = fmaxf(cm, ls[k]);
+      const float nm = fmaxf(mx, cm);
+      if (nm == -INFINITY) continue;
+      const float a = mx == -INFINITY ? 0.f : fast_exp2(mx - nm);
+      L *= a;
+#pragma unroll
+      for (int i = 0; i < NE; ++i) O[i] *= a;
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const float w = ls[k] == -INFINITY ? 0.f : fast_exp2(ls[k] - nm);
+        L += w;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) O[i] = fmaf(w, v[k][i], O[i]);
+      }
+      mx = nm;
     }
-    p.o[(int64_t)b * p.o_bs + (int64_t)(g * G + j) * D + e] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
-    if (p.lse && e == 0) p.lse[(int64_t)b * p.ngl * G + g * G + j] = L > 0.f ? (mx + __log2f(L)) * kLn2 : -INFINITY;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    __nv_bfloat16 *ob = p.o + (int64_t)b * p.o_bs + (int64_t)(g * G + j) * D;
+#pragma unroll
+    for (int i = 0; i < NE; ++i) ob[lane + 32 * i] = __float2bfloat16_rn(O[i] * inv);
+    if (p.lse && lane == 0) p.lse[(int64_t)b * p.ngl * G + g * G + j] = L > 0.f ? (mx + __log2f(L)) * kLn2 : -INFINITY;
   }
 }
 
 template <int D, int STAGES, int CPS>
 __global__ void __launch_bounds__(kThreads, CPS)
     decode_mma_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                      const __grid_constant__ CUtensorMap tm_k16, const __grid_constant__ CUtensorMap tm_v16,
                       const MParams p) {
   using C = DCfg<D, STAGES>;
   constexpr int NT = D / 8;   // output n-tiles (8 dims each)
   constexpr int KS = D / 16;  // k-steps over the head dim
+  constexpr int QS = q_stride<D>();
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full_bar[C::kStages], empty_bar[C::kStages];
+  __shared__ uint64_t q_full[2], seg_done[2];
   __shared__ int64_t s_goff[kMaxGroups];
   __shared__ int s_wing[kMaxGroups];
-  __shared__ int s_pend[kMaxPend];  // regions whose combine this CTA owes (deferred to the end)
-  __shared__ int s_npend;
+  __shared__ __align__(16) __nv_bfloat16 s_q[2][16 * QS];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  // per-warp partials of the two segments in flight: [2][kCW][G][D + 4] fp32 after the tiles
+  float *s_part = reinterpret_cast<float *>(smem_raw + (base - smem_u32(smem_raw)) + C::kStages * 2 * C::kTileBytes);
   const int64_t X0 = (int64_t)blockIdx.x * p.rpc;
   const int64_t X1 = X0 + p.rpc < p.R ? X0 + p.rpc : p.R;
+  if (tid == 0) TRACE(0);
 
   if (tid == 0) {
     for (int i = 0; i < C::kStages; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), kCW);
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&q_full[i]), 1);
+      mbar_init(smem_u32(&seg_done[i]), kCW);
+    }
     fence_mbar_init();
   }
-  if (tid == 0) s_npend = 0;
   for (int g = tid; g < p.ngl; g += kThreads) {
     s_goff[g] = p.g_off[g];
     s_wing[g] = p.win_g[g];
   }
   __syncthreads();
-  // programmatic dependent launch: everything above overlapped the previous kernel's tail;
-  // q / k_new / the cache / the tickets may be written by stream predecessors
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (X0 >= X1) return;
+  // Programmatic dependent launch.  Everything above overlapped the previous kernel's tail.
+  // The consumers and the epilogue warp wait for the stream predecessor (q, k_new, the
+  // workspace, the tickets and o may be its inputs/outputs) before they trigger the next
+  // launch, so a CTA's trigger implies its predecessor completed: when this kernel starts,
+  // every kernel before its predecessor has completed and flushed.  With p.early the host has
+  // established that the predecessor does not write this layer's cache, so the producer
+  // streams cache tiles at once.
+  if (tid == 0) TRACE(1);
+  if (X0 >= X1) {
+    griddep_wait();
+    return;
+  }
 
-  if (warp == kCW) {
+  if (warp == kProd) {
     // ------------------------------------------------------------ producer: TMA K/V tiles
     if (lane == 0) {
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
+      tma_prefetch_desc(&tm_k16);
+      tma_prefetch_desc(&tm_v16);
+      if (!p.early) griddep_wait();
+      TRACE(2);
       int T = 0;
+      bool trig = false;
       for (int64_t x = X0; x < X1;) {
         const Region rg = region_of(p, s_goff, s_wing, x);
         const int64_t seg_end = rg.end < X1 ? rg.end : X1;
         for (int64_t t0 = x; t0 < seg_end; t0 += kRows, ++T) {
           const int st = T % C::kStages;
-          if (T >= C::kStages) mbar_wait(smem_u32(&empty_bar[st]), ((T - C::kStages) / C::kStages) & 1);
+          if (T >= C::kStages) {
+            mbar_wait(smem_u32(&empty_bar[st]), ((T - C::kStages) / C::kStages) & 1);
+            if (!trig) {  // the consumers have passed their griddepcontrol.wait
+              griddep_launch_dependents();
+              trig = true;
+            }
+          }
           const uint32_t fb = smem_u32(&full_bar[st]);
-          mbar_expect_tx(fb, 2 * C::kTileBytes);
           const uint32_t kd = base + st * 2 * C::kTileBytes, vd = kd + C::kTileBytes;
-          for (int sl = 0; sl < C::kSlabs; ++sl) {
-            tma_load_2d(kd + sl * C::kSlabBytes, &tm_k, fb, sl * 64, (int)t0);
-            tma_load_2d(vd + sl * C::kSlabBytes, &tm_v, fb, sl * 64, (int)t0);
+          const int64_t nrows = seg_end - t0;
+          if (nrows >= kRows) {
+            mbar_expect_tx(fb, 2 * C::kTileBytes);
+            for (int sl = 0; sl < C::kSlabs; ++sl) {
+              tma_load_2d(kd + sl * C::kSlabBytes, &tm_k, fb, sl * 64, (int)t0);
+              tma_load_2d(vd + sl * C::kSlabBytes, &tm_v, fb, sl * 64, (int)t0);
+            }
+          } else {  // segment tail: only the 16-row groups that hold rows of the segment
+            const int n16 = ((int)nrows + 15) >> 4;
+            mbar_expect_tx(fb, 2 * n16 * 16 * D * 2);
+            for (int r = 0; r < n16; ++r)
+              for (int sl = 0; sl < C::kSlabs; ++sl) {
+                tma_load_2d(kd + sl * C::kSlabBytes + r * 2048, &tm_k16, fb, sl * 64, (int)t0 + 16 * r);
+                tma_load_2d(vd + sl * C::kSlabBytes + r * 2048, &tm_v16, fb, sl * 64, (int)t0 + 16 * r);
+              }
           }
         }
         x = seg_end;
@@ -220,16 +315,110 @@ __global__ void __launch_bounds__(kThreads, CPS)
     return;
   }
 
+  if (warp == kEpi) {
+    // ------------------------------------------------------------ epilogue warp
+    griddep_wait();
+    griddep_launch_dependents();
+    const int G = p.G;
+    int64_t xs = X0;  // staging cursor (runs two segments ahead of the consumers)
+    int ns = 0;
+    auto stage_next = [&]() {
+      if (xs >= X1) return;
+      const Region r = region_of(p, s_goff, s_wing, xs);
+      const __nv_bfloat16 *qb = p.q + (int64_t)r.b * p.q_bs + (int64_t)r.g * G * D;
+      __nv_bfloat16 *sq = s_q[ns & 1];
+      for (int v = lane; v < G * (D / 8); v += 32) {
+        const int h = v / (D / 8), e = (v - h * (D / 8)) * 8;
+        *reinterpret_cast<uint4 *>(sq + h * QS + e) = *reinterpret_cast<const uint4 *>(qb + h * D + e);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&q_full[ns & 1]));
+      xs = r.end < X1 ? r.end : X1;
+      ++ns;
+    };
+    stage_next();
+    stage_next();
+    int n = 0;
+    for (int64_t x = X0; x < X1; ++n) {
+      const Region rg = region_of(p, s_goff, s_wing, x);
+      const int64_t seg_end = rg.end < X1 ? rg.end : X1;
+      mbar_wait_warp(smem_u32(&seg_done[n & 1]), (n >> 1) & 1);
+      // every consumer warp's partial of segment n is in shared memory (mbarrier release/
+      // acquire): merge the kCW of them by LSE into this CTA's slot of the region
+      const int ridx = rg.b * p.ngl + rg.g;
+      {
+        constexpr int PS = part_stride<D>();
+        constexpr int NE = D / 32;
+        const float *sp = s_part + (size_t)(n & 1) * kCW * G * PS;
+        float *gp = p.part + ((int64_t)blockIdx.x + ridx) * G * PS;
+        for (int j = 0; j < G; ++j) {
+          float ls[kCW], mx = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < kCW; ++w) {
+            ls[w] = sp[(w * G + j) * PS + D];
+            mx = fmaxf(mx, ls[w]);
+          }
+          float L = 0.f, O[NE];
+#pragma unroll
+          for (int i = 0; i < NE; ++i) O[i] = 0.f;
+          if (mx != -INFINITY) {
+#pragma unroll
+            for (int w = 0; w < kCW; ++w) {
+              const float wt = ls[w] == -INFINITY ? 0.f : fast_exp2(ls[w] - mx);
+              L += wt;
+#pragma unroll
+              for (int i = 0; i < NE; ++i) O[i] = fmaf(wt, sp[(w * G + j) * PS + lane + 32 * i], O[i]);
+            }
+          }
+          const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+          for (int i = 0; i < NE; ++i) gp[j * PS + lane + 32 * i] = O[i] * inv;
+          if (lane == 0) gp[j * PS + D] = L > 0.f ? mx + __log2f(L) : -INFINITY;
+        }
+        __syncwarp();
+      }
+      int last = 0;
+      if (lane == 0) {
+        __threadfence();  // cumulative: orders the consumers' partials before the ticket
+        const int64_t c_first = rg.start / p.rpc, c_last = (rg.end - 1) / p.rpc;
+        int *ctr = p.counters + ridx;
+        const int ticket = atomicAdd(ctr, 1);
+        if (ticket == (int)(c_last - c_first)) {
+          *ctr = 0;  // self-reset for the next launch
+          last = 1;
+        }
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      stage_next();  // q of segment n+2 into the buffer segment n used
+      if (last) {
+        __threadfence();
+        combine_region_warp<D>(p, s_goff, s_wing, ridx, lane);
+      }
+      x = seg_end;
+    }
+    if (lane == 0) TRACE(6);
+    return;
+  }
+
   // -------------------------------------------------------------- consumers (warps 0..3)
+  griddep_wait();
+  griddep_launch_dependents();
+  if (tid == 0) TRACE(3);
   const int qr = lane >> 2, qc = lane & 3;  // fragment row (head) / column-pair index
   const int h0 = qr, h1 = qr + 8;           // the two head rows this lane holds
   const int s = p.n_sink;
   const int64_t pos = p.pos;
-  int T = 0;
-  for (int64_t x = X0; x < X1;) {
+  int T = 0, n = 0;
+#ifdef MOA_DEC_TRACE
+  int nseg = 0;
+#endif
+  for (int64_t x = X0; x < X1; ++n) {
     const Region rg = region_of(p, s_goff, s_wing, x);
     const int64_t seg_end = rg.end < X1 ? rg.end : X1;
     const int G = p.G;
+#ifdef MOA_DEC_TRACE
+    ++nseg;
+#endif
     const int W0 = h0 < G ? p.win_q[rg.g * G + h0] : rg.Wg;
     const int W1 = h1 < G ? p.win_q[rg.g * G + h1] : rg.Wg;
     const bool ring_live = pos >= s && rg.Wg > 0;
@@ -243,17 +432,18 @@ __global__ void __launch_bounds__(kThreads, CPS)
     const bool seg_full = pos - s >= (int64_t)rg.Wg - 1 && pos >= s &&
                           __reduce_min_sync(0xffffffffu, (unsigned)minW) >= (unsigned)rg.Wg;
 
-    // Q fragments (A operand, 16 x D, rows >= G are zero), unscaled bf16
+    // Q fragments (A operand, 16 x D, rows >= G are zero) from the staged rows, unscaled bf16
     uint32_t qa[KS][4];
     {
-      const __nv_bfloat16 *qb = p.q + (int64_t)rg.b * p.q_bs + (int64_t)rg.g * G * D;
+      mbar_wait_warp(smem_u32(&q_full[n & 1]), (n >> 1) & 1);
+      const __nv_bfloat16 *qb = s_q[n & 1];
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         const int c = ks * 16 + qc * 2;
-        qa[ks][0] = h0 < G ? *reinterpret_cast<const uint32_t *>(qb + h0 * D + c) : 0u;
-        qa[ks][1] = h1 < G ? *reinterpret_cast<const uint32_t *>(qb + h1 * D + c) : 0u;
-        qa[ks][2] = h0 < G ? *reinterpret_cast<const uint32_t *>(qb + h0 * D + c + 8) : 0u;
-        qa[ks][3] = h1 < G ? *reinterpret_cast<const uint32_t *>(qb + h1 * D + c + 8) : 0u;
+        qa[ks][0] = h0 < G ? *reinterpret_cast<const uint32_t *>(qb + h0 * QS + c) : 0u;
+        qa[ks][1] = h1 < G ? *reinterpret_cast<const uint32_t *>(qb + h1 * QS + c) : 0u;
+        qa[ks][2] = h0 < G ? *reinterpret_cast<const uint32_t *>(qb + h0 * QS + c + 8) : 0u;
+        qa[ks][3] = h1 < G ? *reinterpret_cast<const uint32_t *>(qb + h1 * QS + c + 8) : 0u;
       }
     }
     float o[NT][4];
@@ -265,8 +455,14 @@ __global__ void __launch_bounds__(kThreads, CPS)
       const int st = T % C::kStages;
       const int nrows = (int)((seg_end - t0) < kRows ? (seg_end - t0) : kRows);
       mbar_wait_warp(smem_u32(&full_bar[st]), (T / C::kStages) & 1);
+      if (tid == 0 && T == 0) TRACE(4);
       const uint32_t kb = base + st * 2 * C::kTileBytes, vb = kb + C::kTileBytes;
       const int k0 = warp * 16;  // this warp's first key row in the tile
+      if (k0 >= nrows) {         // rows past a segment tail were not loaded
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
+        continue;
+      }
 
       // ---- S = Q K^T  (16 heads x 16 keys); two accumulators per n-tile halve the HMMA chain
       float sacc[2][4], sacc2[2][4];
@@ -386,12 +582,12 @@ __global__ void __launch_bounds__(kThreads, CPS)
       if (xr >= x && xr < seg_end) {
         const __nv_bfloat16 *kn = p.k_new + (int64_t)rg.b * p.kv_bs + (int64_t)rg.g * D;
         const __nv_bfloat16 *vn = p.v_new + (int64_t)rg.b * p.kv_bs + (int64_t)rg.g * D;
-        const __nv_bfloat16 *qb = p.q + (int64_t)rg.b * p.q_bs + (int64_t)rg.g * G * D;
+        const __nv_bfloat16 *qb = s_q[n & 1];
         float d0 = 0.f, d1 = 0.f;
         for (int e = qc * (D / 4); e < (qc + 1) * (D / 4); ++e) {
           const float kf = __bfloat162float(kn[e]);
-          if (h0 < G) d0 = fmaf(__bfloat162float(qb[h0 * D + e]), kf, d0);
-          if (h1 < G) d1 = fmaf(__bfloat162float(qb[h1 * D + e]), kf, d1);
+          if (h0 < G) d0 = fmaf(__bfloat162float(qb[h0 * QS + e]), kf, d0);
+          if (h1 < G) d1 = fmaf(__bfloat162float(qb[h1 * QS + e]), kf, d1);
         }
         d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
         d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
@@ -436,15 +632,14 @@ __global__ void __launch_bounds__(kThreads, CPS)
       }
     }
 
-    // ---- per-warp partial of this segment: o / l and lse2
+    // ---- per-warp partial of this segment (o / l and lse2) into shared memory; hand the
+    //      segment to the epilogue warp
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-    const int ridx = rg.b * p.ngl + rg.g;
-    const int64_t slot = ((int64_t)blockIdx.x + ridx) * kCW + warp;
     constexpr int PS = part_stride<D>();
-    float *part = p.part + slot * G * PS;
+    float *part = s_part + ((size_t)(n & 1) * kCW + warp) * G * PS;
     {
       const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
 #pragma unroll
@@ -458,30 +653,18 @@ __global__ void __launch_bounds__(kThreads, CPS)
         if (h1 < G) part[h1 * PS + D] = l1 > 0.f ? m1 + __log2f(l1) : -INFINITY;
       }
     }
-    named_bar_sync(1, kCW * 32);
-    if (tid == 0) {
-      __threadfence();  // cumulative: orders every consumer's partial (seen via bar.sync) before the ticket
-      const int64_t c_first = rg.start / p.rpc, c_last = (rg.end - 1) / p.rpc;
-      int *ctr = p.counters + ridx;
-      const int ticket = atomicAdd(ctr, 1);
-      if (ticket == (int)(c_last - c_first)) {  // last contributor: combine later (deferred)
-        *ctr = 0;                                // self-reset for the next launch
-        if (s_npend < kMaxPend) {
-          s_pend[s_npend++] = ridx;
-        } else {  // (only with very many tiny regions) merge right away, single-threaded
-          __threadfence();
-          combine_region<D>(p, s_goff, s_wing, ridx, 0, 1);
-        }
-      }
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&seg_done[n & 1]));
     x = seg_end;
   }
-
-  // ---- deferred combines of the regions this CTA completed last
-  named_bar_sync(1, kCW * 32);
-  const int npend = s_npend;
-  if (npend > 0) __threadfence();
-  for (int k = 0; k < npend; ++k) combine_region<D>(p, s_goff, s_wing, s_pend[k], tid, kCW * 32);
+  if (tid == 0) TRACE(5);
+#ifdef MOA_DEC_TRACE
+  if (tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    TRACE_V(7, (unsigned long long)T | ((unsigned long long)nseg << 40) | ((unsigned long long)smid << 48));
+  }
+#endif
 }
 
 int num_sms_dev() {
@@ -529,21 +712,29 @@ int launch_v(const DecodeMmaArgs &a, void *stream) {
   p.lse = a.lse;
   p.part = a.ws_part;
   p.counters = a.counters;
-  cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D, STAGES, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  p.early = a.early_read;
+#ifdef MOA_DEC_TRACE
+  static int launch_no = 0;
+  p.trace_slot = (launch_no++) & 1;
+#endif
+  const int smem = C::kSmem + 2 * kCW * a.G * part_stride<D>() * 4;
+  cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D, STAGES, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return (int)e;
   const CUtensorMap *km = static_cast<const CUtensorMap *>(a.kmap);
   const CUtensorMap *vm = static_cast<const CUtensorMap *>(a.vmap);
+  const CUtensorMap *km16 = static_cast<const CUtensorMap *>(a.kmap16);
+  const CUtensorMap *vm16 = static_cast<const CUtensorMap *>(a.vmap16);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)n);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, decode_mma_kernel<D, STAGES, CPS>, *km, *vm, p);
+  e = cudaLaunchKernelEx(&cfg, decode_mma_kernel<D, STAGES, CPS>, *km, *vm, *km16, *vm16, p);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
@@ -567,9 +758,15 @@ int launch_d(const DecodeMmaArgs &a, void *stream) {
 }  // namespace
 
 size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d) {
-  const size_t slots = ((size_t)num_sms_dev() * kCtasPerSm + (size_t)batch * ngl + 1) * kCW;
+  const size_t slots = (size_t)num_sms_dev() * kCtasPerSm + (size_t)batch * ngl + 1;  // (CTA, region) slots
   return ((slots * G * (d + 4) * 4) + 255) & ~size_t(255);
 }
+
+#ifdef MOA_DEC_TRACE
+extern "C" int moa_debug_decode_trace(void *host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace));
+}
+#endif
 
 int launch_decode_mma(const DecodeMmaArgs &a, void *stream) {
   if (a.d == 128) return launch_d<128>(a, stream);

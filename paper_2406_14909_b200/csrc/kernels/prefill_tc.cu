@@ -527,12 +527,12 @@ bool make_tile_map(void *m, const void *ptr, int D, int H, int64_t N, int B, int
   return r == CUDA_SUCCESS;
 }
 
-bool encode_cache_map(void *map_out, const void *ptr, int D, int64_t rows) {
+bool encode_cache_map(void *map_out, const void *ptr, int D, int64_t rows, int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-  cuuint32_t box[2] = {64, 64};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(static_cast<CUtensorMap *>(map_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr),
                    dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

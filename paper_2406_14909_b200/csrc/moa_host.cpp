@@ -386,6 +386,7 @@ moa_status moa_bind_layer_cache(moa_ctx *ctx, int layer, void *k_cache, void *v_
   p.bound_batch = batch;
   p.next_pos = 0;
   p.maps_ok = false;
+  ctx->last_cache_write = moa_ctx::kAllLayers;
   if (ctx->device >= 0) {
     // rows not yet reached by the sequence must hold finite values: the tensor-core decode
     // multiplies masked rows by a zero probability, and 0 * NaN would poison the sum
@@ -398,7 +399,10 @@ moa_status moa_bind_layer_cache(moa_ctx *ctx, int layer, void *k_cache, void *v_
   if (ctx->device >= 0 && ctx->dtype == MOA_BF16) {
     DeviceGuard dg(ctx->device);
     const int64_t rows = (int64_t)batch * p.rows_per_seq;
-    if (!moa::encode_cache_map(p.kmap, k_cache, ctx->d, rows) || !moa::encode_cache_map(p.vmap, v_cache, ctx->d, rows))
+    if (!moa::encode_cache_map(p.kmap, k_cache, ctx->d, rows, 64) ||
+        !moa::encode_cache_map(p.vmap, v_cache, ctx->d, rows, 64) ||
+        !moa::encode_cache_map(p.kmap16, k_cache, ctx->d, rows, 16) ||
+        !moa::encode_cache_map(p.vmap16, v_cache, ctx->d, rows, 16))
       return fail(MOA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the layer %d cache", layer);
     p.maps_ok = true;
   }
@@ -469,7 +473,10 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
   int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_tc(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
-  if (!fill) return ok();
+  if (!fill) {
+    ctx->last_cache_write = -1;
+    return ok();
+  }
   moa::CacheArgs c{};
   c.k = k; c.v = v; c.row_stride = kv_row_stride; c.k_cache = p.k_cache; c.v_cache = p.v_cache;
   c.rows_per_seq = p.rows_per_seq; c.d_g_off = p.d_g_off; c.d_win_g = p.d_win_g;
@@ -479,6 +486,7 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   e = moa::launch_cache_fill(c, stream);
   if (e) return cuda_fail((cudaError_t)e, "cache fill launch");
   p.next_pos = N;
+  ctx->last_cache_write = layer;
   return ok();
 }
 
@@ -519,6 +527,7 @@ moa_status moa_cache_fill(moa_ctx *ctx, int layer, const void *k, const void *v,
   int e = moa::launch_cache_fill(c, stream);
   if (e) return cuda_fail((cudaError_t)e, "cache fill launch");
   p.next_pos = N;
+  ctx->last_cache_write = layer;
   return ok();
 }
 
@@ -544,7 +553,17 @@ moa_status moa_kv_append(moa_ctx *ctx, int layer, const void *k_new, const void 
   int e = moa::launch_kv_append(c, stream);
   if (e) return cuda_fail((cudaError_t)e, "kv_append launch");
   p.next_pos = pos + 1;
+  ctx->last_cache_write = layer;
   return ok();
+}
+
+// MOA_DEC_EARLY=0 disables the early cache streaming of the decode kernel (diagnostics)
+static bool early_read_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("MOA_DEC_EARLY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const void *k_new,
@@ -582,16 +601,19 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
     if (ctx->ngl > 128) return fail(MOA_ERR_UNSUPPORTED, "more than 128 local kv-groups");
     if (!p.maps_ok) return fail(MOA_ERR_STATE, "layer %d cache has no tensor maps (re-bind the cache)", layer);
     moa::DecodeMmaArgs m{};
-    m.kmap = p.kmap; m.vmap = p.vmap; m.q = q; m.o = o; m.q_bs = q_batch_stride; m.o_bs = o_batch_stride;
+    m.kmap = p.kmap; m.vmap = p.vmap; m.kmap16 = p.kmap16; m.vmap16 = p.vmap16; m.q = q; m.o = o; m.q_bs = q_batch_stride; m.o_bs = o_batch_stride;
     m.k_new = fused ? k_new : nullptr; m.v_new = fused ? v_new : nullptr; m.kv_bs = kv_batch_stride;
     m.k_cache = p.k_cache; m.v_cache = p.v_cache; m.rows_per_seq = p.rows_per_seq;
     m.d_g_off = p.d_g_off; m.d_win_g = p.d_win_g; m.d_win_q = p.d_win_q;
     m.ngl = ctx->ngl; m.G = ctx->G; m.d = ctx->d; m.n_sink = p.n_sink; m.batch = batch;
     m.pos = pos; m.scale = scale; m.lse = lse_out; m.ws_part = static_cast<float *>(workspace);
     m.counters = p.d_counters;
+    m.early_read = early_read_enabled() && ctx->last_cache_write != layer &&
+                   ctx->last_cache_write != moa_ctx::kAllLayers;
     int e = moa::launch_decode_mma(m, stream);
     if (e) return cuda_fail((cudaError_t)e, "decode launch");
     if (fused) p.next_pos = pos + 1;
+    ctx->last_cache_write = fused ? layer : -1;
     return ok();
   }
   moa::DecodeArgs a{};
@@ -608,6 +630,7 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
   int e = moa::launch_decode(a, ctx->dtype, fused, stream);
   if (e) return cuda_fail((cudaError_t)e, "decode launch");
   if (fused) p.next_pos = pos + 1;
+  ctx->last_cache_write = fused ? layer : -1;
   return ok();
 }
 

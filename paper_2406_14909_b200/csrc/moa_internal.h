@@ -114,8 +114,10 @@ struct LayerPlan {
   int *d_counters = nullptr;     // [max_batch, ngl] decode combine tickets (zeroed at upload)
   // TMA tensor maps (CUtensorMap, 128 B) over the bound K / V cache of this layer:
   // 2D [bound_batch * rows_per_seq rows, d], 64-row x 64-col boxes, 128B swizzle
-  alignas(64) unsigned char kmap[128] = {};
+  alignas(64) unsigned char kmap[128] = {};    // 64-row boxes
   alignas(64) unsigned char vmap[128] = {};
+  alignas(64) unsigned char kmap16[128] = {};  // 16-row boxes (tile tails)
+  alignas(64) unsigned char vmap16[128] = {};
   bool maps_ok = false;
   // bound cache
   void *k_cache = nullptr;
@@ -132,6 +134,10 @@ struct moa_ctx {
   int L = 0, Hq = 0, Hkv = 0, G = 1, d = 128, max_batch = 1;
   int g0 = 0, g1 = 0, ngl = 0, nql = 0;  // local groups [g0, g1), counts
   std::vector<moa::LayerPlan> layers;
+  // layer whose cache the most recent launch of this context wrote: -1 none, kAllLayers unknown
+  // (after a bind); lets a decode launch stream its cache before its stream predecessor ends
+  static constexpr int kAllLayers = -2;
+  int last_cache_write = kAllLayers;
 };
 
 namespace moa {
@@ -194,7 +200,8 @@ size_t decode_ws_bytes(int batch, int n_chunks, int G, int d);
 
 // bf16 decode on mma.sync with TMA-staged swizzled cache tiles (decode_mma.cu)
 struct DecodeMmaArgs {
-  const void *kmap, *vmap;     // host CUtensorMap images
+  const void *kmap, *vmap;     // host CUtensorMap images, 64-row boxes
+  const void *kmap16, *vmap16; // 16-row boxes for the partial last tile of a segment
   const void *q;
   void *o;
   int64_t q_bs, o_bs;
@@ -210,11 +217,12 @@ struct DecodeMmaArgs {
   float *lse;
   float *ws_part;
   int *counters;
+  int early_read;              // see decode_common: predecessor does not write this layer's cache
 };
 int launch_decode_mma(const DecodeMmaArgs &a, void *stream);
 size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d);
 
-// TMA tensor map over a [rows, d] bf16 cache (box 64 rows x 64 cols, 128B swizzle).
-bool encode_cache_map(void *map_out, const void *ptr, int d, int64_t rows);
+// TMA tensor map over a [rows, d] bf16 cache (box box_rows x 64 cols, 128B swizzle).
+bool encode_cache_map(void *map_out, const void *ptr, int d, int64_t rows, int box_rows);
 
 }  // namespace moa

@@ -20,15 +20,65 @@ import paper_2406_14909_b200 as moa  # noqa: E402
 from moa_workloads import CONFIGS, decode_tokens, rule_table  # noqa: E402
 
 
+def dump_trace():
+    import ctypes
+
+    import numpy as np
+
+    from paper_2406_14909_b200 import _lib
+    buf = np.zeros((2, 1024, 8), dtype=np.uint64)
+    fn = _lib.lib().moa_debug_decode_trace
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    assert fn(buf.ctypes.data, buf.nbytes) == 0
+    names = ["entry", "prologue", "prod_start", "cons_wait", "first_tile", "loop_end", "end"]
+    valid = [buf[s_][:, 0] > 0 for s_ in range(2)]
+    t0 = min(int(buf[s_][valid[s_], 0].min()) for s_ in range(2))
+    for s_ in range(2):
+        b = buf[s_][valid[s_]].astype(np.int64)
+        rel = (b[:, :7] - t0) / 1e3
+        print(f"launch slot {s_}: {len(b)} CTAs (us from the first entry of both launches)")
+        for i, n in enumerate(names):
+            col = rel[:, i]
+            print(f"  {n:11s} min {col.min():8.2f}  med {np.median(col):8.2f}  max {col.max():8.2f}")
+        tiles = b[:, 7] & 0xffffffff
+        npend = (b[:, 7] >> 32) & 0xff
+        nseg = (b[:, 7] >> 40) & 0xff
+        smid = (b[:, 7] >> 48) & 0xffff
+        print(f"  tiles/CTA min {tiles.min()} max {tiles.max()}; pending combines max {npend.max()}")
+        loop = rel[:, 5] - rel[:, 4]
+        comb = rel[:, 6] - rel[:, 5]
+        for k in sorted(set(nseg.tolist())):
+            m = nseg == k
+            print(f"  nseg={k}: {m.sum():3d} CTAs, loop us med {np.median(loop[m]):6.2f} max {loop[m].max():6.2f}, "
+                  f"tiles med {np.median(tiles[m]):.0f}")
+        for k in sorted(set(npend.tolist())):
+            m = npend == k
+            print(f"  npend={k}: {m.sum():3d} CTAs, combine us med {np.median(comb[m]):6.2f} max {comb[m].max():6.2f}")
+        per_tile = loop / np.maximum(tiles, 1)
+        order = np.argsort(-loop)[:8]
+        print("  slowest CTAs (cta, sm, tiles, nseg, loop us, us/tile):",
+              [(int(i), int(smid[i]), int(tiles[i]), int(nseg[i]), round(float(loop[i]), 2),
+                round(float(per_tile[i]), 2)) for i in order])
+        # per-SM: sum of loop of its CTAs
+        sm_t = {}
+        for i in range(len(b)):
+            sm_t.setdefault(int(smid[i]), []).append(float(per_tile[i]))
+        v = np.array([np.mean(x) for x in sm_t.values()])
+        print(f"  us/tile by SM: min {v.min():.2f} med {np.median(v):.2f} max {v.max():.2f}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--tokens", type=int, default=64)
     ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--trace", action="store_true", help="read the per-CTA stamps (MOA_LIB=libmoa_trace.so)")
+    ap.add_argument("--read-peak", action="store_true", help="also time a plain 4 GiB read (torch sum)")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     L = a.layers or cfg.layers
-    B, N, s, d, G = cfg.batch, cfg.N, cfg.n_sink, cfg.head_dim, cfg.hq // cfg.hkv
+    B, N, s, d, G = a.batch or cfg.batch, cfg.N, cfg.n_sink, cfg.head_dim, cfg.hq // cfg.hkv
     dev = torch.device("cuda")
     t = rule_table(cfg.name)
     ctx = moa.MoAContext(L, cfg.hq, cfg.hkv, d, B, dtype=torch.bfloat16)
@@ -80,14 +130,28 @@ def main():
             ctx.cache_fill(l, kp, vp)
         torch.cuda.synchronize()
 
-    for mode in (False, True, False, True):
+    for mode in (True, False, True, False):
         reset()
         phase(mode)          # warm
         reset()
         tot, k = phase(mode)
         print(f"per-launch events={mode!s:5}  phase {tot:7.2f} us/launch ({by / tot / 1e3:7.1f} GB/s)   "
               f"kernel events {k:7.2f} us ({by / k / 1e3 if k == k else float('nan'):7.1f} GB/s)", flush=True)
-    print(f"bytes/launch {by / 1e6:.1f} MB, variant {os.environ.get('MOA_DEC_VARIANT', '0')}")
+    if a.trace:
+        dump_trace()
+    print(f"bytes/launch {by / 1e6:.1f} MB, batch {B}, variant {os.environ.get('MOA_DEC_VARIANT', '0')}")
+    if a.read_peak:
+        del kp, vp
+        x = torch.empty(2 * 1024**3, dtype=torch.bfloat16, device=dev).uniform_()
+        for _ in range(3):
+            x.sum(dtype=torch.float32)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            x.sum(dtype=torch.float32)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"torch sum read: {10 * x.numel() * 2 / (e0.elapsed_time(e1) / 1e3) / 1e9:.1f} GB/s")
 
 
 if __name__ == "__main__":
