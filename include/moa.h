@@ -186,7 +186,17 @@ moa_status moa_decode_step(moa_ctx *ctx, int layer, const void *q, void *o,
                            size_t ws_bytes, moa_stream_t stream);
 
 /* Append + decode in one launch (a6 + a7 + a8 fused): identical results to
- * moa_kv_append(pos) followed by moa_decode_step(pos). */
+ * moa_kv_append(pos) followed by moa_decode_step(pos).
+ *
+ * Stream overlap (both decode calls, bf16): the kernel is launched with
+ * programmatic stream serialization.  It reads q, k_new, v_new and writes o,
+ * lse, the workspace and the cache only after its stream predecessor has
+ * completed, and it lets its successor launch only after that point.  When the
+ * most recent launch made through this context did not write this layer's
+ * cache (e.g. it decoded another layer), the kernel starts streaming the
+ * layer's cache rows while its predecessor is still running.  The cache is
+ * owned by the library after binding: the caller must not write it, and
+ * launches of one context go to one stream. */
 moa_status moa_decode_step_fused(moa_ctx *ctx, int layer, const void *q, const void *k_new,
                                  const void *v_new, void *o, int64_t q_batch_stride,
                                  int64_t kv_batch_stride, int64_t o_batch_stride, int batch,

@@ -151,6 +151,21 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *m, 
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// Consumer <-> epilogue hand-offs use named barriers (arrive by the producing side, sync by
+// the consuming side), one per parity of the segment index: q_full (epilogue staged q of a
+// segment) and seg_done (consumers wrote their partials of a segment).  A side reuses a
+// barrier id two segments later only after a hand-off in the other direction, so phases
+// never overlap.
+constexpr int kBarQFull = 1, kBarSegDone = 3;  // ids 1,2 and 3,4 (0 is __syncthreads)
+constexpr int kHandoff = (kCW + 1) * 32;       // consumers + epilogue warp
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  __syncwarp();
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  __syncwarp();
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -225,7 +240,6 @@ __global__ void __launch_bounds__(kThreads, CPS)
   constexpr int QS = q_stride<D>();
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full_bar[C::kStages], empty_bar[C::kStages];
-  __shared__ uint64_t q_full[2], seg_done[2];
   __shared__ int64_t s_goff[kMaxGroups];
   __shared__ int s_wing[kMaxGroups];
   __shared__ __align__(16) __nv_bfloat16 s_q[2][16 * QS];
@@ -242,10 +256,6 @@ __global__ void __launch_bounds__(kThreads, CPS)
     for (int i = 0; i < C::kStages; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), kCW);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&q_full[i]), 1);
-      mbar_init(smem_u32(&seg_done[i]), kCW);
     }
     fence_mbar_init();
   }
@@ -331,8 +341,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
         const int h = v / (D / 8), e = (v - h * (D / 8)) * 8;
         *reinterpret_cast<uint4 *>(sq + h * QS + e) = *reinterpret_cast<const uint4 *>(qb + h * D + e);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&q_full[ns & 1]));
+      named_bar_arrive(kBarQFull + (ns & 1), kHandoff);
       xs = r.end < X1 ? r.end : X1;
       ++ns;
     };
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
     for (int64_t x = X0; x < X1; ++n) {
       const Region rg = region_of(p, s_goff, s_wing, x);
       const int64_t seg_end = rg.end < X1 ? rg.end : X1;
-      mbar_wait_warp(smem_u32(&seg_done[n & 1]), (n >> 1) & 1);
+      named_bar_sync(kBarSegDone + (n & 1), kHandoff);
       // every consumer warp's partial of segment n is in shared memory (mbarrier release/
       // acquire): merge the kCW of them by LSE into this CTA's slot of the region
       const int ridx = rg.b * p.ngl + rg.g;
@@ -435,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
     // Q fragments (A operand, 16 x D, rows >= G are zero) from the staged rows, unscaled bf16
     uint32_t qa[KS][4];
     {
-      mbar_wait_warp(smem_u32(&q_full[n & 1]), (n >> 1) & 1);
+      named_bar_sync(kBarQFull + (n & 1), kHandoff);
       const __nv_bfloat16 *qb = s_q[n & 1];
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
@@ -653,8 +662,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
         if (h1 < G) part[h1 * PS + D] = l1 > 0.f ? m1 + __log2f(l1) : -INFINITY;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&seg_done[n & 1]));
+    named_bar_arrive(kBarSegDone + (n & 1), kHandoff);
     x = seg_end;
   }
   if (tid == 0) TRACE(5);

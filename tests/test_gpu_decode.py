@@ -226,3 +226,56 @@ def test_decode_state_errors(moa):
         ctx.decode_step(0, q, q.clone(), 0, 0.1, ws[:8])
     ctx.decode_step(0, q, q.clone(), 0, 0.1, ws)
     torch.cuda.synchronize()
+
+
+def test_multilayer_stream_overlap_no_sync(moa):
+    """Decode launches of several layers back to back with no host sync, as a
+    model would issue them: q/k_new/v_new are written into REUSED buffers by a
+    torch kernel right before every launch and o is copied out right after,
+    so a decode that read its inputs (or wrote o) before its predecessor
+    finished, or streamed a cache the predecessor was still writing, fails.
+    Covers the early cache streaming between layers (include/moa.h) and the
+    full-wait path (kv_append + decode_step of the same layer)."""
+    dev = torch.device("cuda")
+    dtype = torch.bfloat16
+    L, B, Hq, Hkv, d, s, N, T = 3, 2, 8, 4, 128, 4, 300, 40
+    G = Hq // Hkv
+    wins = [[1, 37, 128, 0, 299, 64, 5, 200], [300, 300, 10, 10, 90, 91, 2, 3], [0, 0, 64, 65, 17, 250, 130, 1]]
+    ctx = moa.MoAContext(L, Hq, Hkv, d, B, dtype=dtype)
+    for l in range(L):
+        ctx.set_spans(l, wins[l], s, N)
+    ctx.alloc_cache(B)
+    ws = ctx.alloc_workspace(B)
+    scale = 1 / math.sqrt(d)
+    K = [normal((B, N + T, Hkv, d), 700 + 10 * l, dtype) for l in range(L)]
+    V = [normal((B, N + T, Hkv, d), 701 + 10 * l, dtype) for l in range(L)]
+    Q = [normal((T, B, Hq, d), 702 + 10 * l, dtype) for l in range(L)]
+    Kg, Vg, Qg = [x.to(dev) for x in K], [x.to(dev) for x in V], [x.to(dev) for x in Q]
+    for l in range(L):
+        ctx.cache_fill(l, Kg[l][:, :N].contiguous(), Vg[l][:, :N].contiguous())
+    qbuf = torch.empty(B, Hq, d, dtype=dtype, device=dev)
+    kbuf = torch.empty(B, Hkv, d, dtype=dtype, device=dev)
+    vbuf = torch.empty(B, Hkv, d, dtype=dtype, device=dev)
+    obuf = torch.empty(B, Hq, d, dtype=dtype, device=dev)
+    out = torch.empty(T, L, B, Hq, d, dtype=dtype, device=dev)
+    for t in range(T):
+        p = N + t
+        for l in range(L):
+            qbuf.copy_(Qg[l][t])
+            kbuf.copy_(Kg[l][:, p])
+            vbuf.copy_(Vg[l][:, p])
+            if l == 1 and t % 2:   # the two-call path of the same layer: the decode must fully wait
+                ctx.kv_append(l, kbuf, vbuf, p)
+                ctx.decode_step(l, qbuf, obuf, p, scale, ws)
+            else:
+                ctx.decode_step_fused(l, qbuf, kbuf, vbuf, obuf, p, scale, ws)
+            out[t, l].copy_(obuf)
+    torch.cuda.synchronize()
+    for l in range(L):
+        Kf, Vf = f64(K[l]), f64(V[l])
+        for t in range(T):
+            p = N + t
+            ref, _ = oracle.decode(f64(Q[l][t]), Kf[:, : p + 1], Vf[:, : p + 1], p, wins[l], s, scale)
+            err = np.abs(f64(out[t, l]) - ref).max()
+            assert err < TOL[dtype], (l, t, err)
+        check_cache_image(ctx, l, K[l], V[l], N + T - 1, wins[l], s, B, G)
