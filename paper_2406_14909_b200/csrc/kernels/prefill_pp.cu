@@ -1,0 +1,556 @@
+// prefill_pp.cu -- MoA causal prefill on the sm_100a tensor cores, two q tiles per CTA
+// ping-ponged on one tensor core (tcgen05 + TMEM + TMA), bf16 I/O, fp32 accumulation
+// (SURVEY §8(a) a4).
+//
+//   O[b,i,h] = sum_{j in V(h,i)} softmax_j(tau q_i . k_j) v_j       (Eq. 1)
+//   V(h,i)   = { j <= i : j < s  or  i - j < W_h }                   (reading c3)
+//
+// A work item is 256 query rows of one (batch, q-head): q tiles Q0 = rows [i0, i0+128) and
+// Q1 = rows [i0+128, i0+256).  The kv tiles of both block-skip schedules are walked once
+// (kv_block_tiles: sinks U window, ascending); each K/V tile is loaded once and used by the
+// q tiles whose own schedule contains it.  FULL tiles skip the mask arithmetic.
+//
+// Warp roles (384 threads, one CTA per SM, persistent over a static slice of the LPT list):
+//   warps 0-3  softmax of Q0 (thread t owns row t = TMEM lane t, all 128 S columns)
+//   warps 4-7  softmax of Q1
+//   warp 8     TMA producer of the K and V rings
+//   warp 9     TMEM allocator + MMA issuer (whole warp waits, one elected lane issues)
+//   warp 10    TMA producer of Q0 / Q1; warp 11 idle
+// setmaxnreg moves registers from warpgroup 2 (producers, MMA) to the softmax warpgroups.
+// TMEM (512 columns): S0 | S1 (fp32 128x128; P_j, bf16 packed, overwrites the first 64
+// columns of S_j once the softmax has it in registers) | O0 | O1 (fp32 128xD).
+// Per kv step the MMA warp issues  PV0(prev), S0(next), PV1(prev), S1(next):  while the
+// softmax of Q1 runs the tensor core computes Q0's products and vice versa, so the tensor
+// pipe never waits for one softmax.  tcgen05 ops of one thread execute in issue order and a
+// commit covers every earlier op, so S_j(t) complete implies PV_j(t-1) complete (O_j may be
+// rescaled, P_j may be overwritten).  The running max is refreshed (and O rescaled in TMEM)
+// only when it grows by more than 2^8.  Exponentials run on MUFU ex2 except one pair in four,
+// which a degree-3 polynomial computes on the FMA pipe with packed f32x2 arithmetic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "../moa_internal.h"
+#include "common.cuh"
+#include "ptx_sm100.cuh"
+
+namespace moa {
+
+bool make_tile_map(void *m, const void *ptr, int D, int H, int64_t N, int B, int64_t row_stride, int box_rows);
+
+namespace {
+
+using namespace ptx;
+
+constexpr int kM = 128;    // q rows per tile (MMA M)
+constexpr int kN = 128;    // keys per kv tile
+constexpr int kThreads = 384;  // warp 11 idles (warpgroup-aligned register reallocation)
+constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10;
+constexpr uint32_t kTmemCols = 512;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kPolyEvery = 4;              // pair c uses the polynomial iff c % kPolyEvery == kPolyEvery - 1
+constexpr int kSoftmaxWarpsPerTile = 4;
+
+template <int D>
+struct PCfg {
+  static constexpr int kSlabs = D / 64;
+  static constexpr int kTileBytes = kM * D * 2;
+  static constexpr int kSlabBytes = kM * 128;
+  static constexpr int kNK = D == 128 ? 3 : 6;
+  static constexpr int kNV = D == 128 ? 2 : 4;
+  static constexpr int kSmemBytes = (2 + kNK + kNV) * kTileBytes + 1024;
+  static constexpr uint32_t kColO0 = 256, kColO1 = 256 + D;
+};
+
+struct PpParams {
+  void *o;
+  float *lse;
+  int64_t o_row_stride;
+  int64_t N;
+  int batch, n_items, nql, G, n_sink;
+  float scale_log2;
+  const int32_t *win_q;
+  const int32_t *items;  // (q-head, q-block) pairs, LPT order
+};
+
+struct PBars {
+  uint64_t q_full[2], q_empty[2];
+  uint64_t k_full[6], k_empty[6];
+  uint64_t v_full[4], v_empty[4];
+  uint64_t s_full[2], p_full[2];
+  uint64_t o_full[2], o_empty[2];
+  uint32_t tmem_base;
+};
+
+struct PItem {
+  int b, h, W;
+  int64_t i0;
+  BlockTiles bt;
+};
+
+__device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
+  PItem it;
+  const int wi = idx / p.batch;
+  it.b = idx - wi * p.batch;
+  it.h = p.items[2 * wi];
+  it.i0 = (int64_t)p.items[2 * wi + 1] * (2 * kM);
+  it.W = p.win_q[it.h];
+  it.bt = kv_block_tiles(it.i0, p.N, it.W, p.n_sink);
+  return it;
+}
+
+// which q tiles use union step k (tile t); false/false = skipped by every role
+__device__ __forceinline__ void step_use(const BlockTiles &bt, int k, int &t, bool &u0, bool &u1) {
+  t = bt.at(k);
+  u0 = tile_in(bt.r[0], t);
+  u1 = bt.has1 && tile_in(bt.r[1], t);
+}
+
+// ---------------------------------------------------------------- packed f32x2 arithmetic
+__device__ __forceinline__ uint64_t f2pk(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2upk(uint64_t r, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// 2^y for a pair on the FMA/ALU pipes: y = n + f, n = round(y), |f| <= 1/2, 2^f by a
+// degree-3 polynomial (relative error 7.7e-5, far below bf16's 3.9e-3), 2^n added to the
+// exponent field.  y is clamped at -126 (masked scores give ~1e-38, negligible).
+__device__ __forceinline__ void exp2_poly2(float ya, float yb, float &ra, float &rb) {
+  const uint64_t y = f2pk(fmaxf(ya, -126.f), fmaxf(yb, -126.f));
+  const uint64_t t = fadd2(y, f2pk(12582912.f, 12582912.f));   // 1.5 * 2^23: round to integer
+  const uint64_t n = fadd2(t, f2pk(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(n, f2pk(-1.f, -1.f), y);               // y - n, exact
+  uint64_t q = ffma2(f, f2pk(0.05508868380750935f, 0.05508868380750935f),
+                     f2pk(0.2426040514594784f, 0.2426040514594784f));
+  q = ffma2(q, f, f2pk(0.6932762416819616f, 0.6932762416819616f));
+  q = ffma2(q, f, f2pk(0.9999289403695111f, 0.9999289403695111f));
+  float qa, qb, ta, tb;
+  f2upk(q, qa, qb);
+  f2upk(t, ta, tb);
+  ra = __int_as_float(__float_as_int(qa) + (__float_as_int(ta) << 23));
+  rb = __int_as_float(__float_as_int(qb) + (__float_as_int(tb) << 23));
+}
+
+__device__ __forceinline__ void tmem_ld32_f(uint32_t taddr, float *x) {
+  tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(x));
+}
+
+// ------------------------------------------------------------------------------------------
+// MMA issuer (warp 9).  Per kv step: [PV0(prev)] [S0(t)] [PV1(prev)] [S1(t)].
+// ------------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_t tmem, uint32_t q_smem,
+                                         uint32_t k_smem, uint32_t v_smem, int total) {
+  using C = PCfg<D>;
+  constexpr uint32_t idesc_s = idesc_bf16_f32(kM, kN, false);
+  constexpr uint32_t idesc_o = idesc_bf16_f32(kM, D, true);
+  const uint64_t qdesc0 = smem_desc_sw128(q_smem, 16, 1024);
+  const uint64_t kdesc0 = smem_desc_sw128(k_smem, 16, 1024);
+  const uint64_t vdesc0 = smem_desc_sw128(v_smem, C::kSlabBytes, 1024);
+  int T = 0;
+  int pc[2] = {0, 0};  // P handshakes consumed per tile
+  int qc[2] = {0, 0};  // items started per tile
+  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+    const PItem it = get_pitem(p, idx);
+    const bool has1 = it.bt.has1;
+    mbar_wait_warp(smem_u32(&bars.q_full[0]), qc[0] & 1);
+    if (has1) mbar_wait_warp(smem_u32(&bars.q_full[1]), qc[1] & 1);
+    bool first[2] = {true, true};
+    bool pend[2] = {false, false};
+    int pT = -1;
+    auto issue_pv = [&](int j, int Tp) {
+      const int vs = Tp % C::kNV;
+      mbar_wait_warp(smem_u32(&bars.v_full[vs]), (Tp / C::kNV) & 1);
+      mbar_wait_warp(smem_u32(&bars.p_full[j]), pc[j] & 1);
+      ++pc[j];
+      const bool fst = first[j];
+      if (fst && qc[j] > 0) mbar_wait_warp(smem_u32(&bars.o_empty[j]), (qc[j] - 1) & 1);
+      first[j] = false;
+      tc_fence_after();
+      const uint64_t vdesc = vdesc0 + (uint64_t)((vs * C::kTileBytes) >> 4);
+      const uint32_t pcol = tmem + (j ? 128u : 0u);
+      const uint32_t ocol = tmem + (j ? C::kColO1 : C::kColO0);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kN / 16; ++kk)
+          mma_ts(ocol, pcol + kk * 8, vdesc + (uint64_t)((kk * 2048) >> 4), idesc_o, (fst && kk == 0) ? 0u : 1u);
+      }
+      __syncwarp();
+    };
+    auto issue_s = [&](int j, int ks) {
+      const uint64_t adesc = qdesc0 + (uint64_t)((j * C::kTileBytes) >> 4);
+      const uint64_t bdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * C::kSlabBytes + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + (j ? 128u : 0u), adesc + off, bdesc + off, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(smem_u32(&bars.s_full[j]));
+      }
+      __syncwarp();
+    };
+    const int ns = it.bt.steps();
+    for (int k = 0; k < ns; ++k) {
+      int t;
+      bool u[2];
+      step_use(it.bt, k, t, u[0], u[1]);
+      if (!u[0] && !u[1]) continue;
+      const int ks = T % C::kNK;
+      mbar_wait_warp(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (pend[j]) issue_pv(j, pT);
+        if (u[j]) issue_s(j, ks);
+      }
+      if (elect_one()) {
+        if (pT >= 0) mma_commit(smem_u32(&bars.v_empty[pT % C::kNV]));
+        mma_commit(smem_u32(&bars.k_empty[ks]));
+      }
+      __syncwarp();
+      pend[0] = u[0];
+      pend[1] = u[1];
+      pT = T;
+      ++T;
+    }
+    if (elect_one()) {
+      mma_commit(smem_u32(&bars.q_empty[0]));
+      if (has1) mma_commit(smem_u32(&bars.q_empty[1]));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (pend[j]) issue_pv(j, pT);
+    if (elect_one()) {
+      mma_commit(smem_u32(&bars.v_empty[pT % C::kNV]));
+      mma_commit(smem_u32(&bars.o_full[0]));
+      if (has1) mma_commit(smem_u32(&bars.o_full[1]));
+    }
+    __syncwarp();
+    ++qc[0];
+    if (has1) ++qc[1];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// softmax of q tile j (warps 4j .. 4j+3): thread owns one row, all 128 columns of S_j.
+// ------------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uint32_t tmem, int total, int j,
+                                             int warp, int lane) {
+  using C = PCfg<D>;
+  const int row = (warp & 3) * 32 + lane;
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t scol = tmem + lane_off + (j ? 128u : 0u);
+  const uint32_t ocol = tmem + lane_off + (j ? C::kColO1 : C::kColO0);
+  const uint64_t sl2 = f2pk(p.scale_log2, p.scale_log2);
+  int sc = 0;  // S handshakes of this tile
+  int ic = 0;  // items of this tile
+  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+    const PItem it = get_pitem(p, idx);
+    if (j == 1 && !it.bt.has1) continue;
+    const int64_t ti0 = it.i0 + j * kM;                     // first row of this q tile
+    const int64_t ti1 = (ti0 + kM < p.N ? ti0 + kM : p.N) - 1;  // last real row
+    const int64_t i = ti0 + row;
+    float m_used = -INFINITY, l = 0.f;
+    const TileRanges rj = j ? it.bt.r[1] : it.bt.r[0];  // (no dynamic indexing: keeps it in registers)
+    const int ns = it.bt.steps();
+    for (int k = 0; k < ns; ++k) {
+      const int t = it.bt.at(k);
+      if (!tile_in(rj, t)) continue;
+      const int64_t j0 = (int64_t)t * kN;
+      const bool full = kv_tile_full(ti0, ti1, t, it.W, p.n_sink);
+      mbar_wait_warp(smem_u32(&bars.s_full[j]), sc & 1);
+      ++sc;
+      tc_fence_after();
+      float x[kN];
+#pragma unroll
+      for (int c = 0; c < kN / 32; ++c) tmem_ld32_f(scol + c * 32, &x[c * 32]);
+      tmem_wait_ld();
+      if (!full) {
+        // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  c > i-j0-W)
+        const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0), lo = dd - it.W;
+#pragma unroll
+        for (int c = 0; c < kN; ++c) {
+          const bool vis = c <= dd && (c < sk || c > lo);
+          if (!vis) x[c] = -INFINITY;
+        }
+      }
+      float mx[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) mx[a] = fmaxf(x[a], x[a + 8]);
+#pragma unroll
+      for (int c = 16; c < kN; c += 16)
+#pragma unroll
+        for (int a = 0; a < 8; a += 2) {
+          mx[a] = fmax3(mx[a], x[c + a], x[c + a + 8]);
+          mx[a + 1] = fmax3(mx[a + 1], x[c + a + 1], x[c + a + 9]);
+        }
+      const float rmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
+      const float mt = rmax * p.scale_log2;
+      bool rescale = false;
+      float alpha = 1.f;
+      if (m_used == -INFINITY) {
+        m_used = mt;  // first visible scores of this row: O and l are still exactly 0
+      } else if (mt > m_used + kRescaleThreshold) {
+        rescale = true;
+        alpha = fast_exp2(m_used - mt);
+        m_used = mt;
+      }
+      if (__any_sync(0xffffffffu, rescale)) {
+        // PV_j(prev) is complete (S_j(t) completed after it); scale this row of O_j
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float r[32];
+          tmem_ld32_f(ocol + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] *= alpha;
+          tmem_st32(ocol + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r));
+        }
+      }
+      l *= alpha;
+      const float nm = m_used == -INFINITY ? 0.f : -m_used;
+      const uint64_t nm2 = f2pk(nm, nm);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int c = ch * 32 + e;  // pair index: columns 2c, 2c+1
+          const uint64_t y = ffma2(f2pk(x[2 * c], x[2 * c + 1]), sl2, nm2);
+          float ya, yb, ea, eb;
+          f2upk(y, ya, yb);
+          if (c % kPolyEvery == kPolyEvery - 1) {
+            exp2_poly2(ya, yb, ea, eb);
+          } else {
+            ea = fast_exp2(ya);
+            eb = fast_exp2(yb);
+          }
+          acc[e & 3] = fadd2(acc[e & 3], f2pk(ea, eb));
+          pk[e] = pack_bf16x2(ea, eb);
+        }
+        tmem_st32(scol + ch * 32, pk);
+      }
+      float s0, s1;
+      f2upk(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), s0, s1);
+      l += s0 + s1;
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars.p_full[j]));
+    }
+    // epilogue: O_j / l -> bf16 rows, lse
+    mbar_wait_warp(smem_u32(&bars.o_full[j]), ic & 1);
+    ++ic;
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16 *orow =
+        static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride + (int64_t)it.h * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      float r[32];
+      tmem_ld32_f(ocol + c * 32, r);
+      tmem_wait_ld();
+      if (i <= ti1) {
+        uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
+#pragma unroll
+        for (int v4 = 0; v4 < 4; ++v4) {
+          uint4 w;
+          w.x = pack_bf16x2(r[8 * v4 + 0] * inv, r[8 * v4 + 1] * inv);
+          w.y = pack_bf16x2(r[8 * v4 + 2] * inv, r[8 * v4 + 3] * inv);
+          w.z = pack_bf16x2(r[8 * v4 + 4] * inv, r[8 * v4 + 5] * inv);
+          w.w = pack_bf16x2(r[8 * v4 + 6] * inv, r[8 * v4 + 7] * inv);
+          dst[v4] = w;
+        }
+      }
+    }
+    if (p.lse && i <= ti1)
+      p.lse[((int64_t)it.b * p.nql + it.h) * p.N + i] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&bars.o_empty[j]));
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_v, const PpParams p) {
+  using C = PCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ PBars bars;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t q_smem = smem_base;                        // Q0, Q1
+  const uint32_t k_smem = q_smem + 2 * C::kTileBytes;       // kNK tiles
+  const uint32_t v_smem = k_smem + C::kNK * C::kTileBytes;  // kNV tiles
+  const int total = p.n_items * p.batch;
+
+  if (tid == 0) {
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(smem_u32(&bars.q_full[j]), 1);
+      mbar_init(smem_u32(&bars.q_empty[j]), 1);
+      mbar_init(smem_u32(&bars.s_full[j]), 1);
+      mbar_init(smem_u32(&bars.p_full[j]), kSoftmaxWarpsPerTile);
+      mbar_init(smem_u32(&bars.o_full[j]), 1);
+      mbar_init(smem_u32(&bars.o_empty[j]), kSoftmaxWarpsPerTile);
+    }
+    for (int s = 0; s < C::kNK; ++s) {
+      mbar_init(smem_u32(&bars.k_full[s]), 1);
+      mbar_init(smem_u32(&bars.k_empty[s]), 1);
+    }
+    for (int s = 0; s < C::kNV; ++s) {
+      mbar_init(smem_u32(&bars.v_full[s]), 1);
+      mbar_init(smem_u32(&bars.v_empty[s]), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == kWarpMMA) tmem_alloc<kTmemCols>(smem_u32(&bars.tmem_base));
+  if (warp == kWarpKV && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+
+  if (warp < 8) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    softmax_role<D>(p, bars, tmem, total, warp >> 2, warp, lane);
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+  if (warp == kWarpKV) {
+    if (lane == 0) {
+      int T = 0;
+      for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+        const PItem it = get_pitem(p, idx);
+        const int g = it.h / p.G;
+        const int ns = it.bt.steps();
+        for (int k = 0; k < ns; ++k) {
+          int t;
+          bool u0, u1;
+          step_use(it.bt, k, t, u0, u1);
+          if (!u0 && !u1) continue;
+          const int j0 = t * kN;
+          const int ks = T % C::kNK;
+          if (T >= C::kNK) mbar_wait(smem_u32(&bars.k_empty[ks]), ((T - C::kNK) / C::kNK) & 1);
+          const uint32_t kbar = smem_u32(&bars.k_full[ks]);
+          mbar_expect_tx(kbar, C::kTileBytes);
+          for (int sl = 0; sl < C::kSlabs; ++sl)
+            tma_load_4d(k_smem + ks * C::kTileBytes + sl * C::kSlabBytes, &tm_k, kbar, sl * 64, g, j0, it.b);
+          const int vs = T % C::kNV;
+          if (T >= C::kNV) mbar_wait(smem_u32(&bars.v_empty[vs]), ((T - C::kNV) / C::kNV) & 1);
+          const uint32_t vbar = smem_u32(&bars.v_full[vs]);
+          mbar_expect_tx(vbar, C::kTileBytes);
+          for (int sl = 0; sl < C::kSlabs; ++sl)
+            tma_load_4d(v_smem + vs * C::kTileBytes + sl * C::kSlabBytes, &tm_v, vbar, sl * 64, g, j0, it.b);
+          ++T;
+        }
+      }
+    }
+  } else if (warp == kWarpQ) {
+    if (lane == 0) {
+      int qc[2] = {0, 0};
+      for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+        const PItem it = get_pitem(p, idx);
+        for (int j = 0; j < 2; ++j) {
+          if (j == 1 && !it.bt.has1) continue;
+          if (qc[j] > 0) mbar_wait(smem_u32(&bars.q_empty[j]), (qc[j] - 1) & 1);
+          ++qc[j];
+          const uint32_t qbar = smem_u32(&bars.q_full[j]);
+          mbar_expect_tx(qbar, C::kTileBytes);
+          for (int sl = 0; sl < C::kSlabs; ++sl)
+            tma_load_4d(q_smem + j * C::kTileBytes + sl * C::kSlabBytes, &tm_q, qbar, sl * 64, it.h,
+                        (int)(it.i0 + j * kM), it.b);
+        }
+      }
+    }
+  } else if (warp == kWarpMMA) {
+    mma_role<D>(p, bars, tmem, q_smem, k_smem, v_smem, total);
+  }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpMMA) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+int num_sms_pp() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int D>
+int launch_pp(const PrefillArgs &a, void *stream) {
+  using C = PCfg<D>;
+  alignas(64) CUtensorMap mq, mk, mv;
+  const int ngl = a.nql / a.G;
+  if (!make_tile_map(&mq, a.q, D, a.nql, a.N, a.batch, a.q_row_stride, kM) ||
+      !make_tile_map(&mk, a.k, D, ngl, a.N, a.batch, a.kv_row_stride, kN) ||
+      !make_tile_map(&mv, a.v, D, ngl, a.N, a.batch, a.kv_row_stride, kN))
+    return (int)cudaErrorInvalidValue;
+  PpParams p;
+  p.o = a.o;
+  p.lse = a.lse;
+  p.o_row_stride = a.o_row_stride;
+  p.N = a.N;
+  p.batch = a.batch;
+  p.n_items = a.n_items2;
+  p.nql = a.nql;
+  p.G = a.G;
+  p.n_sink = a.n_sink;
+  p.scale_log2 = a.scale * kLog2e;
+  p.win_q = a.d_win_q;
+  p.items = a.d_items2;
+  cudaError_t e =
+      cudaFuncSetAttribute(prefill_pp_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  if (e != cudaSuccess) return (int)e;
+  const int total = p.n_items * p.batch;
+  const int grid = total < num_sms_pp() ? total : num_sms_pp();
+  prefill_pp_kernel<D><<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, p);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_prefill_bf16_pp(const PrefillArgs &a, void *stream) {
+  if (a.d == 128) return launch_pp<128>(a, stream);
+  return launch_pp<64>(a, stream);
+}
+
+}  // namespace moa

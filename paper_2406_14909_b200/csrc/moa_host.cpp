@@ -81,7 +81,7 @@ void free_tables(LayerPlan &p) {
   p.d_tables = nullptr;
   p.d_win_q = p.d_win_g = nullptr;
   p.d_g_off = nullptr;
-  p.d_items = p.d_chunks = p.d_g_chunk = nullptr;
+  p.d_items = p.d_items2 = p.d_chunks = p.d_g_chunk = nullptr;
   p.d_counters = nullptr;
 }
 
@@ -93,7 +93,8 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   size_t o_wing = align16(o_winq + p.win_q.size() * 4);
   size_t o_goff = align16(o_wing + p.win_g.size() * 4);
   size_t o_items = align16(o_goff + p.g_off.size() * 8);
-  size_t o_chunks = align16(o_items + p.items.size() * 4);
+  size_t o_items2 = align16(o_items + p.items.size() * 4);
+  size_t o_chunks = align16(o_items2 + p.items2.size() * 4);
   size_t o_gch = align16(o_chunks + p.chunks.size() * 4);
   size_t o_cnt = align16(o_gch + p.g_chunk.size() * 4);
   size_t total = align16(o_cnt + (size_t)ctx->max_batch * ctx->ngl * 4);
@@ -102,6 +103,7 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   std::memcpy(host.data() + o_wing, p.win_g.data(), p.win_g.size() * 4);
   std::memcpy(host.data() + o_goff, p.g_off.data(), p.g_off.size() * 8);
   std::memcpy(host.data() + o_items, p.items.data(), p.items.size() * 4);
+  std::memcpy(host.data() + o_items2, p.items2.data(), p.items2.size() * 4);
   std::memcpy(host.data() + o_chunks, p.chunks.data(), p.chunks.size() * 4);
   std::memcpy(host.data() + o_gch, p.g_chunk.data(), p.g_chunk.size() * 4);
   DeviceGuard dg(ctx->device);
@@ -120,6 +122,7 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   p.d_win_g = reinterpret_cast<const int32_t *>(b + o_wing);
   p.d_g_off = reinterpret_cast<const int64_t *>(b + o_goff);
   p.d_items = reinterpret_cast<const int32_t *>(b + o_items);
+  p.d_items2 = reinterpret_cast<const int32_t *>(b + o_items2);
   p.d_chunks = reinterpret_cast<const int32_t *>(b + o_chunks);
   p.d_g_chunk = reinterpret_cast<const int32_t *>(b + o_gch);
   p.d_counters = reinterpret_cast<int *>(b + o_cnt);
@@ -277,6 +280,32 @@ moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_he
   for (size_t i = 0; i < its.size(); ++i) {
     np.items[2 * i] = its[i].h;
     np.items[2 * i + 1] = its[i].qt;
+  }
+
+  // two-tile work items (h_local, q_block of 2*kTile rows), same ordering rule; cost = the
+  // MMA tiles of both q tiles
+  const int nqb = (int)((N + 2 * moa::kTile - 1) / (2 * moa::kTile));
+  its.clear();
+  for (int h = 0; h < ctx->nql; ++h) {
+    const size_t first = its.size();
+    int64_t hc = 0;
+    for (int qb = 0; qb < nqb; ++qb) {
+      const moa::BlockTiles bt = moa::kv_block_tiles((int64_t)qb * 2 * moa::kTile, N, np.win_q[h], n_sink);
+      const int c = bt.r[0].count() + (bt.has1 ? bt.r[1].count() : 0);
+      hc += c;
+      its.push_back({h, qb, c, 0});
+    }
+    for (size_t k = first; k < its.size(); ++k) its[k].hcost = hc;
+  }
+  std::stable_sort(its.begin(), its.end(), [](const It &a, const It &b) {
+    if (a.hcost != b.hcost) return a.hcost > b.hcost;
+    if (a.h != b.h) return a.h < b.h;
+    return a.cnt > b.cnt;
+  });
+  np.items2.resize(its.size() * 2);
+  for (size_t i = 0; i < its.size(); ++i) {
+    np.items2[2 * i] = its[i].h;
+    np.items2[2 * i + 1] = its[i].qt;
   }
 
   // decode work list: split every group region into chunks of ~chunk_rows rows
@@ -471,7 +500,11 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   a.batch = batch; a.N = N; a.scale = scale; a.lse = lse_out; a.n_sink = p.n_sink;
   a.nql = ctx->nql; a.G = ctx->G; a.d = ctx->d;
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
-  int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_tc(a, stream);
+  a.d_items2 = p.d_items2; a.n_items2 = (int)(p.items2.size() / 2);
+  static const bool use_tc = [] { const char *e = std::getenv("MOA_PREFILL_KERNEL"); return e && std::string(e) == "tc"; }();
+  int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream)
+          : use_tc               ? moa::launch_prefill_bf16_tc(a, stream)
+                                 : moa::launch_prefill_bf16_pp(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
   if (!fill) {
     ctx->last_cache_write = -1;

@@ -66,6 +66,41 @@ MOA_HD bool kv_tile_full(int64_t i0, int64_t i1, int t, int W, int s) {
   return jn > j1 || (i1 - jn < W);
 }
 
+MOA_HD bool tile_in(const TileRanges &r, int t) { return (t >= r.a0 && t < r.a1) || (t >= r.b0 && t < r.b1); }
+
+// Two q tiles processed together (rows [i0, i0+128) and [i0+128, i0+256), the second
+// present iff i0+128 < N): their visited kv tiles are walked once in ascending order,
+// [0, u_a1) U [u_b0, u_b1), and each step is used by the q tiles whose own schedule
+// contains it (tile_in).  A step neither tile uses is skipped by every role.
+struct BlockTiles {
+  TileRanges r[2];
+  bool has1;
+  int u_a1, u_b0, u_b1;
+  MOA_HD int steps() const { return u_a1 + (u_b1 - u_b0); }
+  MOA_HD int at(int k) const { return k < u_a1 ? k : u_b0 + (k - u_a1); }
+};
+
+MOA_HD BlockTiles kv_block_tiles(int64_t i0, int64_t N, int W, int s) {
+  BlockTiles b;
+  b.r[0] = kv_tile_ranges(i0, (i0 + kTile < N ? i0 + kTile : N) - 1, W, s);
+  b.has1 = i0 + kTile < N;
+  if (b.has1) {
+    b.r[1] = kv_tile_ranges(i0 + kTile, (i0 + 2 * kTile < N ? i0 + 2 * kTile : N) - 1, W, s);
+  } else {
+    b.r[1].a0 = b.r[1].a1 = b.r[1].b0 = b.r[1].b1 = 0;
+  }
+  b.u_a1 = b.r[0].a1 > b.r[1].a1 ? b.r[0].a1 : b.r[1].a1;
+  int lo = 1 << 30, hi = 0;
+  for (int k = 0; k < 2; ++k)
+    if (b.r[k].b1 > b.r[k].b0) {
+      lo = b.r[k].b0 < lo ? b.r[k].b0 : lo;
+      hi = b.r[k].b1 > hi ? b.r[k].b1 : hi;
+    }
+  b.u_b0 = lo > b.u_a1 ? lo : b.u_a1;
+  b.u_b1 = hi > b.u_b0 ? hi : b.u_b0;
+  return b;
+}
+
 // Ring arithmetic (reading c13).
 MOA_HD int64_t slot_of(int64_t p, int s, int Wg) {
   if (p < s) return p;
@@ -99,6 +134,7 @@ struct LayerPlan {
   int64_t rows_per_seq = 0;      // sum_g (s + W_g)
   std::vector<int32_t> items;    // prefill work items (h_local, q_tile): heads heaviest first, q tiles of a
                                  // head consecutive (L2 sharing of its K/V), heaviest first
+  std::vector<int32_t> items2;   // prefill work items of two q tiles (h_local, q_block of 2*kTile rows), same order
   std::vector<int32_t> chunks;   // decode chunks: (g_local, row_begin, row_end) triples
   std::vector<int32_t> g_chunk;  // first chunk of each group, size ngl + 1
   int chunk_rows = 0;
@@ -109,6 +145,7 @@ struct LayerPlan {
   const int32_t *d_win_g = nullptr;
   const int64_t *d_g_off = nullptr;
   const int32_t *d_items = nullptr;
+  const int32_t *d_items2 = nullptr;
   const int32_t *d_chunks = nullptr;
   const int32_t *d_g_chunk = nullptr;
   int *d_counters = nullptr;     // [max_batch, ngl] decode combine tickets (zeroed at upload)
@@ -156,9 +193,12 @@ struct PrefillArgs {
   const int32_t *d_win_q;
   const int32_t *d_items;
   int n_items;
+  const int32_t *d_items2;  // (h_local, q_block) pairs of the two-tile kernel
+  int n_items2;
 };
 int launch_prefill_f32(const PrefillArgs &a, void *stream);
 int launch_prefill_bf16_tc(const PrefillArgs &a, void *stream);
+int launch_prefill_bf16_pp(const PrefillArgs &a, void *stream);
 
 struct CacheArgs {
   const void *k, *v;  // prompt K/V (fill) or new token (append)
