@@ -170,6 +170,8 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
   const uint64_t kdesc0 = smem_desc_sw128(k_smem, 16, 1024);
   const uint64_t vdesc0 = smem_desc_sw128(v_smem, C::kSlabBytes, 1024);
   int T = 0;
+  int ks = 0, vs = 0, pvs = 0;  // K / V ring stage of the current step, V stage of the previous
+  uint32_t kph = 0, vph = 0, pvph = 0;
   int pc[2] = {0, 0};  // P handshakes consumed per tile
   int qc[2] = {0, 0};  // items started per tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
@@ -179,10 +181,14 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
     if (has1) mbar_wait_warp(smem_u32(&bars.q_full[1]), qc[1] & 1);
     bool first[2] = {true, true};
     bool pend[2] = {false, false};
-    int pT = -1;
-    auto issue_pv = [&](int j, int Tp) {
-      const int vs = Tp % C::kNV;
-      mbar_wait_warp(smem_u32(&bars.v_full[vs]), (Tp / C::kNV) & 1);
+    int pT = -1, pt = -1;
+    int last_t[2];  // last kv tile of each q tile: its S releases Q_j, its PV completes O_j
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const TileRanges r = j ? it.bt.r[1] : it.bt.r[0];
+      last_t[j] = r.b1 > r.b0 ? r.b1 - 1 : r.a1 - 1;
+    }
+    auto issue_pv = [&](int j, int vs) {  // V(prev) already waited for (v_full[vs])
       mbar_wait_warp(smem_u32(&bars.p_full[j]), pc[j] & 1);
       ++pc[j];
       const bool fst = first[j];
@@ -196,10 +202,11 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
 #pragma unroll
         for (int kk = 0; kk < kN / 16; ++kk)
           mma_ts(ocol, pcol + kk * 8, vdesc + (uint64_t)((kk * 2048) >> 4), idesc_o, (fst && kk == 0) ? 0u : 1u);
+        if (pt == last_t[j]) mma_commit(smem_u32(&bars.o_full[j]));  // tile j's epilogue may start
       }
       __syncwarp();
     };
-    auto issue_s = [&](int j, int ks) {
+    auto issue_s = [&](int j, int ks, int t) {
       const uint64_t adesc = qdesc0 + (uint64_t)((j * C::kTileBytes) >> 4);
       const uint64_t bdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
       if (elect_one()) {
@@ -209,6 +216,7 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
           mma_ss(tmem + (j ? 128u : 0u), adesc + off, bdesc + off, idesc_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(smem_u32(&bars.s_full[j]));
+        if (t == last_t[j]) mma_commit(smem_u32(&bars.q_empty[j]));  // Q_j(next item) may load
       }
       __syncwarp();
     };
@@ -218,37 +226,34 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
       bool u[2];
       step_use(it.bt, k, t, u[0], u[1]);
       if (!u[0] && !u[1]) continue;
-      const int ks = T % C::kNK;
-      mbar_wait_warp(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
+      mbar_wait_warp(smem_u32(&bars.k_full[ks]), kph);
+      if (pT >= 0) mbar_wait_warp(smem_u32(&bars.v_full[pvs]), pvph);  // V(prev): both PVs below
       tc_fence_after();
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        if (pend[j]) issue_pv(j, pT);
-        if (u[j]) issue_s(j, ks);
+        if (pend[j]) issue_pv(j, pvs);
+        if (u[j]) issue_s(j, ks, t);
       }
       if (elect_one()) {
-        if (pT >= 0) mma_commit(smem_u32(&bars.v_empty[pT % C::kNV]));
+        if (pT >= 0) mma_commit(smem_u32(&bars.v_empty[pvs]));
         mma_commit(smem_u32(&bars.k_empty[ks]));
       }
       __syncwarp();
       pend[0] = u[0];
       pend[1] = u[1];
       pT = T;
+      pt = t;
+      pvs = vs;
+      pvph = vph;
+      if (++ks == C::kNK) ks = 0, kph ^= 1u;
+      if (++vs == C::kNV) vs = 0, vph ^= 1u;
       ++T;
     }
-    if (elect_one()) {
-      mma_commit(smem_u32(&bars.q_empty[0]));
-      if (has1) mma_commit(smem_u32(&bars.q_empty[1]));
-    }
-    __syncwarp();
+    mbar_wait_warp(smem_u32(&bars.v_full[pvs]), pvph);
 #pragma unroll
     for (int j = 0; j < 2; ++j)
-      if (pend[j]) issue_pv(j, pT);
-    if (elect_one()) {
-      mma_commit(smem_u32(&bars.v_empty[pT % C::kNV]));
-      mma_commit(smem_u32(&bars.o_full[0]));
-      if (has1) mma_commit(smem_u32(&bars.o_full[1]));
-    }
+      if (pend[j]) issue_pv(j, pvs);
+    if (elect_one()) mma_commit(smem_u32(&bars.v_empty[pvs]));
     __syncwarp();
     ++qc[0];
     if (has1) ++qc[1];
@@ -489,6 +494,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int sl = 0; sl < C::kSlabs; ++sl)
             tma_load_4d(q_smem + j * C::kTileBytes + sl * C::kSlabBytes, &tm_q, qbar, sl * 64, it.h,
                         (int)(it.i0 + j * kM), it.b);
+        }
+        // warm L2 with the next item's Q tiles (their loads wait for this item's last S MMAs)
+        if (idx + (int)gridDim.x < total) {
+          const PItem nx = get_pitem(p, idx + gridDim.x);
+          for (int j = 0; j < (nx.bt.has1 ? 2 : 1); ++j)
+            for (int sl = 0; sl < C::kSlabs; ++sl)
+              tma_prefetch_4d(&tm_q, sl * 64, nx.h, (int)(nx.i0 + j * kM), nx.b);
         }
       }
     }

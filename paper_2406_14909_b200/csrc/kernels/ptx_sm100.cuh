@@ -54,6 +54,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// single probe of a phase (non-blocking)
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// wait with a back-off between probes: for threads off the critical path (TMA producers), so
+// their polling does not compete with latency-critical waiters for the barrier unit
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns = 64) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
+
 // wait by every lane of a warp, then reconverge (before .sync.aligned / bar.sync / elect.sync)
 __device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
   mbar_wait(bar, parity);
@@ -71,6 +89,14 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *m, 
       "[%6];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
+}
+
+// L2 prefetch of one box (no shared-memory destination, no completion)
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap *m, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
 }
 
 // ---------------------------------------------------------------- tcgen05

@@ -8,7 +8,7 @@ set -u
 R=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
-K='regex:prefill_tc_kernel|prefill_f32_kernel|decode_mma_kernel|decode_kernel|cache_fill_kernel|kv_append_kernel'
+K='regex:prefill_pp_kernel|prefill_tc_kernel|prefill_f32_kernel|decode_mma_kernel|decode_kernel|cache_fill_kernel|kv_append_kernel'
 L=32; T=512
 # warm-up launches of bench.py (--warmup 3): 3 steps x (L prefill + L cache fill + T*L decode)
 SKIP=$((3 * (2 * L + T * L)))
@@ -23,7 +23,7 @@ echo "launch list rc=$?"
 timeout -k 10 600 ncu --set full --clock-control none --import-source on -k regex:decode_mma -s 8 -c 1 \
   -o $OUT/${R}_decode_full python tools/prof_run.py decode --layers 4 --tokens 3 > $OUT/${R}_decode_full.log 2>&1
 echo "decode full rc=$?"
-timeout -k 10 600 ncu --set full --clock-control none --import-source on -k regex:prefill_tc -s 1 -c 1 \
+timeout -k 10 600 ncu --set full --clock-control none --import-source on -k regex:prefill_pp -s 1 -c 1 \
   -o $OUT/${R}_prefill_full python tools/prof_run.py prefill --layers 2 > $OUT/${R}_prefill_full.log 2>&1
 echo "prefill full rc=$?"
 ls -la $OUT | grep "$R"

@@ -1,0 +1,58 @@
+"""Event timeline of CTA 0 of the two-tile prefill kernel (diagnostic build -DMOA_PP_DIAG_TRACE).
+
+    python tools/build_variant.py trace -DMOA_PP_DIAG_TRACE
+    MOA_LIB=tools/bin/libmoa_trace.so python tools/trace_pp.py [C2] [n_events]
+"""
+import ctypes
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2406_14909_b200 as moa  # noqa: E402
+from paper_2406_14909_b200 import _lib  # noqa: E402
+from moa_workloads import CONFIGS, prefill_qkv, rule_table  # noqa: E402
+
+TAGS = {1: "mma k_full ok", 2: "mma v_full ok", 3: "mma before v/k_empty commits", 4: "mma after commits",
+        5: "mma before k_full wait", 10: "mma p_full0 ok", 11: "mma p_full1 ok", 20: "mma PV0 issued", 21: "mma PV1 issued",
+        30: "mma S0 issued", 31: "mma S1 issued", 40: "sm s_full seen", 41: "sm p_full arrive"}
+
+
+def main(name="C2", nev=120):
+    cfg = CONFIGS[name]
+    t = rule_table(name)
+    dev = torch.device("cuda")
+    ctx = moa.MoAContext(1, cfg.hq, cfg.hkv, cfg.head_dim, cfg.batch)
+    ctx.set_spans(0, moa.resolve_spans(t["alpha"][8], t["beta"][8], cfg.N, cfg.n_sink), cfg.n_sink, cfg.N)
+    ctx.alloc_cache(cfg.batch)
+    q, k, v = prefill_qkv(cfg, 8, device=dev)
+    o = torch.empty_like(q)
+    sc = 1 / math.sqrt(cfg.head_dim)
+    fn = _lib.lib().moa_debug_pp_trace
+    fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.POINTER(ctypes.c_int)]
+    buf = (ctypes.c_ulonglong * (4 * 4096))()
+    cnt = (ctypes.c_int * 4)()
+    ctx.prefill(0, q, k, v, o, sc)
+    fn(buf, cnt)
+    ctx.prefill(0, q, k, v, o, sc)
+    fn(buf, cnt)
+    ev = []
+    for r in range(4):
+        for i in range(cnt[r]):
+            x = buf[r * 4096 + i]
+            ev.append((x & ((1 << 56) - 1), r, x >> 56))
+    ev.sort()
+    t0 = ev[0][0]
+    start = len(ev) // 3
+    prev = ev[start][0]
+    for c, r, tag in ev[start:start + nev]:
+        who = ["MMA0", "SM0 ", "SM1 ", "MMA1"][r]
+        print(f"{c - t0:10d} (+{c - prev:5d})  {who} {TAGS.get(tag, tag)}")
+        prev = c
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "C2", int(sys.argv[2]) if len(sys.argv) > 2 else 120)
