@@ -38,9 +38,6 @@
 #include "ptx_sm100.cuh"
 
 namespace moa {
-
-bool make_tile_map(void *m, const void *ptr, int D, int H, int64_t N, int B, int64_t row_stride, int box_rows);
-
 namespace {
 
 using namespace ptx;
@@ -59,8 +56,11 @@ struct PCfg {
   static constexpr int kSlabs = D / 64;
   static constexpr int kTileBytes = kM * D * 2;
   static constexpr int kSlabBytes = kM * 128;
-  static constexpr int kNK = D == 128 ? 3 : 6;
-  static constexpr int kNV = D == 128 ? 2 : 4;
+#ifndef MOA_PP_NK128
+#define MOA_PP_NK128 3
+#endif
+  static constexpr int kNK = D == 128 ? MOA_PP_NK128 : 6;
+  static constexpr int kNV = D == 128 ? 5 - MOA_PP_NK128 : 4;
   static constexpr int kSmemBytes = (2 + kNK + kNV) * kTileBytes + 1024;
   static constexpr uint32_t kColO0 = 256, kColO1 = 256 + D;
 };

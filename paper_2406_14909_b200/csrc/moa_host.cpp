@@ -501,10 +501,7 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   a.nql = ctx->nql; a.G = ctx->G; a.d = ctx->d;
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
   a.d_items2 = p.d_items2; a.n_items2 = (int)(p.items2.size() / 2);
-  static const bool use_tc = [] { const char *e = std::getenv("MOA_PREFILL_KERNEL"); return e && std::string(e) == "tc"; }();
-  int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream)
-          : use_tc               ? moa::launch_prefill_bf16_tc(a, stream)
-                                 : moa::launch_prefill_bf16_pp(a, stream);
+  int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_pp(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
   if (!fill) {
     ctx->last_cache_write = -1;

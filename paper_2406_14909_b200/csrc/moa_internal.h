@@ -197,7 +197,6 @@ struct PrefillArgs {
   int n_items2;
 };
 int launch_prefill_f32(const PrefillArgs &a, void *stream);
-int launch_prefill_bf16_tc(const PrefillArgs &a, void *stream);
 int launch_prefill_bf16_pp(const PrefillArgs &a, void *stream);
 
 struct CacheArgs {
@@ -264,5 +263,7 @@ size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d);
 
 // TMA tensor map over a [rows, d] bf16 cache (box box_rows x 64 cols, 128B swizzle).
 bool encode_cache_map(void *map_out, const void *ptr, int d, int64_t rows, int box_rows);
+// TMA tensor map over [B, N, H, d] bf16 (token row stride in elements), 64-column x box_rows boxes.
+bool make_tile_map(void *m, const void *ptr, int d, int H, int64_t N, int B, int64_t row_stride, int box_rows);
 
 }  // namespace moa

@@ -8,7 +8,7 @@ set -u
 R=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
-K='regex:prefill_pp_kernel|prefill_tc_kernel|prefill_f32_kernel|decode_mma_kernel|decode_kernel|cache_fill_kernel|kv_append_kernel'
+K='regex:prefill_pp_kernel|prefill_f32_kernel|decode_mma_kernel|decode_kernel|cache_fill_kernel|kv_append_kernel'
 L=32; T=512
 # warm-up launches of bench.py (--warmup 3): 3 steps x (L prefill + L cache fill + T*L decode)
 SKIP=$((3 * (2 * L + T * L)))
