@@ -38,6 +38,16 @@ section "Readings".  The ones this file relies on:
   ``W_g = max_{h in g} W_h`` recent rows; every q-head masks to its own W_h.
 * c13: ring slot of position p: ``p`` if ``p < s`` else
   ``s + (p - s) mod W_g``.
+* c5 / NEXT-1 (block mode): the paper's prefill kernel uses "the block
+  sliding-window attention pattern with a block size of 64 ... The first
+  block of tokens is not masked and serves as the attention sink"
+  (PAPER.md:690).  With block size b (s and W multiples of b),
+  query block ``i // b`` sees key block ``j // b`` iff ``j <= i`` and
+  (``j // b < s // b`` or ``i // b - j // b < W // b``), causal inside the
+  diagonal block (``build_mask``).  ``block = 0`` is the
+  token-granular mask above.  Decode stays token-granular in both modes: the
+  cache "replace[s] the old KV-Cache that exceeds the span with the latest"
+  token by token.
 
 Parity pins for every function are in ``tests/test_oracle_pins.py``; none of
 them is "parity unpinned".
@@ -54,6 +64,7 @@ __all__ = [
     "window_of",
     "group_windows",
     "visible",
+    "visible_block",
     "visible_keys",
     "attend",
     "prefill",
@@ -65,6 +76,7 @@ __all__ = [
     "cache_image",
     "density",
     "visible_pairs",
+    "visible_pairs_block",
 ]
 
 
@@ -113,10 +125,23 @@ def visible(i: int, j: int, W: int, s: int) -> bool:
     return 0 <= j <= i and (j < s or i - j < W)
 
 
-def visible_keys(i: int, W: int, s: int) -> np.ndarray:
+def visible_block(i: int, j: int, W: int, s: int, b: int) -> bool:
+    """Block-granular mask of block size b:
+    key j is visible to query i iff causal and its block is a sink block or
+    within ``W // b`` blocks of the query's block (the query's own block
+    included).  Requires ``s % b == 0`` and ``W % b == 0``."""
+    assert b >= 1 and s % b == 0 and W % b == 0
+    return 0 <= j <= i and (j // b < s // b or i // b - j // b < W // b)
+
+
+def _visible(i: int, j: int, W: int, s: int, block: int) -> bool:
+    return visible(i, j, W, s) if block == 0 else visible_block(i, j, W, s, block)
+
+
+def visible_keys(i: int, W: int, s: int, block: int = 0) -> np.ndarray:
     """Sorted list of visible key positions of query i (brute-force
-    enumeration of the predicate, O(i))."""
-    return np.array([j for j in range(i + 1) if visible(i, j, W, s)],
+    enumeration of the predicate, O(i)); ``block`` > 0 selects the block mask."""
+    return np.array([j for j in range(i + 1) if _visible(i, j, W, s, block)],
                     dtype=np.int64)
 
 
@@ -146,24 +171,26 @@ def _check_shapes(Q, K, V, windows_q):
     return B, N, Hq, Hkv, d, Hq // Hkv
 
 
-def prefill_rows(Q, K, V, windows_q, n_sink: int, tau: float, rows):
+def prefill_rows(Q, K, V, windows_q, n_sink: int, tau: float, rows, block: int = 0):
     """Eq. 1 for a list of sampled outputs ``rows = [(b, h, i), ...]``.
 
     Returns (O [len(rows), d], LSE [len(rows)]) in fp64.  Each row gathers
-    its visible set V(h,i) by enumerating the predicate and attends over it.
+    its visible set V(h,i) by enumerating the predicate and attends over it
+    (``block`` > 0: the block mask of block size ``block``).
     """
     B, N, Hq, Hkv, d, G = _check_shapes(Q, K, V, windows_q)
     O = np.zeros((len(rows), d), dtype=np.float64)
     L = np.zeros(len(rows), dtype=np.float64)
     for r, (b, h, i) in enumerate(rows):
         g = h // G
-        J = visible_keys(int(i), int(windows_q[h]), n_sink)
+        J = visible_keys(int(i), int(windows_q[h]), n_sink, block)
         O[r], L[r] = attend(Q[b, i, h], K[b, J, g], V[b, J, g], tau)
     return O, L
 
 
-def prefill(Q, K, V, windows_q, n_sink: int, tau: float):
-    """Causal prefill with the per-head MoA mask (Eq. 1 + PAPER.md:178).
+def prefill(Q, K, V, windows_q, n_sink: int, tau: float, block: int = 0):
+    """Causal prefill with the per-head MoA mask (Eq. 1 + PAPER.md:178;
+    ``block`` > 0: block mask).
 
     Q: [B, N, Hq, d]; K, V: [B, N, Hkv, d] (any float dtype, upcast to fp64).
     windows_q: window W_h of every q-head.  Returns O [B, N, Hq, d] and
@@ -171,13 +198,13 @@ def prefill(Q, K, V, windows_q, n_sink: int, tau: float):
     """
     B, N, Hq, Hkv, d, G = _check_shapes(Q, K, V, windows_q)
     rows = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(N)]
-    o, l = prefill_rows(Q, K, V, windows_q, n_sink, tau, rows)
+    o, l = prefill_rows(Q, K, V, windows_q, n_sink, tau, rows, block)
     O = o.reshape(B, Hq, N, d).transpose(0, 2, 1, 3).copy()
     LSE = l.reshape(B, Hq, N)
     return O, LSE
 
 
-def prefill_dense_mask(Q, K, V, windows_q, n_sink: int, tau: float):
+def prefill_dense_mask(Q, K, V, windows_q, n_sink: int, tau: float, block: int = 0):
     """Second, brute-force formulation of the same prefill: a dense N x N
     additive mask M with a finite -1e30 sentinel for masked cells
     (SPEC.md:69 design decision), A = softmax(S + M) by rows, masked
@@ -192,7 +219,7 @@ def prefill_dense_mask(Q, K, V, windows_q, n_sink: int, tau: float):
             M = np.full((N, N), -1e30)
             for i in range(N):
                 for j in range(N):
-                    if visible(i, j, int(windows_q[h]), n_sink):
+                    if _visible(i, j, int(windows_q[h]), n_sink, block):
                         M[i, j] = 0.0
             S = tau * (Q[b, :, h].astype(np.float64) @ K[b, :, g].astype(np.float64).T)
             X = S + M
@@ -291,6 +318,12 @@ def density(windows, n_sink: int, N: int) -> float:
     min(N, s + W_h) / N (reading c11)."""
     w = np.asarray(windows, dtype=np.int64)
     return float(np.mean(np.minimum(N, n_sink + w)) / N)
+
+
+def visible_pairs_block(N: int, W: int, s: int, b: int) -> int:
+    """Number of (query, key) pairs of one head under the block mask, by
+    enumerating the predicate."""
+    return sum(1 for i in range(N) for j in range(i + 1) if visible_block(i, j, W, s, b))
 
 
 def visible_pairs(N: int, W: int, s: int) -> int:

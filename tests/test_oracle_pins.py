@@ -234,3 +234,88 @@ def test_rule_tables_shape_density(name):
          for l in range(cfg.layers)]
     dens = np.mean([oracle.density(wl, cfg.n_sink, cfg.N) for wl in w])
     assert abs(dens - cfg.target_density) < 0.01
+
+
+# --- block mode ("block sliding-window attention pattern with a block size of
+# 64"; SPEC.md:216-224 build_mask) -------------------------------------------------------
+
+def test_block_mask_hand_written_picture():
+    """SPEC.md:216-224's worked example n=16, block=4, one sink block, window_blocks=2,
+    against a hand-typed picture."""
+    with open(os.path.join(GOLDEN, "block_mask_N16_b4_s4_W8.txt")) as f:
+        pic = [l.strip() for l in f if l.strip() and not l.startswith("#")]
+    assert len(pic) == 16
+    for i in range(16):
+        got = "".join("1" if oracle.visible_block(i, j, 8, 4, 4) else "." for j in range(16))
+        assert got == pic[i], (i, got, pic[i])
+        assert list(oracle.visible_keys(i, 8, 4, block=4)) == [j for j in range(16) if pic[i][j] == "1"]
+
+
+def test_block_one_window_block_sees_sink_and_own_block():
+    """window_blocks = 1, sink_blocks = 1 -> each query block sees block 0 and
+    itself only (causal inside it)."""
+    b = 8
+    for i in range(64):
+        keys = set(oracle.visible_keys(i, b, b, block=b).tolist())
+        own = set(range((i // b) * b, i + 1))
+        assert keys == set(range(min(b, i + 1))) | own
+
+
+@pytest.mark.parametrize("N", [1, 7, 33])
+def test_block_size_one_is_token_mask(N):
+    """b = 1 reduces the block predicate to the token predicate (already pinned above)."""
+    for W in range(0, N + 2):
+        for s in range(0, 4):
+            for i in range(N):
+                for j in range(N):
+                    assert oracle.visible_block(i, j, W, s, 1) == oracle.visible(i, j, W, s)
+
+
+@pytest.mark.parametrize("b", [2, 4, 8])
+def test_block_window_between_token_windows(b):
+    """Containment fixed by the definitions: the block window starts at
+    b*floor(i/b) - W + b, between i-W+1 and i-W+b, so token mask(W-b+1) <= block mask(W)
+    <= token mask(W) (same sinks, s a multiple of b)."""
+    N = 6 * b + 3
+    for s in (0, b):
+        for W in range(b, N + b, b):
+            for i in range(N):
+                blk = set(oracle.visible_keys(i, W, s, block=b).tolist())
+                assert set(oracle.visible_keys(i, W - b + 1, s).tolist()) <= blk
+                assert blk <= set(oracle.visible_keys(i, W, s).tolist())
+
+
+@pytest.mark.parametrize("s", [0, 4])
+def test_block_full_window_is_causal_attention(s):
+    """window_blocks >= n_blocks -> pure causal mask, against
+    torch scaled_dot_product_attention(is_causal=True) in fp64."""
+    B, N, H, d, b = 1, 24, 2, 8, 4
+    Q, K, V = _rand((B, N, H, d), 91), _rand((B, N, H, d), 92), _rand((B, N, H, d), 93)
+    O, _ = oracle.prefill(Q, K, V, [N, N + b], s, 0.3, block=b)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(Q).permute(0, 2, 1, 3), torch.from_numpy(K).permute(0, 2, 1, 3),
+        torch.from_numpy(V).permute(0, 2, 1, 3), is_causal=True, scale=0.3).permute(0, 2, 1, 3).numpy()
+    assert np.max(np.abs(O - ref)) < 1e-12
+
+
+@pytest.mark.parametrize("b", [2, 4])
+def test_block_gather_matches_dense_mask(b):
+    """Gather-set formulation == dense additive-mask formulation (brute force) in block mode,
+    all windows multiple of b up to N, GQA."""
+    B, N, Hq, Hkv, d = 1, 20, 4, 2, 8
+    Q, K, V = _rand((B, N, Hq, d), 94), _rand((B, N, Hkv, d), 95), _rand((B, N, Hkv, d), 96)
+    for s in (0, b):
+        for W in range(0 if s else b, N + b, b):
+            wq = [W, max(b, W - b), W, b]
+            O1, L1 = oracle.prefill(Q, K, V, wq, s, 0.25, block=b)
+            O2, L2 = oracle.prefill_dense_mask(Q, K, V, wq, s, 0.25, block=b)
+            assert np.max(np.abs(O1 - O2)) < 1e-12 and np.max(np.abs(L1 - L2)) < 1e-12
+
+
+def test_block_visible_pairs_brute_force():
+    """visible_pairs_block against the picture's count and the b=1 token closed form."""
+    with open(os.path.join(GOLDEN, "block_mask_N16_b4_s4_W8.txt")) as f:
+        pic = [l.strip() for l in f if l.strip() and not l.startswith("#")]
+    assert oracle.visible_pairs_block(16, 8, 4, 4) == sum(r.count("1") for r in pic)
+    for N, W, s in ((50, 7, 3), (64, 64, 0), (33, 1, 0)):
+        assert oracle.visible_pairs_block(N, W, s, 1) == oracle.visible_pairs(N, W, s)
