@@ -121,6 +121,20 @@ moa_status moa_resolve_spans(const float *alpha, const float *beta, int n_heads,
 moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_head,
                          int n_sink, int64_t N);
 
+/*
+ * moa_set_spans with the paper's block-granular prefill mask:
+ * "block sliding-window attention pattern with a block size of 64 ... The first block
+ * of tokens is not masked and serves as the attention sink".
+ * Query i sees key j <= i iff j / block < n_sink / block or i / block - j / block <
+ * W / block (SPEC.md:216-224 build_mask; causal inside the diagonal block).
+ *   block   0 = token-granular mask (== moa_set_spans); else a power of two in [1, 128]
+ *           dividing n_sink and every window (MOA_ERR_INVALID_ARG otherwise).
+ * Only prefill changes: decode stays token-granular (the cache replaces entries token by
+ * token), with the same windows and the same cache layout.
+ */
+moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_per_q_head,
+                                 int n_sink, int64_t N, int block);
+
 /* Bytes of the K (and of the V) cache of all layers / of one layer for
  * `batch` sequences.  All layers' spans must be set for the first form. */
 moa_status moa_cache_bytes(const moa_ctx *ctx, int batch, size_t *k_bytes, size_t *v_bytes);

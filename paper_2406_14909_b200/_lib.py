@@ -29,6 +29,7 @@ _SIGS = [
     ("moa_destroy", c_int, [_P]),
     ("moa_resolve_spans", c_int, [POINTER(c_float), POINTER(c_float), c_int, c_int64, c_int, POINTER(c_int32)]),
     ("moa_set_spans", c_int, [_P, c_int, POINTER(c_int32), c_int, c_int64]),
+    ("moa_set_spans_blocked", c_int, [_P, c_int, POINTER(c_int32), c_int, c_int64, c_int]),
     ("moa_cache_bytes", c_int, [_P, c_int, POINTER(c_size_t), POINTER(c_size_t)]),
     ("moa_layer_cache_bytes", c_int, [_P, c_int, c_int, POINTER(c_size_t), POINTER(c_size_t)]),
     ("moa_workspace_bytes", c_int, [_P, c_int, POINTER(c_size_t)]),

@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(kRows) prefill_f32_kernel(PrefillArgs a) {
   for (int e = 0; e < D; ++e) acc[e] = 0.f;
   float m = -INFINITY, l = 0.f;
 
-  const TileRanges tr = kv_tile_ranges(i0, i1, W, s);
+  const TileRanges tr = kv_tile_ranges(i0, i1, W, s, a.bshift);
+  const int64_t lo_i = win_lo(i, W, a.bshift);  // first window key of this row (token or block mode)
   const int nt = tr.count();
   for (int t = 0; t < nt; ++t) {
     const int kt = tr.at(t);
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(kRows) prefill_f32_kernel(PrefillArgs a) {
 #pragma unroll
       for (int u = 0; u < kSub; ++u) {
         const int64_t j = j0 + sb + u;
-        const bool vis = j <= i && (j < s || i - j < W);
+        const bool vis = j <= i && (j < s || (W > 0 && j >= lo_i));
         sc[u] = vis ? sc[u] : -INFINITY;
         mx = fmaxf(mx, sc[u]);
       }

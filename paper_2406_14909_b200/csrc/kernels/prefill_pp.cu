@@ -72,6 +72,7 @@ struct PpParams {
   int64_t N;
   int batch, n_items, nql, G, n_sink;
   float scale_log2;
+  int bshift;            // -1 token mask, else log2(block size) (block mode)
   const int32_t *win_q;
   const int32_t *items;  // (q-head, q-block) pairs, LPT order
 };
@@ -98,7 +99,7 @@ __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
   it.h = p.items[2 * wi];
   it.i0 = (int64_t)p.items[2 * wi + 1] * (2 * kM);
   it.W = p.win_q[it.h];
-  it.bt = kv_block_tiles(it.i0, p.N, it.W, p.n_sink);
+  it.bt = kv_block_tiles(it.i0, p.N, it.W, p.n_sink, p.bshift);
   return it;
 }
 
@@ -280,6 +281,9 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
     const int64_t ti0 = it.i0 + j * kM;                     // first row of this q tile
     const int64_t ti1 = (ti0 + kM < p.N ? ti0 + kM : p.N) - 1;  // last real row
     const int64_t i = ti0 + row;
+    // first window key of this row: i-W+1 (token mask) or the block-aligned start (block mode);
+    // W = 0 puts it past the row
+    const int64_t lo_i = it.W > 0 ? win_lo(i, it.W, p.bshift) : i + 1;
     float m_used = -INFINITY, l = 0.f;
     const TileRanges rj = j ? it.bt.r[1] : it.bt.r[0];  // (no dynamic indexing: keeps it in registers)
     const int ns = it.bt.steps();
@@ -287,7 +291,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       const int t = it.bt.at(k);
       if (!tile_in(rj, t)) continue;
       const int64_t j0 = (int64_t)t * kN;
-      const bool full = kv_tile_full(ti0, ti1, t, it.W, p.n_sink);
+      const bool full = kv_tile_full(ti0, ti1, t, it.W, p.n_sink, p.bshift);
       mbar_wait_warp(smem_u32(&bars.s_full[j]), sc & 1);
       ++sc;
       tc_fence_after();
@@ -296,8 +300,8 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       for (int c = 0; c < kN / 32; ++c) tmem_ld32_f(scol + c * 32, &x[c * 32]);
       tmem_wait_ld();
       if (!full) {
-        // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  c > i-j0-W)
-        const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0), lo = dd - it.W;
+        // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  j0+c >= lo_i)
+        const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0), lo = (int)(lo_i - j0) - 1;
 #pragma unroll
         for (int c = 0; c < kN; ++c) {
           const bool vis = c <= dd && (c < sk || c > lo);
@@ -546,6 +550,7 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   p.nql = a.nql;
   p.G = a.G;
   p.n_sink = a.n_sink;
+  p.bshift = a.bshift;
   p.scale_log2 = a.scale * kLog2e;
   p.win_q = a.d_win_q;
   p.items = a.d_items2;

@@ -221,6 +221,11 @@ moa_status moa_resolve_spans(const float *alpha, const float *beta, int n_heads,
 
 moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_head, int n_sink,
                          int64_t N) {
+  return moa_set_spans_blocked(ctx, layer, window_per_q_head, n_sink, N, 0);
+}
+
+moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_per_q_head, int n_sink,
+                                 int64_t N, int block) {
   moa_status st = check_layer(ctx, layer, false);
   if (st) return st;
   if (!window_per_q_head) return fail(MOA_ERR_INVALID_ARG, "window_per_q_head is NULL");
@@ -232,10 +237,23 @@ moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_he
     if (w == 0 && n_sink == 0)
       return fail(MOA_ERR_INVALID_ARG, "window[%d] = 0 with no sinks: empty softmax row (reading c7)", h);
   }
+  int bshift = -1;
+  if (block != 0) {
+    if (block < 1 || block > moa::kTile || (block & (block - 1)))
+      return fail(MOA_ERR_INVALID_ARG, "block %d: must be 0 or a power of two in [1, %d]", block, moa::kTile);
+    bshift = 0;
+    while ((1 << bshift) < block) ++bshift;
+    if (n_sink % block) return fail(MOA_ERR_INVALID_ARG, "n_sink %d is not a multiple of block %d", n_sink, block);
+    for (int h = 0; h < ctx->Hq; ++h)
+      if (window_per_q_head[h] % block)
+        return fail(MOA_ERR_INVALID_ARG, "window[%d] = %d is not a multiple of block %d", h, window_per_q_head[h],
+                    block);
+  }
   LayerPlan &p = ctx->layers[layer];
   LayerPlan np;
   np.set = true;
   np.n_sink = n_sink;
+  np.bshift = bshift;
   np.N = N;
   const int G = ctx->G;
   np.win_q.resize(ctx->nql);
@@ -265,7 +283,7 @@ moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_he
     for (int qt = 0; qt < nqt; ++qt) {
       int64_t i0 = (int64_t)qt * moa::kTile;
       int64_t i1 = std::min<int64_t>(N, i0 + moa::kTile) - 1;
-      const int c = moa::kv_tile_ranges(i0, i1, np.win_q[h], n_sink).count();
+      const int c = moa::kv_tile_ranges(i0, i1, np.win_q[h], n_sink, bshift).count();
       hc += c;
       its.push_back({h, qt, c, 0});
     }
@@ -290,7 +308,8 @@ moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_he
     const size_t first = its.size();
     int64_t hc = 0;
     for (int qb = 0; qb < nqb; ++qb) {
-      const moa::BlockTiles bt = moa::kv_block_tiles((int64_t)qb * 2 * moa::kTile, N, np.win_q[h], n_sink);
+      const moa::BlockTiles bt =
+          moa::kv_block_tiles((int64_t)qb * 2 * moa::kTile, N, np.win_q[h], n_sink, bshift);
       const int c = bt.r[0].count() + (bt.has1 ? bt.r[1].count() : 0);
       hc += c;
       its.push_back({h, qb, c, 0});
@@ -501,6 +520,7 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   a.nql = ctx->nql; a.G = ctx->G; a.d = ctx->d;
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
   a.d_items2 = p.d_items2; a.n_items2 = (int)(p.items2.size() / 2);
+  a.bshift = p.bshift;
   int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_pp(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
   if (!fill) {
@@ -733,13 +753,13 @@ moa_status moa_prefill_tiles(const moa_ctx *ctx, int layer, int q_head_local, in
   int64_t i0 = (int64_t)q_tile * moa::kTile;
   int64_t i1 = std::min<int64_t>(p.N, i0 + moa::kTile) - 1;
   int W = p.win_q[q_head_local];
-  moa::TileRanges r = moa::kv_tile_ranges(i0, i1, W, p.n_sink);
+  moa::TileRanges r = moa::kv_tile_ranges(i0, i1, W, p.n_sink, p.bshift);
   int n = r.count();
   *n_tiles = n;
   for (int k2 = 0; k2 < n && k2 < max_tiles; ++k2) {
     int t = r.at(k2);
     if (tiles) tiles[k2] = t;
-    if (edge) edge[k2] = moa::kv_tile_full(i0, i1, t, W, p.n_sink) ? 0 : 1;
+    if (edge) edge[k2] = moa::kv_tile_full(i0, i1, t, W, p.n_sink, p.bshift) ? 0 : 1;
   }
   return ok();
 }

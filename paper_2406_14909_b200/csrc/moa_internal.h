@@ -4,6 +4,9 @@
 //
 // Mask (PAPER.md:178 sinks; reading c3 window incl. the query itself):
 //   key j visible to query i  <=>  0 <= j <= i  and  (j < s  or  i - j < W)
+// Block mode (bshift = log2(block), -1 = token mode): the
+// window of query i starts at the first key of block floor(i/b) - W/b + 1 instead of i-W+1
+// (s and W multiples of b), so one helper gives the first window key for both modes.
 // Ring slot of position p (reading c13):
 //   p < s ? p : s + (p - s) mod W_g
 #pragma once
@@ -32,19 +35,23 @@ constexpr int kTile = MOA_TILE;  // prefill q/kv tile (rows)
 //   window tiles [floor(max(0, i0-W+1) / T), floor(i1 / T) + 1)    (empty if W == 0)
 // merged into two disjoint ascending ranges [a0,a1) U [b0,b1).
 // ------------------------------------------------------------------------------------------
+MOA_HD int64_t win_lo(int64_t i, int W, int bshift) {
+  return bshift < 0 ? i - W + 1 : (((i >> bshift) - (int64_t)(W >> bshift) + 1) << bshift);
+}
+
 struct TileRanges {
   int a0, a1, b0, b1;
   MOA_HD int count() const { return (a1 - a0) + (b1 - b0); }
   MOA_HD int at(int k) const { return k < (a1 - a0) ? a0 + k : b0 + (k - (a1 - a0)); }
 };
 
-MOA_HD TileRanges kv_tile_ranges(int64_t i0, int64_t i1, int W, int s) {
+MOA_HD TileRanges kv_tile_ranges(int64_t i0, int64_t i1, int W, int s, int bshift = -1) {
   TileRanges r;
   int64_t nsink_keys = s < i1 + 1 ? (int64_t)s : i1 + 1;
   r.a0 = 0;
   r.a1 = (int)((nsink_keys + kTile - 1) / kTile);
   if (W > 0) {
-    int64_t lo = i0 - W + 1;
+    int64_t lo = win_lo(i0, W, bshift);  // the window start is non-decreasing in i
     if (lo < 0) lo = 0;
     r.b0 = (int)(lo / kTile);
     r.b1 = (int)(i1 / kTile) + 1;
@@ -59,11 +66,11 @@ MOA_HD TileRanges kv_tile_ranges(int64_t i0, int64_t i1, int W, int s) {
 // A kv tile needs no mask iff every (row, key) pair of the tile is visible:
 // all keys <= the first row (causal) and every non-sink key of the tile is
 // inside the window of the last row (the farthest pair).
-MOA_HD bool kv_tile_full(int64_t i0, int64_t i1, int t, int W, int s) {
+MOA_HD bool kv_tile_full(int64_t i0, int64_t i1, int t, int W, int s, int bshift = -1) {
   int64_t j0 = (int64_t)t * kTile, j1 = j0 + kTile - 1;
   if (j1 > i0) return false;
   int64_t jn = j0 > s ? j0 : (int64_t)s;  // first non-sink key of the tile
-  return jn > j1 || (i1 - jn < W);
+  return jn > j1 || (W > 0 && jn >= win_lo(i1, W, bshift));
 }
 
 MOA_HD bool tile_in(const TileRanges &r, int t) { return (t >= r.a0 && t < r.a1) || (t >= r.b0 && t < r.b1); }
@@ -80,12 +87,12 @@ struct BlockTiles {
   MOA_HD int at(int k) const { return k < u_a1 ? k : u_b0 + (k - u_a1); }
 };
 
-MOA_HD BlockTiles kv_block_tiles(int64_t i0, int64_t N, int W, int s) {
+MOA_HD BlockTiles kv_block_tiles(int64_t i0, int64_t N, int W, int s, int bshift = -1) {
   BlockTiles b;
-  b.r[0] = kv_tile_ranges(i0, (i0 + kTile < N ? i0 + kTile : N) - 1, W, s);
+  b.r[0] = kv_tile_ranges(i0, (i0 + kTile < N ? i0 + kTile : N) - 1, W, s, bshift);
   b.has1 = i0 + kTile < N;
   if (b.has1) {
-    b.r[1] = kv_tile_ranges(i0 + kTile, (i0 + 2 * kTile < N ? i0 + 2 * kTile : N) - 1, W, s);
+    b.r[1] = kv_tile_ranges(i0 + kTile, (i0 + 2 * kTile < N ? i0 + 2 * kTile : N) - 1, W, s, bshift);
   } else {
     b.r[1].a0 = b.r[1].a1 = b.r[1].b0 = b.r[1].b1 = 0;
   }
@@ -127,6 +134,7 @@ MOA_HD int64_t pos_of_row(int64_t r, int64_t p, int s, int Wg) {
 struct LayerPlan {
   bool set = false;
   int n_sink = 0;
+  int bshift = -1;               // prefill mask: -1 token-granular, else log2(block size)
   int64_t N = 0;
   std::vector<int32_t> win_q;    // local q-heads
   std::vector<int32_t> win_g;    // local groups: W_g
@@ -195,6 +203,7 @@ struct PrefillArgs {
   int n_items;
   const int32_t *d_items2;  // (h_local, q_block) pairs of the two-tile kernel
   int n_items2;
+  int bshift;               // -1 token mask, else log2(block size) (block mode)
 };
 int launch_prefill_f32(const PrefillArgs &a, void *stream);
 int launch_prefill_bf16_pp(const PrefillArgs &a, void *stream);

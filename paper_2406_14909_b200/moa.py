@@ -75,9 +75,15 @@ class MoAContext:
             pass
 
     # ---- planning ---------------------------------------------------------------------
-    def set_spans(self, layer: int, windows: Sequence[int], n_sink: int, N: int):
+    def set_spans(self, layer: int, windows: Sequence[int], n_sink: int, N: int, block: int = 0):
+        """moa_set_spans (block = 0, token mask) / moa_set_spans_blocked (block-granular
+        prefill mask of the paper)."""
         w = (c_int32 * len(windows))(*[int(x) for x in windows])
-        check(self.lib.moa_set_spans(self.ctx, layer, w, int(n_sink), int(N)), "moa_set_spans")
+        if block:
+            check(self.lib.moa_set_spans_blocked(self.ctx, layer, w, int(n_sink), int(N), int(block)),
+                  "moa_set_spans_blocked")
+        else:
+            check(self.lib.moa_set_spans(self.ctx, layer, w, int(n_sink), int(N)), "moa_set_spans")
 
     def cache_bytes(self, batch: int):
         k, v = c_size_t(), c_size_t()

@@ -20,12 +20,12 @@ def moa():
     return m
 
 
-def _prefill(moa, q, k, v, W, s, dtype, scale=None, ctx_batch=None):
+def _prefill(moa, q, k, v, W, s, dtype, scale=None, ctx_batch=None, block=0):
     dev = torch.device("cuda")
     B, N, Hq, d = q.shape
     Hkv = k.shape[2]
     ctx = moa.MoAContext(1, Hq, Hkv, d, ctx_batch or B, dtype=dtype)
-    ctx.set_spans(0, W, s, N)
+    ctx.set_spans(0, W, s, N, block=block)
     ctx.alloc_cache(B)
     qg, kg, vg = q.to(dev), k.to(dev), v.to(dev)
     o = torch.full_like(qg, float("nan"))
@@ -131,7 +131,7 @@ def _sample_rows(B, Hq, N, s, W, rng, n_rand=24):
     return rows
 
 
-def _full_layer_prefill(moa, name, layer, batch=None):
+def _full_layer_prefill(moa, name, layer, batch=None, block=0):
     cfg = CONFIGS[name]
     dev = torch.device("cuda")
     B = cfg.batch if batch is None else batch
@@ -139,7 +139,7 @@ def _full_layer_prefill(moa, name, layer, batch=None):
     W = moa.resolve_spans(t["alpha"][layer], t["beta"][layer], cfg.N, cfg.n_sink)
     q, k, v = prefill_qkv(cfg, layer, batch=B, device=dev)
     ctx = moa.MoAContext(1, cfg.hq, cfg.hkv, cfg.head_dim, B, dtype=torch.bfloat16)
-    ctx.set_spans(0, W, cfg.n_sink, cfg.N)
+    ctx.set_spans(0, W, cfg.n_sink, cfg.N, block=block)
     ctx.alloc_cache(B)
     o = torch.empty_like(q)
     lse = torch.empty(B, cfg.hq, cfg.N, dtype=torch.float32, device=dev)
@@ -151,7 +151,8 @@ def _full_layer_prefill(moa, name, layer, batch=None):
     bs = sorted(set(r[0] for r in rows))
     qs, ks, vs = f64(q[bs]), f64(k[bs]), f64(v[bs])
     remap = {b: i for i, b in enumerate(bs)}
-    O, L = oracle.prefill_rows(qs, ks, vs, W, cfg.n_sink, scale, [(remap[b], h, i) for b, h, i in rows])
+    O, L = oracle.prefill_rows(qs, ks, vs, W, cfg.n_sink, scale, [(remap[b], h, i) for b, h, i in rows],
+                               block=block)
     got = np.stack([f64(o[b, i, h]) for b, h, i in rows])
     gl = np.array([float(lse[b, h, i]) for b, h, i in rows])
     assert np.abs(got - O).max() < 2e-2
@@ -237,3 +238,87 @@ def test_prefill_attn_plus_cache_fill_equals_prefill(moa, dtype):
     torch.cuda.synchronize()
     assert ctx.next_pos(0) == N
     check_cache_image(ctx, 0, k.cpu(), v.cpu(), N - 1, W, s, B, 2)
+
+
+# ----------------------------------------------------------------------------------------
+# block mode: the paper's block sliding-window prefill mask
+# ----------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("b", [64, 16])
+@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("N", [100, 300, 513, 1000])
+def test_prefill_block_bf16(moa, b, d, N):
+    B, Hq, Hkv, s = 2, 6, 3, b
+    W = [0, b, 2 * b, 3 * b, 256, (N // b + 2) * b]
+    q = normal((B, N, Hq, d), 401, torch.bfloat16)
+    k = normal((B, N, Hkv, d), 402, torch.bfloat16)
+    v = normal((B, N, Hkv, d), 403, torch.bfloat16)
+    ctx, o, lse, scale = _prefill(moa, q, k, v, W, s, torch.bfloat16, block=b)
+    O, L = oracle.prefill(f64(q), f64(k), f64(v), W, s, scale, block=b)
+    err = np.abs(f64(o) - O)
+    assert np.isfinite(f64(o)).all()
+    assert err.max() < 2e-2, (err.max(), np.unravel_index(err.argmax(), err.shape))
+    assert np.abs(f64(lse) - L).max() < 2e-3
+    check_cache_image(ctx, 0, k, v, N - 1, W, s, B, 2)   # the cache fill is mode-independent
+
+
+@pytest.mark.parametrize("N", [129, 300])
+def test_prefill_block_fp32(moa, N):
+    B, Hq, Hkv, d, s, b = 2, 4, 2, 64, 16, 16
+    W = [16, 48, 0, 160]
+    q = normal((B, N, Hq, d), 411)
+    k = normal((B, N, Hkv, d), 412)
+    v = normal((B, N, Hkv, d), 413)
+    ctx, o, lse, scale = _prefill(moa, q, k, v, W, s, torch.float32, block=b)
+    O, L = oracle.prefill(f64(q), f64(k), f64(v), W, s, scale, block=b)
+    assert np.abs(f64(o) - O).max() < 1e-5
+    assert np.abs(f64(lse) - L).max() < 1e-5
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.bfloat16, 2e-2), (torch.float32, 1e-5)])
+def test_prefill_block_structured(moa, dtype, tol):
+    """Spike keys at the last key of every block: the token window of a row ending inside a
+    block reaches the spike just before the block-aligned window start, the block window
+    does not, so the two masks differ by O(1) (and so would a kernel off by one block)."""
+    B, N, H, d, s, b = 1, 640, 4, 64 if dtype == torch.float32 else 128, 16, 16
+    W = [16, 32, 208, 640]
+    u = torch.zeros(d)
+    u[0] = 1.0
+    spike = (torch.arange(N) % b == b - 1).float() * 8.0
+    k = (spike[None, :, None, None] * u).expand(B, N, H, d).clone()
+    k = (k + 0.01 * normal((B, N, H, d), 7)).to(dtype)
+    v = normal((B, N, H, d), 8, dtype)
+    q = u.expand(B, N, H, d).clone().to(dtype)
+    ctx, o, lse, _ = _prefill(moa, q, k, v, W, s, dtype, scale=1.0, block=b)
+    O, _ = oracle.prefill(f64(q), f64(k), f64(v), W, s, 1.0, block=b)
+    assert np.abs(f64(o) - O).max() < tol
+    Ot, _ = oracle.prefill(f64(q), f64(k), f64(v), W, s, 1.0)   # the token mask differs here
+    assert np.abs(Ot - O).max() > 0.1
+
+
+def test_c4_full_layer_prefill_block64(moa):
+    """C4's rule windows are multiples of 64 (alpha in multiples of 2048, beta in k/8, N=16k),
+    so the layer runs with the paper's block-64 mask; sampled rows vs the oracle."""
+    _full_layer_prefill(moa, "C4", 33, block=64)
+
+
+def test_block_prefill_then_token_decode(moa):
+    """Block mode changes prefill only: the cache and the token-granular decode that follows
+    are those of the token mode."""
+    dev = torch.device("cuda")
+    B, N, Hq, Hkv, d, s, b = 2, 300, 4, 2, 128, 64, 64
+    W = [64, 128, 0, 192]
+    q = normal((B, N, Hq, d), 421, torch.bfloat16)
+    k = normal((B, N, Hkv, d), 422, torch.bfloat16)
+    v = normal((B, N, Hkv, d), 423, torch.bfloat16)
+    qd = normal((B, Hq, d), 424, torch.bfloat16)
+    kd = normal((B, Hkv, d), 425, torch.bfloat16)
+    vd = normal((B, Hkv, d), 426, torch.bfloat16)
+    ctx, o, lse, scale = _prefill(moa, q, k, v, W, s, torch.bfloat16, block=b)
+    ws = ctx.alloc_workspace(B)
+    od = torch.empty(B, Hq, d, dtype=torch.bfloat16, device=dev)
+    ctx.decode_step_fused(0, qd.to(dev), kd.to(dev), vd.to(dev), od, N, scale, ws)
+    torch.cuda.synchronize()
+    Kh, Vh = torch.cat([k, kd[:, None]], 1), torch.cat([v, vd[:, None]], 1)
+    Od, _ = oracle.decode(f64(qd), f64(Kh), f64(Vh), N, W, s, scale)
+    assert np.abs(f64(od) - Od).max() < 2e-2

@@ -162,3 +162,45 @@ def test_validation_errors(moa):
         c.cache_bytes(1)                              # spans unset
     c.set_spans(0, [1, 2, 3, 4], 4, 10)
     assert c.next_pos(0) == -1
+
+
+@pytest.mark.parametrize("b", [1, 16, 64, 128])
+@pytest.mark.parametrize("N,s", [(300, 0), (300, 64), (513, 128), (40, 0)])
+def test_prefill_tile_schedule_block_mode_is_exact(moa, b, N, s):
+    """Block mode: visited tiles / EDGE flags == brute force over the oracle's
+    block predicate."""
+    if s % b:
+        pytest.skip("sinks must be a multiple of the block")
+    T = 128
+    windows = [b, 2 * b, 4 * b, 128 if b <= 128 else b, 256, N // b * b or b, (N // b + 3) * b]
+    windows = [w for w in windows if w % b == 0]
+    c = _ctx(moa, Hq=len(windows), Hkv=len(windows), B=1)
+    c.set_spans(0, windows, s, N, block=b)
+    nqt = (N + T - 1) // T
+    for h, W in enumerate(windows):
+        for qt in range(nqt):
+            rows = range(qt * T, min(N, qt * T + T))
+            vis_tiles, full = set(), {}
+            for t in range((N + T - 1) // T + 1):
+                pairs = [oracle.visible_block(i, j, W, s, b) for i in rows for j in range(t * T, t * T + T)]
+                if any(pairs):
+                    vis_tiles.add(t)
+                    full[t] = all(pairs)
+            tiles, edge = c.prefill_tiles(0, h, qt)
+            assert sorted(tiles) == sorted(vis_tiles), (h, W, qt)
+            for t, e in zip(tiles, edge):
+                assert e == (not full[t]), (h, W, qt, t)
+
+
+def test_block_mode_validation(moa):
+    from paper_2406_14909_b200 import MoAError
+    c = _ctx(moa)
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_spans(0, [64, 64, 64, 64], 64, 1000, block=48)    # not a power of two
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_spans(0, [64, 64, 64, 64], 64, 1000, block=256)   # larger than a tile
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_spans(0, [64, 65, 64, 64], 64, 1000, block=64)    # window not a multiple
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_spans(0, [64, 64, 64, 64], 32, 1000, block=64)    # sinks not a multiple
+    c.set_spans(0, [64, 128, 0, 1024], 64, 1000, block=64)
