@@ -77,6 +77,8 @@ __all__ = [
     "density",
     "visible_pairs",
     "visible_pairs_block",
+    "attention_influence",
+    "influence_blocks",
 ]
 
 
@@ -338,3 +340,66 @@ def visible_pairs(N: int, W: int, s: int) -> int:
         overlap = max(0, min(s, i + 1) - lo) if W > 0 else 0
         total += n_sink + n_win - overlap
     return total
+
+
+# ---------------------------------------------------------------------------
+# Attention influence (Eq. 3; derivation PAPER.md:1361-1405)
+# ---------------------------------------------------------------------------
+
+def attention_influence(A: np.ndarray, G: np.ndarray) -> np.ndarray:
+    """E of one head (Eq. 3, ``eq:effect``):
+
+        E_ij = G_ij * (-A_ij) + sum_{n != j} G_in * A_in * A_ij / (1 - A_ij)
+
+    with A the attention matrix (rows stochastic over their visible keys) and
+    G = dL/dA.  Written term by term as in Eq. 3.  Entries with A_ij = 1 (the
+    row's only visible key: masking it is never a candidate) are 0 (SPEC.md:287
+    degenerate-row decision); masked entries (A_ij = 0) give 0.
+    """
+    A = np.asarray(A, dtype=np.float64)
+    G = np.asarray(G, dtype=np.float64)
+    E = np.zeros_like(A)
+    n_rows, n_cols = A.shape
+    for i in range(n_rows):
+        for j in range(n_cols):
+            a = A[i, j]
+            if a == 0.0 or a >= 1.0:
+                continue
+            direct = G[i, j] * (-a)
+            indirect = sum(G[i, n] * A[i, n] for n in range(n_cols) if n != j) * a / (1.0 - a)
+            E[i, j] = direct + indirect
+    return E
+
+
+def influence_blocks(Q, K, V, dO, tau: float, block: int):
+    """Block-averaged attention influence of every head for one calibration item.
+
+    The profiling pass of the paper: dense causal attention (PAPER.md:691
+    profiles the unmasked model), ``A = softmax(tau Q K^T + causal)``
+    (Eq. 1), ``G = dL/dA = dO V^T`` for ``O = A V`` (chain rule),
+    E by Eq. 3, then "the average attention influence within each block"
+     over ``block x block`` token pairs (masked pairs count as 0,
+    the last block may be partial: mean over its real pairs).
+    Q, dO: [B, N, Hq, d]; K, V: [B, N, Hkv, d].  Returns [B, Hq, nb, nb] fp64.
+    """
+    B, N, Hq, d = Q.shape
+    Hkv = K.shape[2]
+    G_ = Hq // Hkv
+    nb = (N + block - 1) // block
+    out = np.zeros((B, Hq, nb, nb), dtype=np.float64)
+    for b in range(B):
+        for h in range(Hq):
+            g = h // G_
+            S = tau * (Q[b, :, h].astype(np.float64) @ K[b, :, g].astype(np.float64).T)
+            A = np.zeros((N, N))
+            for i in range(N):
+                z = S[i, : i + 1]
+                w = np.exp(z - z.max())
+                A[i, : i + 1] = w / w.sum()
+            Gm = dO[b, :, h].astype(np.float64) @ V[b, :, g].astype(np.float64).T
+            E = attention_influence(A, Gm)
+            for ib in range(nb):
+                for jb in range(nb):
+                    blk = E[ib * block:(ib + 1) * block, jb * block:(jb + 1) * block]
+                    out[b, h, ib, jb] = blk.sum() / blk.size
+    return out

@@ -319,3 +319,70 @@ def test_block_visible_pairs_brute_force():
     assert oracle.visible_pairs_block(16, 8, 4, 4) == sum(r.count("1") for r in pic)
     for N, W, s in ((50, 7, 3), (64, 64, 0), (33, 1, 0)):
         assert oracle.visible_pairs_block(N, W, s, 1) == oracle.visible_pairs(N, W, s)
+
+
+# --- attention influence (Eq. 3; derivation PAPER.md:1361-1405) ----------
+
+def _renormalised_delta(A_row, j):
+    """eq:delta_A by its definition: A as exp(S)/sum exp(S); mask key j (drop its term)
+    and recompute the row; the change of every entry (brute force, not the closed form)."""
+    S = np.log(np.where(A_row > 0, A_row, 1.0))
+    vis = A_row > 0
+    w = np.where(vis, np.exp(S), 0.0)
+    w_masked = w.copy()
+    w_masked[j] = 0.0
+    return w_masked / w_masked.sum() - w / w.sum()
+
+
+def test_influence_spec_worked_example():
+    """row A=[0.75, 0.25], g=[1, 2], masking key 2 -> E = -0.25; masking key 1
+    gives dA = [-0.75, +0.75], sum g dA = 0.75 (the same renormalisation rule)."""
+    E = oracle.attention_influence(np.array([[0.75, 0.25]]), np.array([[1.0, 2.0]]))
+    assert abs(E[0, 1] - (-0.25)) < 1e-12
+    assert abs(E[0, 0] - 0.75) < 1e-12
+
+
+def test_influence_equals_sum_of_g_times_renormalised_change():
+    """Eq. 3 == sum_n g_in dA_in|j with dA from re-normalising the softmax row without key j
+    (eq:each_effect + eq:delta_A evaluated by brute force), random causal rows."""
+    rng = np.random.default_rng(7)
+    N = 9
+    S = rng.standard_normal((N, N)) * 2
+    A = np.zeros((N, N))
+    for i in range(N):
+        w = np.exp(S[i, :i + 1] - S[i, :i + 1].max())
+        A[i, :i + 1] = w / w.sum()
+    G = rng.standard_normal((N, N))
+    E = oracle.attention_influence(A, G)
+    for i in range(1, N):
+        for j in range(i + 1):
+            dA = _renormalised_delta(A[i], j)
+            assert abs(dA.sum()) < 1e-12                     # SPEC.md:299 stochasticity kept
+            assert abs(E[i, j] - float(G[i] @ dA)) < 1e-12
+    assert E[0, 0] == 0.0                                   # single visible key: defined 0
+
+
+def test_influence_zero_gradient_and_block_size_one():
+    rng = np.random.default_rng(8)
+    B, N, H, d = 1, 12, 2, 4
+    Q, K, V = rng.standard_normal((B, N, H, d)), rng.standard_normal((B, N, H, d)), rng.standard_normal((B, N, H, d))
+    assert np.all(oracle.influence_blocks(Q, K, V, np.zeros((B, N, H, d)), 0.5, 4) == 0.0)   # g = 0 -> E = 0
+    dO = rng.standard_normal((B, N, H, d))
+    e1 = oracle.influence_blocks(Q, K, V, dO, 0.5, 1)
+    e3 = oracle.influence_blocks(Q, K, V, dO, 0.5, 3)
+    # block mean of 3x3 == mean of the block-1 entries (averaging is linear)
+    for ib in range(4):
+        for jb in range(4):
+            assert abs(e3[0, 1, ib, jb] - e1[0, 1, ib * 3:ib * 3 + 3, jb * 3:jb * 3 + 3].mean()) < 1e-12
+    assert np.all(e1[0, 0][np.triu_indices(N, 1)] == 0.0)   # non-causal pairs carry no influence
+
+
+def test_influence_gradient_is_chain_rule_of_o_equals_av():
+    """G = dO V^T is dL/dA for O = A V: torch autograd on L = sum(dO * (A V)) in fp64."""
+    rng = np.random.default_rng(9)
+    N, d = 7, 5
+    A = torch.tensor(rng.random((N, N)), requires_grad=True)
+    V = torch.tensor(rng.standard_normal((N, d)))
+    dO = torch.tensor(rng.standard_normal((N, d)))
+    (dO * (A @ V)).sum().backward()
+    assert torch.allclose(A.grad, dO @ V.T, atol=1e-12)
