@@ -231,6 +231,29 @@ moa_status moa_cache_region(const moa_ctx *ctx, int layer, int b, int group_loca
 /* Byte offset of a layer inside a moa_bind_cache buffer laid out for `batch`. */
 moa_status moa_layer_offset(const moa_ctx *ctx, int layer, int batch, size_t *byte_offset);
 
+/*
+ * Block-averaged attention influence of the profiling stage: for one
+ * calibration item with dense causal attention A = softmax(scale * Q K^T + causal) (Eq. 1)
+ * and G = dL/dA = dO V^T (O = A V), the influence of masking A_ij (Eq. 3, PAPER.md:225-236;
+ * derivation PAPER.md:1361-1405)
+ *     E_ij = -A_ij / (1 - A_ij) * (G_ij - sum_n G_in A_in)     (E = 0 where A_ij = 1)
+ * averaged over the block x block token pairs of every (query block, key block)
+ * ("the average attention influence within each block"; the last block
+ * of a ragged N averages its real pairs).  Stateless; bf16 inputs, fp32 math and output.
+ *   q, dout   [B, N, Hq, d] bf16, token row stride q_row_stride (elements).
+ *   k, v      [B, N, Hkv, d] bf16 (Hq % Hkv == 0), row stride kv_row_stride.
+ *   head_dim  64 or 128.  block: 64 (the paper's block; MOA_ERR_UNSUPPORTED otherwise).
+ *   e_blocks  fp32 [B, Hq, nb, nb], nb = ceil(N / block), caller-owned device memory:
+ *             accumulate = 0 overwrites every entry (key blocks after the query block: 0);
+ *             accumulate = 1 adds to the causal entries (averaging over calibration items
+ *             is the caller's division by the item count).
+ * Stream-ordered, no allocation, no host synchronisation.
+ */
+moa_status moa_attention_influence(const void *q, const void *k, const void *v, const void *dout, int batch,
+                                   int64_t N, int num_q_heads, int num_kv_heads, int head_dim,
+                                   int64_t q_row_stride, int64_t kv_row_stride, float scale, int block,
+                                   float *e_blocks, int accumulate, moa_stream_t stream);
+
 /* Prefill block-skip schedule (a2): the kv tiles (of MOA_TILE keys) that q-tile
  * `q_tile` (rows [q_tile*MOA_TILE, ...)) of local q-head h visits, in visit
  * order, with flags 1 = EDGE (needs the mask) / 0 = FULL.  *n_tiles is set

@@ -1,0 +1,263 @@
+// influence.cu -- block-averaged attention influence of the MoA profiling stage
+// (Eq. 3, derivation PAPER.md:1361-1405).
+//
+// For one calibration item and every (batch, q-head), with dense causal attention
+// (the profiled model is unmasked):
+//   A   = softmax(tau Q K^T + causal)                         (Eq. 1)
+//   G   = dL/dA = dO V^T                                       (O = A V, chain rule)
+//   E_ij = -A_ij / (1 - A_ij) * (G_ij - R_i),  R_i = sum_n G_in A_in   (Eq. 3, last line
+//          of the derivation; E = 0 where A_ij = 1, the row's only visible key)
+//   out[b, h, ib, jb] (+)= mean of E over the block x block token pairs
+//
+// One CTA per (64-row query block, q-head, batch), 4 warps x 16 rows.  QK^T and dO V^T
+// run on the tensor cores (mma.sync m16n8k16, bf16 in, fp32 accumulate); K/V blocks are
+// staged in padded shared memory.  Pass 1 walks the causal key blocks once for the row
+// statistics (online max m and the sums l = sum 2^(S-m), u = sum G 2^(S-m) kept as
+// "star key + rest" so that 1 - A and R - G are formed without cancellation when a row
+// is nearly one-hot), pass 2 recomputes S and G per key block, forms E and reduces it to the
+// block mean.  The kernel never materialises A, G or E in memory.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "../moa_internal.h"
+#include "common.cuh"
+
+namespace moa {
+namespace {
+
+constexpr int kB = 64;        // query / key block (the paper's 64)
+constexpr int kThreadsInf = 128;
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int D>
+struct InfSmem {
+  static constexpr int kStride = D + 8;  // bf16 elements per padded row: conflict-free 32-bit fragment loads
+  __nv_bfloat16 k[kB * kStride];
+  __nv_bfloat16 v[kB * kStride];
+  float red[4];
+};
+
+// S (16 rows x 64 keys) = Q K^T and G = dO V^T for this warp's rows, from the staged block.
+template <int D>
+__device__ __forceinline__ void block_products(const InfSmem<D> &sm, const uint32_t (&qa)[D / 16][4],
+                                               const uint32_t (&da)[D / 16][4], int lane, float (&S)[8][4],
+                                               float (&G)[8][4]) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int n = 0; n < 8; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) S[n][e] = G[n][e] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int key = n * 8 + g;  // B fragment column = key; k = head-dim index
+      const uint32_t *kr = reinterpret_cast<const uint32_t *>(&sm.k[key * InfSmem<D>::kStride + kk * 16]);
+      const uint32_t *vr = reinterpret_cast<const uint32_t *>(&sm.v[key * InfSmem<D>::kStride + kk * 16]);
+      mma16816(S[n], qa[kk], kr[t], kr[t + 4]);
+      mma16816(G[n], da[kk], vr[t], vr[t + 4]);
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a) {
+  __shared__ InfSmem<D> sm;
+  const int nb = (int)((a.N + kB - 1) / kB);
+  const int ib = nb - 1 - (int)blockIdx.x;  // heaviest (longest causal row) blocks first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int gkv = h / a.G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t N = a.N;
+  const int64_t r0 = (int64_t)ib * kB + warp * 16 + g, r1 = r0 + 8;  // this thread's two rows
+  const __nv_bfloat16 *Q = static_cast<const __nv_bfloat16 *>(a.q);
+  const __nv_bfloat16 *dO = static_cast<const __nv_bfloat16 *>(a.dout);
+  const __nv_bfloat16 *K = static_cast<const __nv_bfloat16 *>(a.k);
+  const __nv_bfloat16 *V = static_cast<const __nv_bfloat16 *>(a.v);
+
+  // A fragments of Q and dO for this warp's 16 rows (rows >= N read as 0)
+  uint32_t qa[D / 16][4], da[D / 16][4];
+  {
+    auto ld = [&](const __nv_bfloat16 *X, int64_t stride, int64_t r, int col) -> uint32_t {
+      if (r >= N) return 0u;
+      return *reinterpret_cast<const uint32_t *>(X + ((int64_t)b * N + r) * stride + (int64_t)h * D + col);
+    };
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const int c = kk * 16 + 2 * t;
+      qa[kk][0] = ld(Q, a.q_row_stride, r0, c);
+      qa[kk][1] = ld(Q, a.q_row_stride, r1, c);
+      qa[kk][2] = ld(Q, a.q_row_stride, r0, c + 8);
+      qa[kk][3] = ld(Q, a.q_row_stride, r1, c + 8);
+      da[kk][0] = ld(dO, a.q_row_stride, r0, c);
+      da[kk][1] = ld(dO, a.q_row_stride, r1, c);
+      da[kk][2] = ld(dO, a.q_row_stride, r0, c + 8);
+      da[kk][3] = ld(dO, a.q_row_stride, r1, c + 8);
+    }
+  }
+  auto stage = [&](int jb) {
+    __syncthreads();
+    constexpr int kVec = D / 8;  // 16-byte vectors per row
+    for (int idx = threadIdx.x; idx < kB * kVec; idx += kThreadsInf) {
+      const int r = idx / kVec, c = (idx - r * kVec) * 8;
+      const int64_t j = (int64_t)jb * kB + r;
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = kv;
+      if (j < N) {
+        const int64_t off = ((int64_t)b * N + j) * a.kv_row_stride + (int64_t)gkv * D + c;
+        kv = *reinterpret_cast<const uint4 *>(K + off);
+        vv = *reinterpret_cast<const uint4 *>(V + off);
+      }
+      *reinterpret_cast<uint4 *>(&sm.k[r * InfSmem<D>::kStride + c]) = kv;
+      *reinterpret_cast<uint4 *>(&sm.v[r * InfSmem<D>::kStride + c]) = vv;
+    }
+    __syncthreads();
+  };
+  const float sl2 = a.scale * kLog2e;  // scores in log2 units
+  float S[8][4], G[8][4];
+
+  // ---- pass 1: row statistics over the causal key blocks 0..ib.  With p_k = 2^(S_k - m)
+  // (m = the row max, in log2 units) the row is kept as l = 1 + Lr and u = sum G p = Gs + Ur,
+  // where key js (the first key attaining m, G_js = Gs) is split off: 1 - A_js = Lr / l and
+  // R - G_js = (Ur - Gs Lr) / l are then formed without cancellation when A_js -> 1.
+  float m[2] = {-INFINITY, -INFINITY}, Lr[2] = {0.f, 0.f}, Ur[2] = {0.f, 0.f}, Gs[2] = {0.f, 0.f};
+  int js[2] = {-1, -1};
+  for (int jb = 0; jb <= ib; ++jb) {
+    stage(jb);
+    block_products<D>(sm, qa, da, lane, S, G);
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int64_t i = rr ? r1 : r0;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t j = (int64_t)jb * kB + n * 8 + 2 * t + e;
+          if (j <= i) mx = fmaxf(mx, S[n][2 * rr + e] * sl2);
+        }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      // (every row sees key jb*64 <= i, so mx is finite; rows >= N run on zero Q and are
+      // dropped in pass 2; no early exit: the quad shuffles below need every lane)
+      // the block's star key: smallest index attaining mx, and its G
+      int jstar = 0x7fffffff;
+      float gstar = 0.f;
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int jl = jb * kB + n * 8 + 2 * t + e;
+          if (jl <= i && S[n][2 * rr + e] * sl2 == mx && jl < jstar) {
+            jstar = jl;
+            gstar = G[n][2 * rr + e];
+          }
+        }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        const int jo = __shfl_xor_sync(0xffffffffu, jstar, o);
+        const float go = __shfl_xor_sync(0xffffffffu, gstar, o);
+        if (jo < jstar) jstar = jo, gstar = go;
+      }
+      float rs = 0.f, us = 0.f;  // the block's keys other than its star, in units 2^(S - mx)
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int jl = jb * kB + n * 8 + 2 * t + e;
+          if (jl <= i && jl != jstar) {
+            const float pp = exp2f(S[n][2 * rr + e] * sl2 - mx);
+            rs += pp;
+            us += pp * G[n][2 * rr + e];
+          }
+        }
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+      us += __shfl_xor_sync(0xffffffffu, us, 1);
+      us += __shfl_xor_sync(0xffffffffu, us, 2);
+      if (mx == -INFINITY) {
+      } else if (mx > m[rr]) {  // the block holds the new row max: the old row (star included) joins the rest
+        const float alpha = exp2f(m[rr] - mx);  // 0 for the first block
+        Lr[rr] = (js[rr] >= 0 ? (1.f + Lr[rr]) * alpha : 0.f) + rs;
+        Ur[rr] = (js[rr] >= 0 ? (Gs[rr] + Ur[rr]) * alpha : 0.f) + us;
+        m[rr] = mx;
+        js[rr] = jstar;
+        Gs[rr] = gstar;
+      } else {  // every key of the block joins the rest (a tie with the row max counts 1)
+        const float beta = exp2f(mx - m[rr]);
+        Lr[rr] += (1.f + rs) * beta;
+        Ur[rr] += (gstar + us) * beta;
+      }
+    }
+  }
+  float l[2];
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) l[rr] = 1.f + Lr[rr];
+
+  // ---- pass 2: E per key block, reduced to the block mean
+  float *out = a.e_blocks + (((int64_t)b * a.nql + h) * nb + ib) * nb;
+  const int64_t rows_real = (N - (int64_t)ib * kB) < kB ? N - (int64_t)ib * kB : kB;
+  for (int jb = 0; jb <= ib; ++jb) {
+    stage(jb);
+    block_products<D>(sm, qa, da, lane, S, G);
+    float acc = 0.f;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int64_t i = rr ? r1 : r0;
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int jl = jb * kB + n * 8 + 2 * t + e;
+          if (jl <= i && i < N) {
+            const float g = G[n][2 * rr + e];
+            float E;
+            if (jl == js[rr]) {
+              // A/(1-A) = 1/Lr, R - G = (Ur - Gs Lr)/l; a row with one visible key: E = 0
+              E = Lr[rr] > 0.f ? (Ur[rr] - Gs[rr] * Lr[rr]) / (Lr[rr] * l[rr]) : 0.f;
+            } else {
+              const float pp = exp2f(S[n][2 * rr + e] * sl2 - m[rr]);
+              // A/(1-A) = p/(l-p), R - G = ((Gs - g) + (Ur - g Lr))/l
+              E = pp / (1.f + (Lr[rr] - pp)) * ((Gs[rr] - g) + (Ur[rr] - g * Lr[rr])) / l[rr];
+            }
+            acc += E;
+          }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sm.red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t cols_real = (N - (int64_t)jb * kB) < kB ? N - (int64_t)jb * kB : kB;
+      const float mean = (sm.red[0] + sm.red[1] + sm.red[2] + sm.red[3]) / (float)(rows_real * cols_real);
+      out[jb] = a.accumulate ? out[jb] + mean : mean;
+    }
+  }
+  if (!a.accumulate)
+    for (int jb = ib + 1 + (int)threadIdx.x; jb < nb; jb += kThreadsInf) out[jb] = 0.f;  // no causal pairs
+}
+
+}  // namespace
+
+int launch_influence(const InfluenceArgs &a, void *stream) {
+  const int nb = (int)((a.N + kB - 1) / kB);
+  dim3 grid((unsigned)nb, (unsigned)a.nql, (unsigned)a.batch);
+  if (a.d == 128)
+    influence_kernel<128><<<grid, kThreadsInf, 0, (cudaStream_t)stream>>>(a);
+  else
+    influence_kernel<64><<<grid, kThreadsInf, 0, (cudaStream_t)stream>>>(a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace moa

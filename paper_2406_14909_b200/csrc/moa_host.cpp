@@ -764,6 +764,32 @@ moa_status moa_prefill_tiles(const moa_ctx *ctx, int layer, int q_head_local, in
   return ok();
 }
 
+moa_status moa_attention_influence(const void *q, const void *k, const void *v, const void *dout, int batch,
+                                   int64_t N, int num_q_heads, int num_kv_heads, int head_dim,
+                                   int64_t q_row_stride, int64_t kv_row_stride, float scale, int block,
+                                   float *e_blocks, int accumulate, moa_stream_t stream) {
+  if (!q || !k || !v || !dout || !e_blocks) return fail(MOA_ERR_INVALID_ARG, "NULL pointer");
+  if (batch < 1 || N < 1 || N > (int64_t(1) << 31)) return fail(MOA_ERR_INVALID_ARG, "bad batch / N");
+  if (num_q_heads < 1 || num_kv_heads < 1 || num_q_heads % num_kv_heads)
+    return fail(MOA_ERR_INVALID_ARG, "num_q_heads must be a positive multiple of num_kv_heads");
+  if (head_dim != 64 && head_dim != 128) return fail(MOA_ERR_SHAPE, "head_dim %d not in {64, 128}", head_dim);
+  if (block != 64) return fail(MOA_ERR_UNSUPPORTED, "block %d: only the paper's 64 is implemented", block);
+  if (q_row_stride < (int64_t)num_q_heads * head_dim || kv_row_stride < (int64_t)num_kv_heads * head_dim)
+    return fail(MOA_ERR_SHAPE, "row strides smaller than heads * head_dim");
+  if (((uintptr_t)k & 15) || ((uintptr_t)v & 15) || ((uintptr_t)q & 3) || ((uintptr_t)dout & 3) ||
+      (kv_row_stride * 2) % 16 || (q_row_stride * 2) % 4)
+    return fail(MOA_ERR_INVALID_ARG, "k/v must be 16-byte aligned (row stride too), q/dout 4-byte aligned");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(MOA_ERR_INVALID_ARG, "scale must be finite > 0");
+  moa::InfluenceArgs a{};
+  a.q = q; a.k = k; a.v = v; a.dout = dout;
+  a.q_row_stride = q_row_stride; a.kv_row_stride = kv_row_stride;
+  a.batch = batch; a.N = N; a.nql = num_q_heads; a.G = num_q_heads / num_kv_heads; a.d = head_dim;
+  a.scale = scale; a.e_blocks = e_blocks; a.accumulate = accumulate ? 1 : 0;
+  int e = moa::launch_influence(a, stream);
+  if (e) return cuda_fail((cudaError_t)e, "influence launch");
+  return ok();
+}
+
 moa_status moa_prefill_items(const moa_ctx *ctx, int layer, int32_t *items, int max_items,
                              int32_t *n_items) {
   moa_status st = check_layer(ctx, layer, true);

@@ -270,6 +270,19 @@ struct DecodeMmaArgs {
 int launch_decode_mma(const DecodeMmaArgs &a, void *stream);
 size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d);
 
+// attention influence of the profiling stage (kernels/influence.cu)
+struct InfluenceArgs {
+  const void *q, *k, *v, *dout;  // bf16 [B, N, Hq, d] (q, dout) / [B, N, Hkv, d] (k, v)
+  int64_t q_row_stride, kv_row_stride;
+  int batch;
+  int64_t N;
+  int nql, G, d;
+  float scale;
+  float *e_blocks;  // [B, Hq, nb, nb] fp32
+  int accumulate;
+};
+int launch_influence(const InfluenceArgs &a, void *stream);
+
 // TMA tensor map over a [rows, d] bf16 cache (box box_rows x 64 cols, 128B swizzle).
 bool encode_cache_map(void *map_out, const void *ptr, int d, int64_t rows, int box_rows);
 // TMA tensor map over [B, N, H, d] bf16 (token row stride in elements), 64-column x box_rows boxes.

@@ -42,6 +42,28 @@ def resolve_spans(alpha: Sequence[float], beta: Sequence[float], N: int, n_sink:
     return list(w)
 
 
+def attention_influence(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, dout: torch.Tensor, scale: float,
+                        out: Optional[torch.Tensor] = None, block: int = 64, accumulate: bool = False,
+                        stream=None) -> torch.Tensor:
+    """Block-averaged attention influence (Eq. 3) of one calibration item through
+    ``moa_attention_influence``: q, dout [B, N, Hq, d], k, v [B, N, Hkv, d] bf16 CUDA tensors
+    (token-major, any token row stride); returns / fills fp32 [B, Hq, nb, nb]."""
+    B, N, Hq, d = q.shape
+    Hkv = k.shape[2]
+    nb = (N + block - 1) // block
+    if out is None:
+        out = torch.empty(B, Hq, nb, nb, dtype=torch.float32, device=q.device)
+    for t in (q, k, v, dout):
+        if t.dtype != torch.bfloat16 or t.stride(3) != 1 or t.stride(2) != d:
+            raise MoAError(1, "attention_influence", "bf16 tensors with contiguous heads x head_dim rows")
+    if dout.stride(1) != q.stride(1) or v.stride(1) != k.stride(1):
+        raise MoAError(1, "attention_influence", "dout/q and v/k must share their token row strides")
+    check(_lib.lib().moa_attention_influence(_ptr(q), _ptr(k), _ptr(v), _ptr(dout), B, N, Hq, Hkv, d,
+                                             q.stride(1), k.stride(1), float(scale), int(block), _ptr(out),
+                                             int(bool(accumulate)), _stream(stream)), "moa_attention_influence")
+    return out
+
+
 class MoAContext:
     """One context per (process, device): span tables, cache layout, launches."""
 
