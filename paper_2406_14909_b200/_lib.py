@@ -74,7 +74,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             f"libmoa.so not found at {path}: build it with `python -m paper_2406_14909_b200.build` "
             "(no CPU fallback exists)")
     lib = ctypes.CDLL(path)
+    diagnostic = os.path.abspath(path) != os.path.abspath(LIB_PATH)
     for name, res, args in _SIGS:
+        if diagnostic and not hasattr(lib, name):
+            continue  # an older diagnostic build (tools A/B runs) may lack newer entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

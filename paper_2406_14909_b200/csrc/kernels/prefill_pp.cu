@@ -45,7 +45,7 @@ using namespace ptx;
 constexpr int kM = 128;    // q rows per tile (MMA M)
 constexpr int kN = 128;    // keys per kv tile
 constexpr int kThreads = 384;  // warp 11 idles (warpgroup-aligned register reallocation)
-constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10;
+constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10, kSoftmaxWarp0 = 0;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kPolyEvery = 4;              // pair c uses the polynomial iff c % kPolyEvery == kPolyEvery - 1
@@ -86,12 +86,21 @@ struct PBars {
   uint32_t tmem_base;
 };
 
+// Mask mode as a template constant: BS = -1 token mask, 6 the paper's block of 64, kBsRuntime
+// any other block size (p.bshift at run time); the common modes fold their arithmetic.
+constexpr int kBsRuntime = 99;
+template <int BS>
+__device__ __forceinline__ int bshift_of(const PpParams &p) {
+  return BS == kBsRuntime ? p.bshift : BS;
+}
+
 struct PItem {
   int b, h, W;
   int64_t i0;
   BlockTiles bt;
 };
 
+template <int BS>
 __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
   PItem it;
   const int wi = idx / p.batch;
@@ -99,7 +108,7 @@ __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
   it.h = p.items[2 * wi];
   it.i0 = (int64_t)p.items[2 * wi + 1] * (2 * kM);
   it.W = p.win_q[it.h];
-  it.bt = kv_block_tiles(it.i0, p.N, it.W, p.n_sink, p.bshift);
+  it.bt = kv_block_tiles(it.i0, p.N, it.W, p.n_sink, bshift_of<BS>(p));
   return it;
 }
 
@@ -161,7 +170,7 @@ __device__ __forceinline__ void tmem_ld32_f(uint32_t taddr, float *x) {
 // ------------------------------------------------------------------------------------------
 // MMA issuer (warp 9).  Per kv step: [PV0(prev)] [S0(t)] [PV1(prev)] [S1(t)].
 // ------------------------------------------------------------------------------------------
-template <int D>
+template <int D, int BS>
 __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_t tmem, uint32_t q_smem,
                                          uint32_t k_smem, uint32_t v_smem, int total) {
   using C = PCfg<D>;
@@ -176,7 +185,7 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
   int pc[2] = {0, 0};  // P handshakes consumed per tile
   int qc[2] = {0, 0};  // items started per tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-    const PItem it = get_pitem(p, idx);
+    const PItem it = get_pitem<BS>(p, idx);
     const bool has1 = it.bt.has1;
     mbar_wait_warp(smem_u32(&bars.q_full[0]), qc[0] & 1);
     if (has1) mbar_wait_warp(smem_u32(&bars.q_full[1]), qc[1] & 1);
@@ -264,7 +273,7 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
 // ------------------------------------------------------------------------------------------
 // softmax of q tile j (warps 4j .. 4j+3): thread owns one row, all 128 columns of S_j.
 // ------------------------------------------------------------------------------------------
-template <int D>
+template <int D, int BS>
 __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uint32_t tmem, int total, int j,
                                              int warp, int lane) {
   using C = PCfg<D>;
@@ -276,14 +285,14 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
   int sc = 0;  // S handshakes of this tile
   int ic = 0;  // items of this tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-    const PItem it = get_pitem(p, idx);
+    const PItem it = get_pitem<BS>(p, idx);
     if (j == 1 && !it.bt.has1) continue;
     const int64_t ti0 = it.i0 + j * kM;                     // first row of this q tile
     const int64_t ti1 = (ti0 + kM < p.N ? ti0 + kM : p.N) - 1;  // last real row
     const int64_t i = ti0 + row;
     // first window key of this row: i-W+1 (token mask) or the block-aligned start (block mode);
     // W = 0 puts it past the row
-    const int64_t lo_i = it.W > 0 ? win_lo(i, it.W, p.bshift) : i + 1;
+    const int64_t lo_i = BS >= 0 ? (it.W > 0 ? win_lo(i, it.W, bshift_of<BS>(p)) : i + 1) : i - it.W + 1;
     float m_used = -INFINITY, l = 0.f;
     const TileRanges rj = j ? it.bt.r[1] : it.bt.r[0];  // (no dynamic indexing: keeps it in registers)
     const int ns = it.bt.steps();
@@ -291,7 +300,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       const int t = it.bt.at(k);
       if (!tile_in(rj, t)) continue;
       const int64_t j0 = (int64_t)t * kN;
-      const bool full = kv_tile_full(ti0, ti1, t, it.W, p.n_sink, p.bshift);
+      const bool full = kv_tile_full(ti0, ti1, t, it.W, p.n_sink, bshift_of<BS>(p));
       mbar_wait_warp(smem_u32(&bars.s_full[j]), sc & 1);
       ++sc;
       tc_fence_after();
@@ -301,7 +310,8 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       tmem_wait_ld();
       if (!full) {
         // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  j0+c >= lo_i)
-        const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0), lo = (int)(lo_i - j0) - 1;
+        const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0);
+        const int lo = BS >= 0 ? (int)(lo_i - j0) - 1 : dd - it.W;  // token mask: the original form
 #pragma unroll
         for (int c = 0; c < kN; ++c) {
           const bool vis = c <= dd && (c < sk || c > lo);
@@ -406,7 +416,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
   }
 }
 
-template <int D>
+template <int D, int BS>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const PpParams p) {
@@ -450,16 +460,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
 
-  if (warp < 8) {
+  if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
-    softmax_role<D>(p, bars, tmem, total, warp >> 2, warp, lane);
+    softmax_role<D, BS>(p, bars, tmem, total, (warp - kSoftmaxWarp0) >> 2, warp, lane);
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
   if (warp == kWarpKV) {
     if (lane == 0) {
       int T = 0;
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-        const PItem it = get_pitem(p, idx);
+        const PItem it = get_pitem<BS>(p, idx);
         const int g = it.h / p.G;
         const int ns = it.bt.steps();
         for (int k = 0; k < ns; ++k) {
@@ -488,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int qc[2] = {0, 0};
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-        const PItem it = get_pitem(p, idx);
+        const PItem it = get_pitem<BS>(p, idx);
         for (int j = 0; j < 2; ++j) {
           if (j == 1 && !it.bt.has1) continue;
           if (qc[j] > 0) mbar_wait(smem_u32(&bars.q_empty[j]), (qc[j] - 1) & 1);
@@ -501,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // warm L2 with the next item's Q tiles (their loads wait for this item's last S MMAs)
         if (idx + (int)gridDim.x < total) {
-          const PItem nx = get_pitem(p, idx + gridDim.x);
+          const PItem nx = get_pitem<BS>(p, idx + gridDim.x);
           for (int j = 0; j < (nx.bt.has1 ? 2 : 1); ++j)
             for (int sl = 0; sl < C::kSlabs; ++sl)
               tma_prefetch_4d(&tm_q, sl * 64, nx.h, (int)(nx.i0 + j * kM), nx.b);
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kWarpMMA) {
-    mma_role<D>(p, bars, tmem, q_smem, k_smem, v_smem, total);
+    mma_role<D, BS>(p, bars, tmem, q_smem, k_smem, v_smem, total);
   }
   }
 
@@ -554,12 +564,16 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   p.scale_log2 = a.scale * kLog2e;
   p.win_q = a.d_win_q;
   p.items = a.d_items2;
-  cudaError_t e =
-      cudaFuncSetAttribute(prefill_pp_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  // the token mask (bshift < 0) and the block mask are separate instantiations, so the
+  // token path carries no block-mode arithmetic
+  auto kern = p.bshift < 0    ? prefill_pp_kernel<D, -1>
+              : p.bshift == 6 ? prefill_pp_kernel<D, 6>
+                              : prefill_pp_kernel<D, kBsRuntime>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return (int)e;
   const int total = p.n_items * p.batch;
   const int grid = total < num_sms_pp() ? total : num_sms_pp();
-  prefill_pp_kernel<D><<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, p);
+  kern<<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, p);
   return (int)cudaGetLastError();
 }
 
