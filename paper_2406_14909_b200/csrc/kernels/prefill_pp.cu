@@ -14,12 +14,13 @@
 //   warps 0-3  softmax of Q0 (thread t owns row t = TMEM lane t, all 128 S columns)
 //   warps 4-7  softmax of Q1
 //   warp 8     TMA producer of the K and V rings
-//   warp 9     TMEM allocator + MMA issuer (whole warp waits, one elected lane issues)
-//   warp 10    TMA producer of Q0 / Q1; warp 11 idle
+//   warp 9     TMEM allocator + MMA issue for Q0 (whole warp waits, one elected lane issues)
+//   warp 10    TMA producer of Q0 / Q1
+//   warp 11    MMA issue for Q1 (takes turns with warp 9)
 // setmaxnreg moves registers from warpgroup 2 (producers, MMA) to the softmax warpgroups.
 // TMEM (512 columns): S0 | S1 (fp32 128x128; P_j, bf16 packed, overwrites the first 64
 // columns of S_j once the softmax has it in registers) | O0 | O1 (fp32 128xD).
-// Per kv step the MMA warp issues  PV0(prev), S0(next), PV1(prev), S1(next):  while the
+// Per kv step the MMA warps issue  PV0(prev), S0(next), PV1(prev), S1(next) in turns:  while the
 // softmax of Q1 runs the tensor core computes Q0's products and vice versa, so the tensor
 // pipe never waits for one softmax.  tcgen05 ops of one thread execute in issue order and a
 // commit covers every earlier op, so S_j(t) complete implies PV_j(t-1) complete (O_j may be
@@ -45,7 +46,7 @@ using namespace ptx;
 constexpr int kM = 128;    // q rows per tile (MMA M)
 constexpr int kN = 128;    // keys per kv tile
 constexpr int kThreads = 384;  // warp 11 idles (warpgroup-aligned register reallocation)
-constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10, kSoftmaxWarp0 = 0;
+constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10, kWarpMMA1 = 11, kSoftmaxWarp0 = 0;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kPolyEvery = 4;              // pair c uses the polynomial iff c % kPolyEvery == kPolyEvery - 1
@@ -168,106 +169,127 @@ __device__ __forceinline__ void tmem_ld32_f(uint32_t taddr, float *x) {
 }
 
 // ------------------------------------------------------------------------------------------
-// MMA issuer (warp 9).  Per kv step: [PV0(prev)] [S0(t)] [PV1(prev)] [S1(t)].
+// MMA issue: warp 9 issues Q0's MMAs, warp 11 Q1's, taking turns.  Dispatch of a tcgen05.mma
+// is nearly synchronous for the issuing thread (~50-90 cycles per 128x128x16 MMA;
+// profiles/r01_microbench.txt), so with one issuing warp every barrier wait, commit and
+// loop instruction between dispatches is idle tensor time.  With two warps, warp j does its
+// waits (K(t), V(t-1), P_j, O_j drained) and bookkeeping while the other warp dispatches,
+// then takes the turn and dispatches [PV_j(t-1)] [S_j(t)] and hands the turn over (named
+// barriers 2 and 3 between the two warps: a bar.arrive / bar.sync pair per hand-over).
+// The strict alternation keeps the single-issuer order PV0, S0, PV1, S1 per step (the two
+// tiles ping-pong), and each tile's MMAs come from one thread, so S_j(t) complete =>
+// PV_j(t-1) complete (in-order tcgen05 execution + commits covering all earlier ops of the
+// thread).  K/V slots are released by one commit from each warp (barrier count 2); a warp
+// that does not use a step commits anyway (its commit only tracks its own MMAs).  Both warps
+// walk the same item and step sequence: one turn per used step plus one per item.
 // ------------------------------------------------------------------------------------------
+constexpr int kBarTurn0 = 2;  // named barriers: kBarTurn0 + j = "warp of tile j may dispatch"
+
 template <int D, int BS>
 __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_t tmem, uint32_t q_smem,
-                                         uint32_t k_smem, uint32_t v_smem, int total) {
+                                         uint32_t k_smem, uint32_t v_smem, int total, int j) {
   using C = PCfg<D>;
   constexpr uint32_t idesc_s = idesc_bf16_f32(kM, kN, false);
   constexpr uint32_t idesc_o = idesc_bf16_f32(kM, D, true);
-  const uint64_t qdesc0 = smem_desc_sw128(q_smem, 16, 1024);
+  const uint64_t adesc = smem_desc_sw128(q_smem + j * C::kTileBytes, 16, 1024);
   const uint64_t kdesc0 = smem_desc_sw128(k_smem, 16, 1024);
   const uint64_t vdesc0 = smem_desc_sw128(v_smem, C::kSlabBytes, 1024);
-  int T = 0;
-  int ks = 0, vs = 0, pvs = 0;  // K / V ring stage of the current step, V stage of the previous
-  uint32_t kph = 0, vph = 0, pvph = 0;
-  int pc[2] = {0, 0};  // P handshakes consumed per tile
-  int qc[2] = {0, 0};  // items started per tile
+  const uint32_t scol = tmem + (j ? 128u : 0u);  // S_j; P_j in its first 64 columns
+  const uint32_t ocol = tmem + (j ? C::kColO1 : C::kColO0);
+  int ks = 0, vs = 0;  // K / V ring stage of the current step
+  uint32_t kph = 0, vph = 0, pph = 0, qph = 0, oph = 0;
+  bool ostarted = false;
+  bool wait_turn = j == 1;  // warp 9 (Q0) dispatches first
+  auto take_turn = [&]() {
+    if (wait_turn) asm volatile("bar.sync %0, 64;" ::"r"(kBarTurn0 + j) : "memory");
+    wait_turn = true;
+  };
+  auto pass_turn = [&]() { asm volatile("bar.arrive %0, 64;" ::"r"(kBarTurn0 + (j ^ 1)) : "memory"); };
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
     const PItem it = get_pitem<BS>(p, idx);
-    const bool has1 = it.bt.has1;
-    mbar_wait_warp(smem_u32(&bars.q_full[0]), qc[0] & 1);
-    if (has1) mbar_wait_warp(smem_u32(&bars.q_full[1]), qc[1] & 1);
-    bool first[2] = {true, true};
-    bool pend[2] = {false, false};
-    int pT = -1, pt = -1;
-    int last_t[2];  // last kv tile of each q tile: its S releases Q_j, its PV completes O_j
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const TileRanges r = j ? it.bt.r[1] : it.bt.r[0];
-      last_t[j] = r.b1 > r.b0 ? r.b1 - 1 : r.a1 - 1;
+    const bool mine = j == 0 || it.bt.has1;  // this q tile has rows in the item
+    const TileRanges r = j ? it.bt.r[1] : it.bt.r[0];
+    const int last_t = r.b1 > r.b0 ? r.b1 - 1 : r.a1 - 1;  // its S releases Q_j, its PV completes O_j
+    if (mine) {
+      mbar_wait_warp(smem_u32(&bars.q_full[j]), qph);
+      qph ^= 1u;
     }
-    auto issue_pv = [&](int j, int vs) {  // V(prev) already waited for (v_full[vs])
-      mbar_wait_warp(smem_u32(&bars.p_full[j]), pc[j] & 1);
-      ++pc[j];
-      const bool fst = first[j];
-      if (fst && qc[j] > 0) mbar_wait_warp(smem_u32(&bars.o_empty[j]), (qc[j] - 1) & 1);
-      first[j] = false;
-      tc_fence_after();
-      const uint64_t vdesc = vdesc0 + (uint64_t)((vs * C::kTileBytes) >> 4);
-      const uint32_t pcol = tmem + (j ? 128u : 0u);
-      const uint32_t ocol = tmem + (j ? C::kColO1 : C::kColO0);
+    bool first = true, pend = false;
+    int pt = -1, pvs = 0;
+    uint32_t pvph = 0;
+    // PV_j of the previous step: V(prev), P_j(prev) and (first PV of an item) O_j drained
+    auto prepare_pv = [&]() {
+      mbar_wait_warp(smem_u32(&bars.v_full[pvs]), pvph);
+      mbar_wait_warp(smem_u32(&bars.p_full[j]), pph);
+      pph ^= 1u;
+      if (first && ostarted) {
+        mbar_wait_warp(smem_u32(&bars.o_empty[j]), oph);
+        oph ^= 1u;
+      }
+    };
+    auto dispatch_pv = [&]() {
+      const uint64_t vdesc = vdesc0 + (uint64_t)((pvs * C::kTileBytes) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < kN / 16; ++kk)
-          mma_ts(ocol, pcol + kk * 8, vdesc + (uint64_t)((kk * 2048) >> 4), idesc_o, (fst && kk == 0) ? 0u : 1u);
-        if (pt == last_t[j]) mma_commit(smem_u32(&bars.o_full[j]));  // tile j's epilogue may start
+          mma_ts(ocol, scol + kk * 8, vdesc + (uint64_t)((kk * 2048) >> 4), idesc_o, (first && kk == 0) ? 0u : 1u);
+        if (pt == last_t) mma_commit(smem_u32(&bars.o_full[j]));  // tile j's epilogue may start
       }
       __syncwarp();
-    };
-    auto issue_s = [&](int j, int ks, int t) {
-      const uint64_t adesc = qdesc0 + (uint64_t)((j * C::kTileBytes) >> 4);
-      const uint64_t bdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * C::kSlabBytes + (kk & 3) * 32) >> 4;
-          mma_ss(tmem + (j ? 128u : 0u), adesc + off, bdesc + off, idesc_s, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(smem_u32(&bars.s_full[j]));
-        if (t == last_t[j]) mma_commit(smem_u32(&bars.q_empty[j]));  // Q_j(next item) may load
-      }
-      __syncwarp();
+      first = false;
+      ostarted = true;
     };
     const int ns = it.bt.steps();
     for (int k = 0; k < ns; ++k) {
       int t;
-      bool u[2];
-      step_use(it.bt, k, t, u[0], u[1]);
-      if (!u[0] && !u[1]) continue;
-      mbar_wait_warp(smem_u32(&bars.k_full[ks]), kph);
-      if (pT >= 0) mbar_wait_warp(smem_u32(&bars.v_full[pvs]), pvph);  // V(prev): both PVs below
+      bool u0, u1;
+      step_use(it.bt, k, t, u0, u1);
+      if (!u0 && !u1) continue;
+      const bool use = mine && (j ? u1 : u0);
+      // ---- waits, overlapped with the other warp's dispatch
+      if (use) mbar_wait_warp(smem_u32(&bars.k_full[ks]), kph);
+      if (pend) prepare_pv();
+      take_turn();
       tc_fence_after();
+      if (pend) dispatch_pv();
+      if (use) {
+        const uint64_t bdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
+        if (elect_one()) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        if (pend[j]) issue_pv(j, pvs);
-        if (u[j]) issue_s(j, ks, t);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * C::kSlabBytes + (kk & 3) * 32) >> 4;
+            mma_ss(scol, adesc + off, bdesc + off, idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(smem_u32(&bars.s_full[j]));
+          if (t == last_t) mma_commit(smem_u32(&bars.q_empty[j]));  // Q_j(next item) may load
+        }
+        __syncwarp();
       }
+      pass_turn();
       if (elect_one()) {
-        if (pT >= 0) mma_commit(smem_u32(&bars.v_empty[pvs]));
+        if (pt >= 0) mma_commit(smem_u32(&bars.v_empty[pvs]));
         mma_commit(smem_u32(&bars.k_empty[ks]));
       }
       __syncwarp();
-      pend[0] = u[0];
-      pend[1] = u[1];
-      pT = T;
+      pend = use;
       pt = t;
       pvs = vs;
       pvph = vph;
       if (++ks == C::kNK) ks = 0, kph ^= 1u;
       if (++vs == C::kNV) vs = 0, vph ^= 1u;
-      ++T;
     }
-    mbar_wait_warp(smem_u32(&bars.v_full[pvs]), pvph);
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-      if (pend[j]) issue_pv(j, pvs);
-    if (elect_one()) mma_commit(smem_u32(&bars.v_empty[pvs]));
+    // trailing PV of the item (one turn per item for both warps, even without one)
+    if (pend) prepare_pv();
+    take_turn();
+    tc_fence_after();
+    if (pend) dispatch_pv();
+    pass_turn();
+    if (elect_one() && pt >= 0) mma_commit(smem_u32(&bars.v_empty[pvs]));
     __syncwarp();
-    ++qc[0];
-    if (has1) ++qc[1];
   }
+  // the other warp's last hand-over to this one is never taken: drain it, so the named
+  // barrier is clean for the next kernel on this SM
+  if (j == 0) asm volatile("bar.sync %0, 64;" ::"r"(kBarTurn0) : "memory");
 }
 
 // ------------------------------------------------------------------------------------------
@@ -441,11 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < C::kNK; ++s) {
       mbar_init(smem_u32(&bars.k_full[s]), 1);
-      mbar_init(smem_u32(&bars.k_empty[s]), 1);
+      mbar_init(smem_u32(&bars.k_empty[s]), 2);  // one commit per MMA warp
     }
     for (int s = 0; s < C::kNV; ++s) {
       mbar_init(smem_u32(&bars.v_full[s]), 1);
-      mbar_init(smem_u32(&bars.v_empty[s]), 1);
+      mbar_init(smem_u32(&bars.v_empty[s]), 2);
     }
     fence_mbar_init();
   }
@@ -518,8 +540,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kWarpMMA) {
-    mma_role<D, BS>(p, bars, tmem, q_smem, k_smem, v_smem, total);
+  } else if (warp == kWarpMMA || warp == kWarpMMA1) {
+    mma_role<D, BS>(p, bars, tmem, q_smem, k_smem, v_smem, total, warp == kWarpMMA ? 0 : 1);
   }
   }
 
