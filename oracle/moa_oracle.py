@@ -79,6 +79,8 @@ __all__ = [
     "visible_pairs_block",
     "attention_influence",
     "influence_blocks",
+    "rule_window_blocked",
+    "rule_losses",
 ]
 
 
@@ -402,4 +404,39 @@ def influence_blocks(Q, K, V, dO, tau: float, block: int):
                 for jb in range(nb):
                     blk = E[ib * block:(ib + 1) * block, jb * block:(jb + 1) * block]
                     out[b, h, ib, jb] = blk.sum() / blk.size
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Rule losses (Eq. 4) from the block-averaged influence
+# ---------------------------------------------------------------------------
+
+def rule_window_blocked(alpha: float, beta: float, N: int, n_sink: int, block: int) -> int:
+    """Window of a rule for the block mask: the span of Eq. 2 (clipped to
+    [0, N]) rounded up to a whole block (SPEC.md:200 ``span_of``), minus the
+    sinks; a multiple of ``block`` when ``n_sink`` is."""
+    span = span_of(alpha, beta, N)
+    span = -(-span // block) * block
+    return int(max(0, span - n_sink))
+
+
+def rule_losses(E_blocks: np.ndarray, alphas, betas, N: int, n_sink: int, block: int) -> np.ndarray:
+    """Delta L_{h,r} = sum_{i,j} M_{r,i,j} * Ebar_{h,i,j} (Eq. 4) with M the
+    masked (causal but invisible) positions of rule r's block mask at length N, evaluated on
+    the block-averaged influence ``E_blocks`` [H, nb, nb] (means over block x block pairs,
+    the ragged last block over its real pairs): a fully masked block contributes its mean
+    times its pair count, i.e. the token-level sum.  Returns [H, R] fp64."""
+    H, nb, _ = E_blocks.shape
+    out = np.zeros((H, len(alphas)))
+    for r, (a, b_) in enumerate(zip(alphas, betas)):
+        W = rule_window_blocked(a, b_, N, n_sink, block)
+        for ib in range(nb):
+            rows = min(block, N - ib * block)
+            for jb in range(ib + 1):
+                i_any, j_any = ib * block, jb * block   # block-mask visibility is per block
+                if visible_block(i_any + block - 1 if ib * block + block <= N else N - 1,
+                                 j_any, W, n_sink, block):
+                    continue
+                cols = min(block, N - jb * block)
+                out[:, r] += E_blocks[:, ib, jb] * rows * cols
     return out

@@ -386,3 +386,51 @@ def test_influence_gradient_is_chain_rule_of_o_equals_av():
     dO = torch.tensor(rng.standard_normal((N, d)))
     (dO * (A @ V)).sum().backward()
     assert torch.allclose(A.grad, dO @ V.T, atol=1e-12)
+
+
+# --- rule losses (Eq. 4) ---------------------------------------------------
+
+def _token_level_rule_loss(E_tok, W, s, b):
+    """Eq. 4 at token level: sum of E over the pairs the rule's block mask hides (direct
+    summation with the block predicate, independent of the block averaging)."""
+    N = E_tok.shape[0]
+    return sum(E_tok[i, j] for i in range(N) for j in range(i + 1) if not oracle.visible_block(i, j, W, s, b))
+
+
+def test_rule_losses_equal_token_level_sums():
+    """Block-averaged influence + Eq. 4 == token-level sum of E over the masked pairs
+    (SPEC.md:345 'sums over masks then multiply by block token counts'), ragged N."""
+    rng = np.random.default_rng(11)
+    B, N, H, d, b, s = 1, 22, 2, 4, 4, 4
+    Q, K, V, dO = (rng.standard_normal((B, N, H, d)) for _ in range(4))
+    E_blocks = oracle.influence_blocks(Q, K, V, dO, 0.7, b)[0]
+    alphas = [0.0, 4.0, 8.0, -8.0, 0.0]
+    betas = [0.25, 0.0, 0.5, 0.0, 1.0]
+    L = oracle.rule_losses(E_blocks, alphas, betas, N, s, b)
+    for h in range(H):
+        S = 0.7 * Q[0, :, h] @ K[0, :, h].T
+        A = np.zeros((N, N))
+        for i in range(N):
+            w = np.exp(S[i, :i + 1] - S[i, :i + 1].max())
+            A[i, :i + 1] = w / w.sum()
+        E_tok = oracle.attention_influence(A, dO[0, :, h] @ V[0, :, h].T)
+        for r, (a, be) in enumerate(zip(alphas, betas)):
+            W = oracle.rule_window_blocked(a, be, N, s, b)
+            assert abs(L[h, r] - _token_level_rule_loss(E_tok, W, s, b)) < 1e-12
+
+
+def test_rule_losses_full_rule_zero_and_nesting():
+    """the full-attention rule masks nothing (loss 0); a wider rule masks a
+    subset, so with Ebar >= 0 its loss is not larger."""
+    rng = np.random.default_rng(12)
+    H, N, b, s = 3, 200, 8, 8
+    nb = -(-N // b)
+    E = rng.random((H, nb, nb))
+    L = oracle.rule_losses(E, [0.0, 16.0, 64.0, 0.0], [1.0, 0.0, 0.0, 0.5], N, s, b)
+    assert np.all(L[:, 0] == 0.0)
+    assert np.all(L[:, 2] <= L[:, 1]) and np.all(L[:, 3] <= L[:, 1])
+    # sink-only rule (span <= s): every causal block outside the sink column is masked
+    Ls = oracle.rule_losses(E, [0.0], [0.0], N, s, b)
+    cnt = lambda i: min(b, N - i * b)
+    want = sum(E[:, ib, jb] * cnt(ib) * cnt(jb) for ib in range(nb) for jb in range(1, ib + 1))
+    assert np.allclose(Ls[:, 0], want, rtol=0, atol=1e-10)
