@@ -254,6 +254,25 @@ moa_status moa_attention_influence(const void *q, const void *k, const void *v, 
                                    int64_t q_row_stride, int64_t kv_row_stride, float scale, int block,
                                    float *e_blocks, int accumulate, moa_stream_t stream);
 
+/*
+ * Rule losses (Eq. 4): for every head h and
+ * candidate elastic rule r,  Delta L_{h,r} = sum_{i,j} M_{r,i,j} * Ebar_{h,i,j}  with M the
+ * positions the rule's block mask hides at length N (causal, invisible), evaluated on the
+ * block-averaged influence of moa_attention_influence: a hidden block adds its mean times
+ * its token-pair count (the token-level sum).  Rule windows: span = clamp(ceil(alpha +
+ * beta * N), 0, N) (Eq. 2) rounded up to a whole block, window = span -
+ * n_sink.
+ *   e_blocks  device fp32 [heads, nb, nb], nb = ceil(N / block) (one batch entry of
+ *             moa_attention_influence's output, averaged over calibration items).
+ *   alpha, beta  host arrays of n_rules (1 <= n_rules <= 128) rules.
+ *   n_sink    multiple of block; block 64.
+ *   loss_out  device fp32 [heads, n_rules].
+ * Stream-ordered, no allocation.
+ */
+moa_status moa_rule_losses(const float *e_blocks, int heads, int64_t N, int block, int n_sink,
+                           const float *alpha, const float *beta, int n_rules, float *loss_out,
+                           moa_stream_t stream);
+
 /* Prefill block-skip schedule (a2): the kv tiles (of MOA_TILE keys) that q-tile
  * `q_tile` (rows [q_tile*MOA_TILE, ...)) of local q-head h visits, in visit
  * order, with flags 1 = EDGE (needs the mask) / 0 = FULL.  *n_tiles is set

@@ -261,3 +261,50 @@ int launch_influence(const InfluenceArgs &a, void *stream) {
 }
 
 }  // namespace moa
+
+namespace moa {
+namespace {
+
+// ---- Eq. 4: rule losses from the block-averaged influence.
+// One CTA per (rule, head).  For query block ib the masked key blocks of the block mask are
+// sb <= jb <= ib - wb (sb = sink blocks, wb = window blocks; the whole causal row when the
+// window is 0 and ib >= sb); each contributes its mean times its pair count.
+__global__ void __launch_bounds__(256) rule_loss_kernel(const float *__restrict__ e_blocks, int nb, int64_t N,
+                                                        int block, const RuleWindows win, int sink_blocks,
+                                                        int n_rules, float *__restrict__ loss) {
+  const int r = blockIdx.x, h = blockIdx.y;
+  const int wb = win.blocks[r];
+  const float *E = e_blocks + (int64_t)h * nb * nb;
+  double acc = 0.0;
+  for (int ib = threadIdx.x; ib < nb; ib += blockDim.x) {
+    const int64_t rows = N - (int64_t)ib * block < block ? N - (int64_t)ib * block : block;
+    const int hi = ib - wb;  // last masked key block (inclusive)
+    double row = 0.0;
+    for (int jb = sink_blocks; jb <= hi; ++jb) {
+      const int64_t cols = N - (int64_t)jb * block < block ? N - (int64_t)jb * block : block;
+      row += (double)E[(int64_t)ib * nb + jb] * (double)cols;
+    }
+    acc += row * (double)rows;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss[(int64_t)h * n_rules + r] = (float)red[0];
+}
+
+}  // namespace
+
+int launch_rule_losses(const float *e_blocks, int heads, int64_t N, int block, const RuleWindows &win,
+                       int sink_blocks, int n_rules, float *loss, void *stream) {
+  const int nb = (int)((N + block - 1) / block);
+  dim3 grid((unsigned)n_rules, (unsigned)heads);
+  rule_loss_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(e_blocks, nb, N, block, win, sink_blocks, n_rules,
+                                                          loss);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace moa

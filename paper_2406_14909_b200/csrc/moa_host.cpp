@@ -790,6 +790,29 @@ moa_status moa_attention_influence(const void *q, const void *k, const void *v, 
   return ok();
 }
 
+moa_status moa_rule_losses(const float *e_blocks, int heads, int64_t N, int block, int n_sink,
+                           const float *alpha, const float *beta, int n_rules, float *loss_out,
+                           moa_stream_t stream) {
+  if (!e_blocks || !alpha || !beta || !loss_out) return fail(MOA_ERR_INVALID_ARG, "NULL pointer");
+  if (heads < 1 || N < 1 || N > (int64_t(1) << 31)) return fail(MOA_ERR_INVALID_ARG, "bad heads / N");
+  if (block != 64) return fail(MOA_ERR_UNSUPPORTED, "block %d: only the paper's 64 is implemented", block);
+  if (n_sink < 0 || n_sink % block) return fail(MOA_ERR_INVALID_ARG, "n_sink %d not a multiple of block", n_sink);
+  if (n_rules < 1 || n_rules > moa::kMaxRules)
+    return fail(MOA_ERR_INVALID_ARG, "n_rules %d not in [1, %d]", n_rules, moa::kMaxRules);
+  moa::RuleWindows win{};
+  for (int r = 0; r < n_rules; ++r) {
+    double sp = std::ceil((double)alpha[r] + (double)beta[r] * (double)N);
+    if (!(sp == sp)) return fail(MOA_ERR_INVALID_ARG, "NaN rule %d", r);
+    sp = std::min(std::max(sp, 0.0), (double)N);
+    int64_t span = ((int64_t)sp + block - 1) / block * block;
+    int64_t w = std::max<int64_t>(0, span - n_sink);
+    win.blocks[r] = (int32_t)(w / block);
+  }
+  int e = moa::launch_rule_losses(e_blocks, heads, N, block, win, n_sink / block, n_rules, loss_out, stream);
+  if (e) return cuda_fail((cudaError_t)e, "rule loss launch");
+  return ok();
+}
+
 moa_status moa_prefill_items(const moa_ctx *ctx, int layer, int32_t *items, int max_items,
                              int32_t *n_items) {
   moa_status st = check_layer(ctx, layer, true);

@@ -282,6 +282,13 @@ struct InfluenceArgs {
   int accumulate;
 };
 int launch_influence(const InfluenceArgs &a, void *stream);
+// Eq. 4 rule losses: window of every rule in blocks (passed by value, <= kMaxRules rules)
+constexpr int kMaxRules = 128;
+struct RuleWindows {
+  int32_t blocks[kMaxRules];
+};
+int launch_rule_losses(const float *e_blocks, int heads, int64_t N, int block, const RuleWindows &win,
+                       int sink_blocks, int n_rules, float *loss, void *stream);
 
 // TMA tensor map over a [rows, d] bf16 cache (box box_rows x 64 cols, 128B swizzle).
 bool encode_cache_map(void *map_out, const void *ptr, int d, int64_t rows, int box_rows);

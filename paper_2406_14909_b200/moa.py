@@ -64,6 +64,21 @@ def attention_influence(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, dout:
     return out
 
 
+def rule_losses(e_blocks: torch.Tensor, N: int, n_sink: int, alphas: Sequence[float], betas: Sequence[float],
+                block: int = 64, stream=None) -> torch.Tensor:
+    """Eq. 4 rule losses [heads, n_rules] (fp32, device) from one entry [heads, nb, nb] of
+    attention_influence's output through ``moa_rule_losses``."""
+    if e_blocks.dtype != torch.float32 or not e_blocks.is_contiguous() or e_blocks.dim() != 3:
+        raise MoAError(1, "rule_losses", "e_blocks must be a contiguous fp32 [heads, nb, nb] tensor")
+    n = len(alphas)
+    a = (c_float * n)(*alphas)
+    b = (c_float * n)(*betas)
+    out = torch.empty(e_blocks.shape[0], n, dtype=torch.float32, device=e_blocks.device)
+    check(_lib.lib().moa_rule_losses(_ptr(e_blocks), e_blocks.shape[0], int(N), int(block), int(n_sink), a, b, n,
+                                     _ptr(out), _stream(stream)), "moa_rule_losses")
+    return out
+
+
 class MoAContext:
     """One context per (process, device): span tables, cache layout, launches."""
 

@@ -68,3 +68,20 @@ def test_influence_peaked_rows(moa, scale):
     got, ref = _run(moa, 1, 160, 2, 2, 64, 800, scale=scale)
     assert np.isfinite(got).all()
     assert np.abs(got - ref).max() <= 1e-3 * np.abs(ref).max() + 1e-6, (np.abs(got - ref).max(), np.abs(ref).max())
+
+
+def test_rule_losses_match_oracle(moa):
+    """Eq. 4 on the GPU from the kernel's own influence blocks vs the oracle's Eq. 4 on the same
+    blocks (fp64), over the paper's 6 x 9 rule grid at N = 1000 (ragged)."""
+    from moa_workloads import ALPHA_GRID, BETA_GRID
+    dev = torch.device("cuda")
+    B, N, H, d, s = 1, 1000, 3, 64, 64
+    q, k, v, do = (normal((B, N, H, d), 900 + i, torch.bfloat16).to(dev) for i in range(4))
+    e = moa.attention_influence(q, k, v, do, 1 / math.sqrt(d))
+    alphas = [a for a in ALPHA_GRID for _ in BETA_GRID]
+    betas = [b for _ in ALPHA_GRID for b in BETA_GRID]
+    alphas = [a / 8 for a in alphas]                       # spans at N = 1000 cover short and long windows
+    got = f64(moa.rule_losses(e[0].contiguous(), N, s, alphas, betas))
+    ref = oracle.rule_losses(f64(e[0]), alphas, betas, N, s, 64)
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max() + 1e-7
+    assert np.all(got[:, [i for i, (a, b) in enumerate(zip(alphas, betas)) if a + b * N >= N]] == 0.0)
