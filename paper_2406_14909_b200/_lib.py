@@ -57,6 +57,8 @@ _SIGS = [
     ("moa_next_pos", c_int, [_P, c_int, POINTER(c_int64)]),
     ("moa_attention_influence", c_int, [_P, _P, _P, _P, c_int, c_int64, c_int, c_int, c_int, c_int64, c_int64,
                                         c_float, c_int, _P, c_int, _P]),
+    ("moa_plan_rules", c_int, [POINTER(c_float), POINTER(c_float), c_int, c_int, c_int, c_float, c_int,
+                               POINTER(c_int32), POINTER(c_float), POINTER(c_float)]),
     ("moa_rule_losses", c_int, [_P, c_int, c_int64, c_int, c_int, POINTER(c_float), POINTER(c_float), c_int, _P,
                                 _P]),
 ]

@@ -813,6 +813,97 @@ moa_status moa_rule_losses(const float *e_blocks, int heads, int64_t N, int bloc
   return ok();
 }
 
+// ---- rule selection (Eq. 5): Lagrangian relaxation of the density budget.
+// For a price lam >= 0 every layer independently picks the subset S of at most k rules and the
+// per-head choice in S minimising sum_h (loss[h][r] + lam * density[r]); the mean density of
+// that plan falls as lam grows.  The smallest lam (bisection) whose plan meets the budget is
+// returned: it minimises loss + lam * density over all plans, so no plan of equal or lower
+// density has a lower loss.
+namespace {
+
+struct PlanEval {
+  double loss = 0.0, dens = 0.0;
+};
+
+PlanEval plan_at(const float *loss, const float *density, int layers, int hpl, int R, int k, double lam,
+                 int32_t *choice) {
+  PlanEval ev;
+  std::vector<int32_t> best_pick(hpl), pick(hpl);
+  for (int l = 0; l < layers; ++l) {
+    const float *L = loss + (size_t)l * hpl * R;
+    double best = INFINITY, best_loss = 0.0, best_d = 0.0;
+    auto try_subset = [&](int a, int b) {
+      double c = 0.0, cl = 0.0, cd = 0.0;
+      for (int h = 0; h < hpl; ++h) {
+        const double va = L[(size_t)h * R + a] + lam * density[a];
+        int r = a;
+        if (b >= 0) {
+          const double vb = L[(size_t)h * R + b] + lam * density[b];
+          if (vb < va || (vb == va && density[b] < density[a])) r = b;
+        }
+        pick[h] = r;
+        c += L[(size_t)h * R + r] + lam * density[r];
+        cl += L[(size_t)h * R + r];
+        cd += density[r];
+      }
+      if (c < best || (c == best && cd < best_d)) {
+        best = c, best_loss = cl, best_d = cd;
+        best_pick = pick;
+      }
+    };
+    for (int a = 0; a < R; ++a) {
+      try_subset(a, -1);
+      if (k >= 2)
+        for (int b = a + 1; b < R; ++b) try_subset(a, b);
+    }
+    ev.loss += best_loss;
+    ev.dens += best_d;
+    if (choice) std::copy(best_pick.begin(), best_pick.end(), choice + (size_t)l * hpl);
+  }
+  ev.dens /= (double)layers * hpl;
+  return ev;
+}
+
+}  // namespace
+
+moa_status moa_plan_rules(const float *loss, const float *density, int layers, int heads_per_layer, int n_rules,
+                          float density_budget, int max_rules_per_layer, int32_t *rule_out, float *loss_out,
+                          float *density_out) {
+  if (!loss || !density || !rule_out) return fail(MOA_ERR_INVALID_ARG, "NULL pointer");
+  if (layers < 1 || heads_per_layer < 1 || n_rules < 1) return fail(MOA_ERR_INVALID_ARG, "empty instance");
+  if (max_rules_per_layer != 1 && max_rules_per_layer != 2)
+    return fail(MOA_ERR_UNSUPPORTED, "max_rules_per_layer %d: 1 or 2 (the paper's limit, PAPER.md:384)",
+                max_rules_per_layer);
+  for (int r = 0; r < n_rules; ++r)
+    if (!(density[r] >= 0.f && density[r] <= 1.f)) return fail(MOA_ERR_INVALID_ARG, "density[%d] not in [0,1]", r);
+  const int H = layers * heads_per_layer, k = max_rules_per_layer;
+  const float dmin = *std::min_element(density, density + n_rules);
+  if (dmin > density_budget)
+    return fail(MOA_ERR_INVALID_ARG, "infeasible: the sparsest rule has density %.4f > budget %.4f", dmin,
+                density_budget);
+  PlanEval ev = plan_at(loss, density, layers, heads_per_layer, n_rules, k, 0.0, rule_out);
+  if (ev.dens > density_budget) {
+    double lo = 0.0, hi = 1.0;
+    while (plan_at(loss, density, layers, heads_per_layer, n_rules, k, hi, nullptr).dens > density_budget) {
+      lo = hi;
+      hi *= 2.0;
+      if (hi > 1e30) return fail(MOA_ERR_INVALID_ARG, "no price meets the density budget");
+    }
+    for (int it = 0; it < 100 && hi - lo > 1e-12 * hi; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (plan_at(loss, density, layers, heads_per_layer, n_rules, k, mid, nullptr).dens > density_budget)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    ev = plan_at(loss, density, layers, heads_per_layer, n_rules, k, hi, rule_out);
+  }
+  (void)H;
+  if (loss_out) *loss_out = (float)ev.loss;
+  if (density_out) *density_out = (float)ev.dens;
+  return ok();
+}
+
 moa_status moa_prefill_items(const moa_ctx *ctx, int layer, int32_t *items, int max_items,
                              int32_t *n_items) {
   moa_status st = check_layer(ctx, layer, true);

@@ -79,6 +79,22 @@ def rule_losses(e_blocks: torch.Tensor, N: int, n_sink: int, alphas: Sequence[fl
     return out
 
 
+def plan_rules(loss, density, layers: int, heads_per_layer: int, density_budget: float, max_rules_per_layer: int = 2):
+    """One rule per head under the density budget (``moa_plan_rules``).  loss: [H, R] host
+    array-like (H = layers * heads_per_layer), density: [R].  Returns (rules [H], loss, density)."""
+    import numpy as np
+    L = np.ascontiguousarray(np.asarray(loss, dtype=np.float32))
+    d = np.ascontiguousarray(np.asarray(density, dtype=np.float32))
+    H, R = L.shape
+    assert H == layers * heads_per_layer and d.shape == (R,)
+    out = (c_int32 * H)()
+    lo, do = c_float(), c_float()
+    check(_lib.lib().moa_plan_rules(L.ctypes.data_as(ctypes.POINTER(c_float)), d.ctypes.data_as(ctypes.POINTER(c_float)),
+                                    layers, heads_per_layer, R, float(density_budget), int(max_rules_per_layer), out,
+                                    byref(lo), byref(do)), "moa_plan_rules")
+    return list(out), lo.value, do.value
+
+
 class MoAContext:
     """One context per (process, device): span tables, cache layout, launches."""
 

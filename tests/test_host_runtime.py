@@ -204,3 +204,48 @@ def test_block_mode_validation(moa):
     with pytest.raises(MoAError, match="INVALID_ARG"):
         c.set_spans(0, [64, 64, 64, 64], 32, 1000, block=64)    # sinks not a multiple
     c.set_spans(0, [64, 128, 0, 1024], 64, 1000, block=64)
+
+
+# --- rule selection (Eq. 5; SPEC.md plan_optimizer) -----------------------
+
+def test_plan_rules_spec_examples(moa):
+    """SPEC.md solve_single examples: 1 head -> the only feasible rule (loss 5); 2 heads x 2
+    rules at budget 0.75 -> h1 keeps rule 1, h2 takes rule 2 (loss 1, density 0.75)."""
+    assert moa.plan_rules([[0, 5]], [1.0, 0.5], 1, 1, 0.5) == ([1], 5.0, 0.5)
+    assert moa.plan_rules([[0, 3], [0, 1]], [1.0, 0.5], 1, 2, 0.75) == ([0, 1], 1.0, 0.75)
+
+
+def _enumerate(loss, dens, layers, hpl, k):
+    import itertools
+    H, R = loss.shape
+    for plan in itertools.product(range(R), repeat=H):
+        if any(len(set(plan[l * hpl:(l + 1) * hpl])) > k for l in range(layers)):
+            continue
+        yield plan, float(sum(loss[h, r] for h, r in enumerate(plan))), float(np.mean([dens[r] for r in plan]))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_plan_rules_is_optimal_at_its_density(moa, seed):
+    """Brute force over every plan (<= 2 layers x 2 heads, <= 4 rules): the returned plan meets
+    the budget and the per-layer rule limit, and no plan of equal or lower density has a lower
+    loss (the Lagrangian optimality the solver guarantees); when the budget is slack the
+    returned plan is the unconstrained optimum."""
+    rng = np.random.default_rng(seed)
+    layers, hpl, R = int(rng.integers(1, 3)), 2, int(rng.integers(2, 5))
+    H = layers * hpl
+    dens = np.sort(rng.random(R)).astype(np.float32)
+    loss = (rng.random((H, R)) * (1.0 - dens)[None, :] * 10).astype(np.float32)   # sparser rule, larger loss
+    budget = float(rng.uniform(dens.min(), dens.max()))
+    k = int(rng.integers(1, 3))
+    plan, L, D = moa.plan_rules(loss, dens, layers, hpl, budget, k)
+    assert D <= budget + 1e-6
+    for l in range(layers):
+        assert len(set(plan[l * hpl:(l + 1) * hpl])) <= k
+    assert abs(L - sum(loss[h, r] for h, r in enumerate(plan))) < 1e-4
+    assert abs(D - np.mean([dens[r] for r in plan])) < 1e-6
+    for p, Lp, Dp in _enumerate(loss.astype(np.float64), dens.astype(np.float64), layers, hpl, k):
+        if Dp <= D + 1e-9:
+            assert Lp >= L - 1e-4, (p, Lp, Dp, plan, L, D)
+    best_free = min(Lp for _, Lp, _ in _enumerate(loss.astype(np.float64), dens.astype(np.float64), layers, hpl, k))
+    if budget >= dens.max():
+        assert abs(L - best_free) < 1e-4
