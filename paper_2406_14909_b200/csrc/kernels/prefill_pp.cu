@@ -49,7 +49,10 @@ constexpr int kThreads = 384;  // warp 11 idles (warpgroup-aligned register real
 constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10, kWarpMMA1 = 11, kSoftmaxWarp0 = 0;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr int kPolyEvery = 4;              // pair c uses the polynomial iff c % kPolyEvery == kPolyEvery - 1
+#ifndef MOA_PP_POLY_EVERY
+#define MOA_PP_POLY_EVERY 4
+#endif
+constexpr int kPolyEvery = MOA_PP_POLY_EVERY;  // pair c uses the polynomial iff c % kPolyEvery == kPolyEvery - 1
 constexpr int kSoftmaxWarpsPerTile = 4;
 
 template <int D>
@@ -185,6 +188,20 @@ __device__ __forceinline__ void tmem_ld32_f(uint32_t taddr, float *x) {
 // ------------------------------------------------------------------------------------------
 constexpr int kBarTurn0 = 2;  // named barriers: kBarTurn0 + j = "warp of tile j may dispatch"
 
+// diagnostic build (-DMOA_PP_DIAG_TRACE, tools/trace_pp.py): (tag, clock64) events of CTA 0
+#ifdef MOA_PP_DIAG_TRACE
+__device__ unsigned long long g_pp_trace[4][4096];
+__device__ int g_pp_trace_n[4];
+#define PPTR(role, tag)                                                                          \
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) {                                              \
+    if (trn_ < 4096) g_pp_trace[role][trn_] = ((unsigned long long)(tag) << 56) | (unsigned long long)clock64(); \
+    ++trn_;                                                                                      \
+    g_pp_trace_n[role] = trn_ < 4096 ? trn_ : 4096;                                              \
+  }
+#else
+#define PPTR(role, tag) {}
+#endif
+
 template <int D, int BS>
 __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_t tmem, uint32_t q_smem,
                                          uint32_t k_smem, uint32_t v_smem, int total, int j) {
@@ -200,11 +217,18 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
   uint32_t kph = 0, vph = 0, pph = 0, qph = 0, oph = 0;
   bool ostarted = false;
   bool wait_turn = j == 1;  // warp 9 (Q0) dispatches first
+  int trn_ = 0;
+  (void)trn_;
   auto take_turn = [&]() {
+    PPTR(j ? 3 : 0, 1)
     if (wait_turn) asm volatile("bar.sync %0, 64;" ::"r"(kBarTurn0 + j) : "memory");
     wait_turn = true;
+    PPTR(j ? 3 : 0, 2)
   };
-  auto pass_turn = [&]() { asm volatile("bar.arrive %0, 64;" ::"r"(kBarTurn0 + (j ^ 1)) : "memory"); };
+  auto pass_turn = [&]() {
+    PPTR(j ? 3 : 0, 3)
+    asm volatile("bar.arrive %0, 64;" ::"r"(kBarTurn0 + (j ^ 1)) : "memory");
+  };
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
     const PItem it = get_pitem<BS>(p, idx);
     const bool mine = j == 0 || it.bt.has1;  // this q tile has rows in the item
@@ -304,6 +328,8 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
   const uint32_t scol = tmem + lane_off + (j ? 128u : 0u);
   const uint32_t ocol = tmem + lane_off + (j ? C::kColO1 : C::kColO0);
   const uint64_t sl2 = f2pk(p.scale_log2, p.scale_log2);
+  int trn_ = 0;
+  (void)trn_;
   int sc = 0;  // S handshakes of this tile
   int ic = 0;  // items of this tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
@@ -325,6 +351,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       const bool full = kv_tile_full(ti0, ti1, t, it.W, p.n_sink, bshift_of<BS>(p));
       mbar_wait_warp(smem_u32(&bars.s_full[j]), sc & 1);
       ++sc;
+      if ((warp & 3) == 0) PPTR(1 + j, 40)
       tc_fence_after();
       float x[kN];
 #pragma unroll
@@ -404,6 +431,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&bars.p_full[j]));
+      if ((warp & 3) == 0) PPTR(1 + j, 41)
     }
     // epilogue: O_j / l -> bf16 rows, lse
     mbar_wait_warp(smem_u32(&bars.o_full[j]), ic & 1);
@@ -600,6 +628,17 @@ int launch_pp(const PrefillArgs &a, void *stream) {
 }
 
 }  // namespace
+
+#ifdef MOA_PP_DIAG_TRACE
+extern "C" int moa_debug_pp_trace(unsigned long long *out, int *counts) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_pp_trace, sizeof(g_pp_trace));
+  cudaMemcpyFromSymbol(counts, g_pp_trace_n, sizeof(g_pp_trace_n));
+  static const int z[4] = {};
+  cudaMemcpyToSymbol(g_pp_trace_n, z, sizeof(z));
+  return 0;
+}
+#endif
 
 int launch_prefill_bf16_pp(const PrefillArgs &a, void *stream) {
   if (a.d == 128) return launch_pp<128>(a, stream);

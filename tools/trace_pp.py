@@ -16,8 +16,8 @@ import paper_2406_14909_b200 as moa  # noqa: E402
 from paper_2406_14909_b200 import _lib  # noqa: E402
 from moa_workloads import CONFIGS, prefill_qkv, rule_table  # noqa: E402
 
-TAGS = {1: "mma k_full ok", 2: "mma v_full ok", 3: "mma before v/k_empty commits", 4: "mma after commits",
-        5: "mma before k_full wait", 10: "mma p_full0 ok", 11: "mma p_full1 ok", 20: "mma PV0 issued", 21: "mma PV1 issued",
+TAGS = {1: "waits done, wait for turn", 2: "turn taken", 3: "dispatch done, pass turn", 4: "-",
+        5: "-", 10: "mma p_full0 ok", 11: "mma p_full1 ok", 20: "mma PV0 issued", 21: "mma PV1 issued",
         30: "mma S0 issued", 31: "mma S1 issued", 40: "sm s_full seen", 41: "sm p_full arrive"}
 
 
