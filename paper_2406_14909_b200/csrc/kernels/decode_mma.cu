@@ -88,7 +88,8 @@ struct MParams {
   const __nv_bfloat16 *k_new, *v_new;
   int64_t kv_bs;
   __nv_bfloat16 *kc, *vc;
-  int64_t rows_per_seq, R, rpc;  // total rows, rows per CTA
+  int64_t rows_per_seq, R;       // rows per sequence, total rows
+  int64_t seg_cost, ctot;        // CTA split: a segment costs seg_cost rows; total cost
   const int64_t *g_off;
   const int32_t *win_g, *win_q;
   int ngl, G, n_sink, batch;
@@ -102,6 +103,37 @@ struct MParams {
   int trace_slot;
 #endif
 };
+
+// Work split (balanced by cost, not rows): row x of region r (regions in (b, g) row order) sits
+// at cost position C(x) = x + seg_cost * r, C_tot = R + seg_cost * (regions - 1); CTA c takes
+// the rows with ceil(c C_tot / n) <= C(x) < ceil((c+1) C_tot / n).  A CTA whose range
+// crosses region boundaries thus gets seg_cost fewer rows per extra segment (each segment
+// costs it a q stage, a partial tile and a partial write), and cuts that fall in the jump
+// between two regions land on the region boundary.
+__device__ __forceinline__ int64_t region_start(const MParams &p, const int64_t *g_off, int r) {
+  const int b = r / p.ngl, g = r - b * p.ngl;
+  return (int64_t)b * p.rows_per_seq + g_off[g];
+}
+// smallest row x with C(x) >= T
+__device__ __forceinline__ int64_t cut_row(const MParams &p, const int64_t *g_off, int64_t T) {
+  const int nreg = p.batch * p.ngl;
+  int lo = 0, hi = nreg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (region_start(p, g_off, mid) + p.seg_cost * mid <= T)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const int64_t st = region_start(p, g_off, lo);
+  const int64_t en = lo + 1 < nreg ? region_start(p, g_off, lo + 1) : p.R;
+  const int64_t x = st + (T - (st + p.seg_cost * lo));
+  return x < en ? x : en;
+}
+// the CTA whose range holds row x of region r
+__device__ __forceinline__ int64_t cta_of(const MParams &p, int64_t x, int r) {
+  return ((x + p.seg_cost * r) * (int64_t)gridDim.x) / p.ctot;
+}
 
 struct Region {
   int b, g, Wg;
@@ -185,7 +217,7 @@ __device__ __forceinline__ void combine_region_warp(const MParams &p, const int6
   const int G = p.G;
   const int64_t start = (int64_t)b * p.rows_per_seq + g_off[g];
   const int64_t end = start + p.n_sink + win_g[g];
-  const int64_t c_first = start / p.rpc, c_last = (end - 1) / p.rpc;
+  const int64_t c_first = cta_of(p, start, ridx), c_last = cta_of(p, end - 1, ridx);
   const int64_t sl0 = c_first + ridx;
   const int nsl = (int)(c_last - c_first + 1);
   for (int j = 0; j < G; ++j) {
@@ -248,8 +280,6 @@ __global__ void __launch_bounds__(kThreads, CPS)
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   // per-warp partials of the two segments in flight: [2][kCW][G][D + 4] fp32 after the tiles
   float *s_part = reinterpret_cast<float *>(smem_raw + (base - smem_u32(smem_raw)) + C::kStages * 2 * C::kTileBytes);
-  const int64_t X0 = (int64_t)blockIdx.x * p.rpc;
-  const int64_t X1 = X0 + p.rpc < p.R ? X0 + p.rpc : p.R;
   if (tid == 0) TRACE(0);
 
   if (tid == 0) {
@@ -264,6 +294,9 @@ __global__ void __launch_bounds__(kThreads, CPS)
     s_wing[g] = p.win_g[g];
   }
   __syncthreads();
+  const int64_t n_cta = gridDim.x;
+  const int64_t X0 = cut_row(p, s_goff, ((int64_t)blockIdx.x * p.ctot + n_cta - 1) / n_cta);
+  const int64_t X1 = cut_row(p, s_goff, ((int64_t)(blockIdx.x + 1) * p.ctot + n_cta - 1) / n_cta);
   // Programmatic dependent launch.  Everything above overlapped the previous kernel's tail.
   // The consumers and the epilogue warp wait for the stream predecessor (q, k_new, the
   // workspace, the tickets and o may be its inputs/outputs) before they trigger the next
@@ -389,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
       int last = 0;
       if (lane == 0) {
         __threadfence();  // cumulative: orders the consumers' partials before the ticket
-        const int64_t c_first = rg.start / p.rpc, c_last = (rg.end - 1) / p.rpc;
+        const int64_t c_first = cta_of(p, rg.start, ridx), c_last = cta_of(p, rg.end - 1, ridx);
         int *ctr = p.counters + ridx;
         const int ticket = atomicAdd(ctr, 1);
         if (ticket == (int)(c_last - c_first)) {
@@ -707,7 +740,12 @@ int launch_v(const DecodeMmaArgs &a, void *stream) {
   p.rows_per_seq = a.rows_per_seq;
   p.R = (int64_t)a.batch * a.rows_per_seq;
   const int n = ctas_for(p.R, CPS);
-  p.rpc = (p.R + n - 1) / n;
+  static const int64_t seg_cost = [] {
+    const char *e = std::getenv("MOA_DEC_SEG_COST");  // tuning override
+    return e ? (int64_t)std::atoll(e) : (int64_t)128;
+  }();
+  p.seg_cost = seg_cost;
+  p.ctot = p.R + seg_cost * ((int64_t)a.batch * a.ngl - 1);
   p.g_off = a.d_g_off;
   p.win_g = a.d_win_g;
   p.win_q = a.d_win_q;
