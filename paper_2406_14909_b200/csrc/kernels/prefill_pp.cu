@@ -53,7 +53,12 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define MOA_PP_POLY_EVERY 4
 #endif
 constexpr int kPolyEvery = MOA_PP_POLY_EVERY;  // pair c uses the polynomial iff c % kPolyEvery == kPolyEvery - 1
-constexpr int kSoftmaxWarpsPerTile = 4;
+// token mask: a q tile's softmax runs on its own 4 warps (full rows); block masks: all 8 softmax
+// warps work on both tiles, half the columns each (softmax_split_role) -- the block mask's
+// extra EDGE tiles made the 4-warp softmax the longer pole (+9 % on C4 with block 64)
+template <int BS>
+constexpr int softmax_warps_per_tile() { return BS >= 0 ? 8 : 4; }
+constexpr int kBarPair0 = 4;  // named barriers 4..7: warps q and q + 4 (rows 32q..32q+31), split softmax
 
 template <int D>
 struct PCfg {
@@ -65,7 +70,7 @@ struct PCfg {
 #endif
   static constexpr int kNK = D == 128 ? MOA_PP_NK128 : 6;
   static constexpr int kNV = D == 128 ? 5 - MOA_PP_NK128 : 4;
-  static constexpr int kSmemBytes = (2 + kNK + kNV) * kTileBytes + 1024;
+  static constexpr int kSmemBytes = (2 + kNK + kNV) * kTileBytes;  // base 1024-aligned (see kernel)
   static constexpr uint32_t kColO0 = 256, kColO1 = 256 + D;
 };
 
@@ -466,15 +471,194 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// softmax (warps 0-7): warp w owns rows 32 (w & 3) .. +31 (its TMEM lanes) and column half
+// hf = w >> 2 of BOTH q tiles, in the order the tensor core completes them (S0(t), S1(t)).
+// The two warps of a row block (w, w ^ 4) exchange their half-row max (and at the end their
+// half-row sums) through shared memory and a named barrier.  Eight warps per tile halve the
+// per-thread work of a tile's softmax, which bounds the ping-pong: one tile's softmax must
+// fit under the other tile's MMAs.
+// ------------------------------------------------------------------------------------------
+template <int D, int BS>
+__device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bars, uint32_t tmem, int total, int warp,
+                                             int lane, float (*red)[2][kM]) {
+  using C = PCfg<D>;
+  constexpr int kCols = kN / 2;   // S columns of this warp per tile
+  constexpr int kOCols = D / 2;   // O columns of this warp per tile
+  const int hf = warp >> 2;
+  const int row = (warp & 3) * 32 + lane;
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+  const int bar_pair = kBarPair0 + (warp & 3);
+  auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_pair) : "memory"); };
+  const uint64_t sl2 = f2pk(p.scale_log2, p.scale_log2);
+  int trn_ = 0;
+  (void)trn_;
+  int sc[2] = {0, 0};  // S handshakes per tile
+  int ic[2] = {0, 0};  // items per tile
+  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+    const PItem it = get_pitem<BS>(p, idx);
+    const bool has1 = it.bt.has1;
+    float m_used[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+    const int ns = it.bt.steps();
+    for (int k = 0; k < ns; ++k) {
+      int t;
+      bool u[2];
+      step_use(it.bt, k, t, u[0], u[1]);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (!u[j]) continue;
+        const int64_t ti0 = it.i0 + j * kM;                         // first row of this q tile
+        const int64_t ti1 = (ti0 + kM < p.N ? ti0 + kM : p.N) - 1;  // last real row
+        const int64_t i = ti0 + row;
+        const int64_t j0 = (int64_t)t * kN + hf * kCols;  // key of this warp's first column
+        const uint32_t sbase = tmem + lane_off + (j ? 128u : 0u);
+        const uint32_t ocol = tmem + lane_off + (j ? C::kColO1 : C::kColO0) + hf * kOCols;
+        const bool full = kv_tile_full(ti0, ti1, t, it.W, p.n_sink, bshift_of<BS>(p));
+        mbar_wait_warp(smem_u32(&bars.s_full[j]), sc[j] & 1);
+        ++sc[j];
+        if (warp == 0) PPTR(1 + j, 40)
+        tc_fence_after();
+        float x[kCols];
+#pragma unroll
+        for (int c = 0; c < kCols / 32; ++c) tmem_ld32_f(sbase + hf * kCols + c * 32, &x[c * 32]);
+        tmem_wait_ld();
+        if (!full) {
+          const int64_t lo_i = BS >= 0 ? (it.W > 0 ? win_lo(i, it.W, bshift_of<BS>(p)) : i + 1) : i - it.W + 1;
+          // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  j0+c >= lo_i)
+          const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0), lo = (int)(lo_i - j0) - 1;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) {
+            const bool vis = c <= dd && (c < sk || c > lo);
+            if (!vis) x[c] = -INFINITY;
+          }
+        }
+        float mx[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) mx[a] = fmaxf(x[a], x[a + 8]);
+#pragma unroll
+        for (int c = 16; c < kCols; c += 16)
+#pragma unroll
+          for (int a = 0; a < 8; a += 2) {
+            mx[a] = fmax3(mx[a], x[c + a], x[c + a + 8]);
+            mx[a + 1] = fmax3(mx[a + 1], x[c + a + 1], x[c + a + 9]);
+          }
+        float rmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
+        // row max of both halves.  red[j][hf] is rewritten only after the next s_full of tile j,
+        // which follows the partner's p_full arrival, i.e. its read below.  The barrier also
+        // orders the partner's S load before our P store over its columns.
+        red[j][hf][row] = rmax;
+        pair_sync();
+        rmax = fmaxf(rmax, red[j][hf ^ 1][row]);
+        const float mt = rmax * p.scale_log2;
+        bool rescale = false;
+        float alpha = 1.f;
+        if (m_used[j] == -INFINITY) {
+          m_used[j] = mt;  // first visible scores of this row: O and l are still exactly 0
+        } else if (mt > m_used[j] + kRescaleThreshold) {
+          rescale = true;
+          alpha = fast_exp2(m_used[j] - mt);
+          m_used[j] = mt;
+        }
+        if (__any_sync(0xffffffffu, rescale)) {
+          // PV_j(prev) is complete (S_j(t) completed after it); scale our half of this row of O_j
+#pragma unroll
+          for (int c = 0; c < kOCols / 32; ++c) {
+            float r[32];
+            tmem_ld32_f(ocol + c * 32, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) r[e] *= alpha;
+            tmem_st32(ocol + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r));
+          }
+        }
+        l[j] *= alpha;
+        const float nm = m_used[j] == -INFINITY ? 0.f : -m_used[j];
+        const uint64_t nm2 = f2pk(nm, nm);
+        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+        uint32_t pk[kCols / 2];
+#pragma unroll
+        for (int c = 0; c < kCols / 2; ++c) {  // pair index: columns 2c, 2c+1
+          const uint64_t y = ffma2(f2pk(x[2 * c], x[2 * c + 1]), sl2, nm2);
+          float ya, yb, ea, eb;
+          f2upk(y, ya, yb);
+          if (c % kPolyEvery == kPolyEvery - 1) {
+            exp2_poly2(ya, yb, ea, eb);
+          } else {
+            ea = fast_exp2(ya);
+            eb = fast_exp2(yb);
+          }
+          acc[c & 3] = fadd2(acc[c & 3], f2pk(ea, eb));
+          pk[c] = pack_bf16x2(ea, eb);
+        }
+        // P_j (bf16 pairs) in packed columns [hf * 32, +32) of S_j: over the first half's S
+        tmem_st32(sbase + hf * (kCols / 2), pk);
+        float s0, s1;
+        f2upk(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), s0, s1);
+        l[j] += s0 + s1;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars.p_full[j]));
+        if (warp == 0) PPTR(1 + j, 41)
+      }
+    }
+    // epilogues: O_j / l -> bf16 rows (our half of the columns), lse
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (j == 1 && !has1) continue;
+      const int64_t ti0 = it.i0 + j * kM;
+      const int64_t ti1 = (ti0 + kM < p.N ? ti0 + kM : p.N) - 1;
+      const int64_t i = ti0 + row;
+      const uint32_t ocol = tmem + lane_off + (j ? C::kColO1 : C::kColO0) + hf * kOCols;
+      mbar_wait_warp(smem_u32(&bars.o_full[j]), ic[j] & 1);
+      ++ic[j];
+      red[j][hf][row] = l[j];
+      pair_sync();
+      const float lt = l[j] + red[j][hf ^ 1][row];
+      pair_sync();  // both read before the slot is reused by the next item's row max
+      tc_fence_after();
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      __nv_bfloat16 *orow = static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride +
+                            (int64_t)it.h * D + hf * kOCols;
+#pragma unroll
+      for (int c = 0; c < kOCols / 32; ++c) {
+        float r[32];
+        tmem_ld32_f(ocol + c * 32, r);
+        tmem_wait_ld();
+        if (i <= ti1) {
+          uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
+#pragma unroll
+          for (int v4 = 0; v4 < 4; ++v4) {
+            uint4 w;
+            w.x = pack_bf16x2(r[8 * v4 + 0] * inv, r[8 * v4 + 1] * inv);
+            w.y = pack_bf16x2(r[8 * v4 + 2] * inv, r[8 * v4 + 3] * inv);
+            w.z = pack_bf16x2(r[8 * v4 + 4] * inv, r[8 * v4 + 5] * inv);
+            w.w = pack_bf16x2(r[8 * v4 + 6] * inv, r[8 * v4 + 7] * inv);
+            dst[v4] = w;
+          }
+        }
+      }
+      if (p.lse && i <= ti1 && hf == 0)
+        p.lse[((int64_t)it.b * p.nql + it.h) * p.N + i] =
+            lt > 0.f ? (m_used[j] + __log2f(lt)) * kLn2 : -INFINITY;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars.o_empty[j]));
+    }
+  }
+}
+
 template <int D, int BS>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const PpParams p) {
   using C = PCfg<D>;
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 TMA / UMMA tiles need 1024-B alignment
   __shared__ PBars bars;
+  __shared__ float red[2][2][kM];  // split softmax: [tile][column half][row] row max / row sum
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t smem_base = smem_u32(smem_raw);
+  if (smem_base & 1023u) __trap();
   const uint32_t q_smem = smem_base;                        // Q0, Q1
   const uint32_t k_smem = q_smem + 2 * C::kTileBytes;       // kNK tiles
   const uint32_t v_smem = k_smem + C::kNK * C::kTileBytes;  // kNV tiles
@@ -485,9 +669,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&bars.q_full[j]), 1);
       mbar_init(smem_u32(&bars.q_empty[j]), 1);
       mbar_init(smem_u32(&bars.s_full[j]), 1);
-      mbar_init(smem_u32(&bars.p_full[j]), kSoftmaxWarpsPerTile);
+      mbar_init(smem_u32(&bars.p_full[j]), softmax_warps_per_tile<BS>());
       mbar_init(smem_u32(&bars.o_full[j]), 1);
-      mbar_init(smem_u32(&bars.o_empty[j]), kSoftmaxWarpsPerTile);
+      mbar_init(smem_u32(&bars.o_empty[j]), softmax_warps_per_tile<BS>());
     }
     for (int s = 0; s < C::kNK; ++s) {
       mbar_init(smem_u32(&bars.k_full[s]), 1);
@@ -512,7 +696,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
-    softmax_role<D, BS>(p, bars, tmem, total, (warp - kSoftmaxWarp0) >> 2, warp, lane);
+    if (BS >= 0)
+      softmax_split_role<D, BS>(p, bars, tmem, total, warp, lane, red);
+    else
+      softmax_role<D, BS>(p, bars, tmem, total, (warp - kSoftmaxWarp0) >> 2, warp, lane);
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
   if (warp == kWarpKV) {
