@@ -39,40 +39,55 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ uint32_t smem_u32i(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
 template <int D>
 struct InfSmem {
-  static constexpr int kStride = D + 8;  // bf16 elements per padded row: conflict-free 32-bit fragment loads
-  __nv_bfloat16 k[kB * kStride];
-  __nv_bfloat16 v[kB * kStride];
-  float red[4];
+  static constexpr int kStride = D + 8;  // bf16 elements per padded row: conflict-free ldmatrix rows
+  static constexpr int kBuf = kB * kStride;                       // one K or V block (elements)
+  static constexpr int kBytes = 2 * 2 * kBuf * 2;                 // K, V x 2 stages, bf16
 };
 
 // S (16 rows x 64 keys) = Q K^T and G = dO V^T for this warp's rows, from the staged block.
 template <int D>
-__device__ __forceinline__ void block_products(const InfSmem<D> &sm, const uint32_t (&qa)[D / 16][4],
+__device__ __forceinline__ void block_products(const __nv_bfloat16 *ks, const __nv_bfloat16 *vs,
+                                               const uint32_t (&qa)[D / 16][4],
                                                const uint32_t (&da)[D / 16][4], int lane, float (&S)[8][4],
                                                float (&G)[8][4]) {
-  const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int n = 0; n < 8; ++n)
 #pragma unroll
     for (int e = 0; e < 4; ++e) S[n][e] = G[n][e] = 0.f;
+  // ldmatrix.x4: lanes 8m..8m+7 address rows (keys) of 8x8 matrix m = (n-tile n0 + (m >> 1),
+  // dims kk*16 + 8 (m & 1)); registers r0..r3 = b0, b1 of n-tile n0 and of n-tile n0 + 1
+  const int mrow = lane & 7, msel = lane >> 3;
 #pragma unroll
   for (int kk = 0; kk < D / 16; ++kk) {
 #pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      const int key = n * 8 + g;  // B fragment column = key; k = head-dim index
-      const uint32_t *kr = reinterpret_cast<const uint32_t *>(&sm.k[key * InfSmem<D>::kStride + kk * 16]);
-      const uint32_t *vr = reinterpret_cast<const uint32_t *>(&sm.v[key * InfSmem<D>::kStride + kk * 16]);
-      mma16816(S[n], qa[kk], kr[t], kr[t + 4]);
-      mma16816(G[n], da[kk], vr[t], vr[t + 4]);
+    for (int n = 0; n < 8; n += 2) {
+      const int key = (n + (msel >> 1)) * 8 + mrow;
+      const int col = kk * 16 + (msel & 1) * 8;
+      uint32_t kb[4], vb[4];
+      ldsm_x4(kb, smem_u32i(&ks[key * InfSmem<D>::kStride + col]));
+      ldsm_x4(vb, smem_u32i(&vs[key * InfSmem<D>::kStride + col]));
+      mma16816(S[n], qa[kk], kb[0], kb[1]);
+      mma16816(S[n + 1], qa[kk], kb[2], kb[3]);
+      mma16816(G[n], da[kk], vb[0], vb[1]);
+      mma16816(G[n + 1], da[kk], vb[2], vb[3]);
     }
   }
 }
 
 template <int D>
 __global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a) {
-  __shared__ InfSmem<D> sm;
+  extern __shared__ __align__(16) uint8_t inf_dsm[];
+  __nv_bfloat16 *kv_s = reinterpret_cast<__nv_bfloat16 *>(inf_dsm);  // [stage][K | V][kBuf]
+  __shared__ float red[4];
   const int nb = (int)((a.N + kB - 1) / kB);
   const int ib = nb - 1 - (int)blockIdx.x;  // heaviest (longest causal row) blocks first
   const int h = blockIdx.y, b = blockIdx.z;
@@ -106,23 +121,35 @@ __global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a)
       da[kk][3] = ld(dO, a.q_row_stride, r1, c + 8);
     }
   }
-  auto stage = [&](int jb) {
-    __syncthreads();
+  // K/V block jb -> stage buf, 16-byte cp.async (zero fill past N); double-buffered: block
+  // jb+1 streams in while block jb is computed
+  auto stage_async = [&](int jb, int buf) {
     constexpr int kVec = D / 8;  // 16-byte vectors per row
+    __nv_bfloat16 *kd = kv_s + (size_t)buf * 2 * InfSmem<D>::kBuf, *vd = kd + InfSmem<D>::kBuf;
     for (int idx = threadIdx.x; idx < kB * kVec; idx += kThreadsInf) {
       const int r = idx / kVec, c = (idx - r * kVec) * 8;
       const int64_t j = (int64_t)jb * kB + r;
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = kv;
-      if (j < N) {
-        const int64_t off = ((int64_t)b * N + j) * a.kv_row_stride + (int64_t)gkv * D + c;
-        kv = *reinterpret_cast<const uint4 *>(K + off);
-        vv = *reinterpret_cast<const uint4 *>(V + off);
-      }
-      *reinterpret_cast<uint4 *>(&sm.k[r * InfSmem<D>::kStride + c]) = kv;
-      *reinterpret_cast<uint4 *>(&sm.v[r * InfSmem<D>::kStride + c]) = vv;
+      const int64_t off = ((int64_t)b * N + (j < N ? j : N - 1)) * a.kv_row_stride + (int64_t)gkv * D + c;
+      const uint32_t bytes = j < N ? 16u : 0u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32i(&kd[r * InfSmem<D>::kStride + c])),
+                   "l"(K + off), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32i(&vd[r * InfSmem<D>::kStride + c])),
+                   "l"(V + off), "r"(bytes)
+                   : "memory");
     }
-    __syncthreads();
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  auto pass_block = [&](int jb) -> int {  // wait for block jb (prefetch jb+1 first); its stage
+    if (jb + 1 <= ib) stage_async(jb + 1, (jb + 1) & 1);
+    if (jb + 1 <= ib)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    return jb & 1;
+  };
+  auto kbuf = [&](int buf) { return kv_s + (size_t)buf * 2 * InfSmem<D>::kBuf; };
   const float sl2 = a.scale * kLog2e;  // scores in log2 units
   float S[8][4], G[8][4];
 
@@ -132,9 +159,11 @@ __global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a)
   // R - G_js = (Ur - Gs Lr) / l are then formed without cancellation when A_js -> 1.
   float m[2] = {-INFINITY, -INFINITY}, Lr[2] = {0.f, 0.f}, Ur[2] = {0.f, 0.f}, Gs[2] = {0.f, 0.f};
   int js[2] = {-1, -1};
+  stage_async(0, 0);
   for (int jb = 0; jb <= ib; ++jb) {
-    stage(jb);
-    block_products<D>(sm, qa, da, lane, S, G);
+    const int buf = pass_block(jb);
+    block_products<D>(kbuf(buf), kbuf(buf) + InfSmem<D>::kBuf, qa, da, lane, S, G);
+    __syncthreads();  // every warp has read the stage before it is refilled (block jb+2)
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
       const int64_t i = rr ? r1 : r0;
@@ -200,16 +229,20 @@ __global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a)
       }
     }
   }
-  float l[2];
+  float l[2], inv_l[2];
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) l[rr] = 1.f + Lr[rr];
+  for (int rr = 0; rr < 2; ++rr) {
+    l[rr] = 1.f + Lr[rr];
+    inv_l[rr] = 1.f / l[rr];
+  }
 
   // ---- pass 2: E per key block, reduced to the block mean
   float *out = a.e_blocks + (((int64_t)b * a.nql + h) * nb + ib) * nb;
   const int64_t rows_real = (N - (int64_t)ib * kB) < kB ? N - (int64_t)ib * kB : kB;
+  stage_async(0, 0);
   for (int jb = 0; jb <= ib; ++jb) {
-    stage(jb);
-    block_products<D>(sm, qa, da, lane, S, G);
+    const int buf = pass_block(jb);
+    block_products<D>(kbuf(buf), kbuf(buf) + InfSmem<D>::kBuf, qa, da, lane, S, G);
     float acc = 0.f;
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
@@ -228,7 +261,7 @@ __global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a)
             } else {
               const float pp = exp2f(S[n][2 * rr + e] * sl2 - m[rr]);
               // A/(1-A) = p/(l-p), R - G = ((Gs - g) + (Ur - g Lr))/l
-              E = pp / (1.f + (Lr[rr] - pp)) * ((Gs[rr] - g) + (Ur[rr] - g * Lr[rr])) / l[rr];
+              E = __fdividef(pp, 1.f + (Lr[rr] - pp)) * ((Gs[rr] - g) + (Ur[rr] - g * Lr[rr])) * inv_l[rr];
             }
             acc += E;
           }
@@ -236,13 +269,14 @@ __global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a)
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) sm.red[warp] = acc;
+    if (lane == 0) red[warp] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
       const int64_t cols_real = (N - (int64_t)jb * kB) < kB ? N - (int64_t)jb * kB : kB;
-      const float mean = (sm.red[0] + sm.red[1] + sm.red[2] + sm.red[3]) / (float)(rows_real * cols_real);
+      const float mean = (red[0] + red[1] + red[2] + red[3]) / (float)(rows_real * cols_real);
       out[jb] = a.accumulate ? out[jb] + mean : mean;
     }
+    __syncthreads();  // red and the stage are reused by the next block
   }
   if (!a.accumulate)
     for (int jb = ib + 1 + (int)threadIdx.x; jb < nb; jb += kThreadsInf) out[jb] = 0.f;  // no causal pairs
@@ -253,10 +287,17 @@ __global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a)
 int launch_influence(const InfluenceArgs &a, void *stream) {
   const int nb = (int)((a.N + kB - 1) / kB);
   dim3 grid((unsigned)nb, (unsigned)a.nql, (unsigned)a.batch);
-  if (a.d == 128)
-    influence_kernel<128><<<grid, kThreadsInf, 0, (cudaStream_t)stream>>>(a);
-  else
-    influence_kernel<64><<<grid, kThreadsInf, 0, (cudaStream_t)stream>>>(a);
+  if (a.d == 128) {
+    cudaError_t e = cudaFuncSetAttribute(influence_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         InfSmem<128>::kBytes);
+    if (e != cudaSuccess) return (int)e;
+    influence_kernel<128><<<grid, kThreadsInf, InfSmem<128>::kBytes, (cudaStream_t)stream>>>(a);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(influence_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         InfSmem<64>::kBytes);
+    if (e != cudaSuccess) return (int)e;
+    influence_kernel<64><<<grid, kThreadsInf, InfSmem<64>::kBytes, (cudaStream_t)stream>>>(a);
+  }
   return (int)cudaGetLastError();
 }
 
