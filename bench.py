@@ -11,7 +11,10 @@ append + split-KV decode + combine, one launch per layer-token).
 
 Multi-GPU (torchrun, one rank per GPU): every rank serves its own batch of 8
 sequences (data parallel over independent sequences, no collective on the
-data path) -> "scaling": "weak".  Timing: barrier + synchronize on both sides,
+data path) -> "scaling": "weak".  At N > 1 (or with --kv-shard) the line also
+carries "kv_shard": the north-star partition -- one batch of 8, its kv-groups
+split over the ranks, the head outputs all-gathered with NCCL after every layer
+(strong scaling, with and without the all-gather).  Timing: barrier + synchronize on both sides,
 CUDA events on the launching stream, max over ranks.  The working set (8.6 GB
 of cache cycled over 32 layers, 268 MB per layer) exceeds the 126 MB L2, so no
 flush is needed between steps.
@@ -285,6 +288,15 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- e2e: host buffers through the public API, H2D/D2H inside the timed region
     e2e = run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev)
+    kv_shard = None
+    if world > 1 or args.kv_shard:
+        del Q, K, V, O
+        ctx = None
+        torch.cuda.empty_cache()
+        try:
+            kv_shard = run_kv_shard(rank, world, dev, scale)
+        except Exception as exc:  # reported, never fatal for the main line
+            kv_shard = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -320,7 +332,71 @@ def run_ours(args, rank, world, local_rank):
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
+        if kv_shard is not None:
+            line["kv_shard"] = kv_shard
         print(json.dumps(line), flush=True)
+
+
+def run_kv_shard(rank, world, dev, scale, T=64):
+    """North-star partition across GPUs: the SAME batch of 8 sequences, its
+    kv-groups split over the ranks (each rank's cache holds only its groups), and after every
+    layer the head outputs all-gathered with NCCL (torch.distributed.all_gather_into_tensor
+    over NVLink) into the full [B, Hq, d] layout.  Strong scaling: decode tokens/s of the
+    whole job with and without the per-layer all-gather, device-timed, max over ranks."""
+    import paper_2406_14909_b200 as moa
+    from paper_2406_14909_b200 import dist as mdist
+
+    L, B, N, d, s, G = CFG.layers, CFG.batch, CFG.N, CFG.head_dim, CFG.n_sink, CFG.group
+    shard = mdist.plan_shards(world, CFG.hkv, B, "kv")[rank]
+    windows = windows_all_layers(moa)
+    ctx = mdist.make_context(shard, L, CFG.hq, CFG.hkv, d, device=dev.index)
+    for l in range(L):
+        ctx.set_spans(l, windows[l], s, N)
+    ctx.alloc_cache(B)
+    ws = ctx.alloc_workspace(B)
+    g = torch.Generator(device=dev).manual_seed(77)
+    kp = torch.randn(B, N, CFG.hkv, d, device=dev, generator=g).to(torch.bfloat16)  # prompt K/V (all groups)
+    vp = torch.randn(B, N, CFG.hkv, d, device=dev, generator=g).to(torch.bfloat16)
+    kl, vl = mdist.local_slice_kv(kp, shard), mdist.local_slice_kv(vp, shard)
+    qd, kd, vd = decode_tokens(CFG, 0, T, device=dev)
+    hq_l = (shard.g1 - shard.g0) * G
+    od = torch.empty(B, hq_l, d, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def phase(gather):
+        for l in range(L):
+            ctx.cache_fill(l, kl, vl)          # positions restart at N
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for t in range(T):
+            ql = mdist.local_slice_q(qd[t], shard, G)
+            kt, vt = mdist.local_slice_kv(kd[t], shard), mdist.local_slice_kv(vd[t], shard)
+            for l in range(L):
+                ctx.decode_step_fused(l, ql, kt, vt, od, N + t, scale, ws)
+                if gather:
+                    mdist.gather_heads(od, shard)  # [B, Hq, d] on every rank
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            x = torch.tensor([ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+            ms = x.item()
+        return ms
+
+    phase(True)
+    with_ag = phase(True)
+    compute = phase(False)
+    return {"mode": f"kv-groups over {world} rank(s) ({CFG.hkv // world} groups each), same batch of {B}",
+            "decode_tokens_per_s": B * T / (with_ag / 1e3),
+            "decode_tokens_per_s_no_allgather": B * T / (compute / 1e3),
+            "allgather_us_per_layer": (with_ag - compute) * 1e3 / (T * L),
+            "tokens": T, "scaling": "strong",
+            "note": "NCCL all_gather_into_tensor of each layer's head outputs (torch.distributed), device-timed, "
+                    "max over ranks"}
 
 
 def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
@@ -415,6 +491,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kv-shard", action="store_true", help="also run the kv-group sharded decode at N = 1")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
