@@ -249,3 +249,24 @@ def test_plan_rules_is_optimal_at_its_density(moa, seed):
     best_free = min(Lp for _, Lp, _ in _enumerate(loss.astype(np.float64), dens.astype(np.float64), layers, hpl, k))
     if budget >= dens.max():
         assert abs(L - best_free) < 1e-4
+
+
+def test_bench_algorithmic_work_matches_oracle_counts():
+    """The roofline numerators of bench.py (in-window prefill FLOPs, decode bytes) against the
+    oracle's brute-force pair count and resident-row count."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        N, s, T, d, G = int(rng.integers(20, 90)), int(rng.integers(0, 6)), int(rng.integers(1, 4)), 8, 2
+        H = 4
+        wl = [int(rng.integers(0 if s else 1, N + 10)) for _ in range(H)]
+        flops, dec = bench.algorithmic_work([wl], 1, N, T, s, d, G)
+        assert flops == sum(4 * d * oracle.visible_pairs(N, w, s) for w in wl)
+        wg = oracle.group_windows(wl, G)
+        p = N + T - 1  # the ring is full at the last decode position of the step
+        rows = sum(len(oracle.resident_positions(p, s, int(w))) for w in wg)
+        assert dec == rows * d * 2 * 2 + H * d * 2 * 2 + len(wg) * d * 2 * 2 * 2
