@@ -135,6 +135,32 @@ moa_status moa_set_spans(moa_ctx *ctx, int layer, const int32_t *window_per_q_he
 moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_per_q_head,
                                  int n_sink, int64_t N, int block);
 
+/*
+ * Ragged batch: per-sequence prompt lengths and spans.
+ * Eq. 2 makes every span a function of the input length N (PAPER.md:181,
+ * "elastic rules ... scale with the input length"), so sequences of different
+ * lengths in one batch have different windows W_{b,h} = span_h(N_b) - n_sink
+ * (moa_resolve_spans at N_b).  The layer's moa_set_spans(..., N) fixes the padded
+ * length N (the row stride of q/k/v/o) and the cache capacity W_g; this call
+ * installs, for sequences b < batch,
+ *   seq_len                 host [batch]: N_b in [1, N].
+ *   window_per_seq_q_head   host [batch, num_q_heads] (ALL heads; the context keeps its
+ *                           shard) or NULL (= the layer's windows for every sequence).
+ *                           0 <= W_{b,h} <= W_g of the head's group (the ring must hold the
+ *                           window); block mode: multiples of the block.
+ * batch = 0 returns the layer to a uniform batch.  moa_set_spans clears it.
+ * While a layer is ragged:
+ *   - moa_prefill / moa_prefill_attn / moa_cache_fill take N = the padded length and
+ *     batch = this batch; sequence b is the prompt of its first N_b rows under its own
+ *     windows; output / lse rows i >= N_b are not written.  The cache fill stores
+ *     positions < N_b.
+ *   - decode goes through moa_decode_step_fused_ragged (the uniform append / decode
+ *     calls return MOA_ERR_STATE).
+ * Errors: MOA_ERR_INVALID_ARG (ranges above), nothing is changed on error.
+ */
+moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq_len,
+                          const int32_t *window_per_seq_q_head);
+
 /* Bytes of the K (and of the V) cache of all layers / of one layer for
  * `batch` sequences.  All layers' spans must be set for the first form. */
 moa_status moa_cache_bytes(const moa_ctx *ctx, int batch, size_t *k_bytes, size_t *v_bytes);
@@ -216,6 +242,23 @@ moa_status moa_decode_step_fused(moa_ctx *ctx, int layer, const void *q, const v
                                  int64_t kv_batch_stride, int64_t o_batch_stride, int batch,
                                  int64_t pos, float scale, float *lse_out, void *workspace,
                                  size_t ws_bytes, moa_stream_t stream);
+
+/*
+ * Append + decode of a ragged batch: moa_decode_step_fused where sequence b is at its
+ * own position pos[b] (a6 + a7 + a8 per sequence, PAPER.md:704 cache replacement).
+ *   pos   DEVICE int64 [batch], caller-owned, 8-byte aligned, read by the kernel after its
+ *         stream predecessor completes (so a preceding kernel may advance it; CUDA-graph
+ *         friendly).  pos[b] must be the next position of sequence b (N_b after the
+ *         prefill, +1 per step); this is not checked.  pos[b] < 0 marks an inactive
+ *         sequence: nothing is written to its cache, its o row is 0 and its lse -inf.
+ * Windows: the layer's ragged windows (moa_set_ragged) or, on a uniform layer, the
+ * layer's windows.  On a ragged layer batch must equal the ragged batch.
+ */
+moa_status moa_decode_step_fused_ragged(moa_ctx *ctx, int layer, const void *q, const void *k_new,
+                                        const void *v_new, void *o, int64_t q_batch_stride,
+                                        int64_t kv_batch_stride, int64_t o_batch_stride, int batch,
+                                        const int64_t *pos, float scale, float *lse_out, void *workspace,
+                                        size_t ws_bytes, moa_stream_t stream);
 
 /* ---------------- host-side introspection (planning contexts too) ---------------- */
 

@@ -70,6 +70,8 @@ __all__ = [
     "prefill",
     "prefill_rows",
     "prefill_dense_mask",
+    "prefill_ragged",
+    "decode_ragged",
     "decode",
     "slot_of",
     "resident_positions",
@@ -234,6 +236,47 @@ def prefill_dense_mask(Q, K, V, windows_q, n_sink: int, tau: float, block: int =
             O[b, :, h] = A @ V[b, :, g].astype(np.float64)
             LSE[b, h] = mx[:, 0] + np.log(E.sum(axis=1))
     return O, LSE
+
+
+# ---------------------------------------------------------------------------
+# Ragged batches: per-sequence length, per-sequence spans
+# ---------------------------------------------------------------------------
+
+def prefill_ragged(Q, K, V, seq_len, windows_bq, n_sink: int, tau: float, block: int = 0):
+    """Prefill of a padded ragged batch: sequence b is the prompt of its first
+    ``seq_len[b]`` rows and its heads use ``windows_bq[b]`` -- the spans of Eq. 2
+    resolved at that sequence's own length (spans "scale with the
+    input length").  Each sequence is its own problem (Eq. 1 per sequence), so this
+    is ``prefill`` of every truncated sequence.  Rows i >= N_b are NaN (no output).
+    Returns O [B, N, Hq, d], LSE [B, Hq, N] (fp64)."""
+    B, N, Hq, Hkv, d, G = _check_shapes(Q, K, V, windows_bq[0])
+    O = np.full((B, N, Hq, d), np.nan)
+    LSE = np.full((B, Hq, N), np.nan)
+    for b in range(B):
+        n = int(seq_len[b])
+        assert 1 <= n <= N
+        o, l = prefill(Q[b:b + 1, :n], K[b:b + 1, :n], V[b:b + 1, :n], list(windows_bq[b]), n_sink, tau, block)
+        O[b, :n] = o[0]
+        LSE[b, :, :n] = l[0]
+    return O, LSE
+
+
+def decode_ragged(q, K_hist, V_hist, pos, windows_bq, n_sink: int, tau: float):
+    """Decode step of a ragged batch: sequence b is at its own position pos[b]
+    with its own windows (``decode`` per sequence).  pos[b] < 0 marks
+    an inactive sequence: O row 0, LSE -inf (the C-ABI's convention).
+    Returns O [B, Hq, d], LSE [B, Hq]."""
+    B, Hq, d = q.shape
+    O = np.zeros((B, Hq, d), dtype=np.float64)
+    L = np.full((B, Hq), -np.inf)
+    for b in range(B):
+        p = int(pos[b])
+        if p < 0:
+            continue
+        o, l = decode(q[b:b + 1], K_hist[b:b + 1, :p + 1], V_hist[b:b + 1, :p + 1], p, list(windows_bq[b]),
+                      n_sink, tau)
+        O[b], L[b] = o[0], l[0]
+    return O, L
 
 
 # ---------------------------------------------------------------------------

@@ -30,6 +30,7 @@ _SIGS = [
     ("moa_resolve_spans", c_int, [POINTER(c_float), POINTER(c_float), c_int, c_int64, c_int, POINTER(c_int32)]),
     ("moa_set_spans", c_int, [_P, c_int, POINTER(c_int32), c_int, c_int64]),
     ("moa_set_spans_blocked", c_int, [_P, c_int, POINTER(c_int32), c_int, c_int64, c_int]),
+    ("moa_set_ragged", c_int, [_P, c_int, c_int, POINTER(c_int64), POINTER(c_int32)]),
     ("moa_cache_bytes", c_int, [_P, c_int, POINTER(c_size_t), POINTER(c_size_t)]),
     ("moa_layer_cache_bytes", c_int, [_P, c_int, c_int, POINTER(c_size_t), POINTER(c_size_t)]),
     ("moa_workspace_bytes", c_int, [_P, c_int, POINTER(c_size_t)]),
@@ -45,6 +46,8 @@ _SIGS = [
                                 c_size_t, _P]),
     ("moa_decode_step_fused", c_int, [_P, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int, c_int64,
                                       c_float, _P, _P, c_size_t, _P]),
+    ("moa_decode_step_fused_ragged", c_int, [_P, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int, _P,
+                                             c_float, _P, _P, c_size_t, _P]),
     ("moa_get_window", c_int, [_P, c_int, c_int, POINTER(c_int32)]),
     ("moa_get_group_window", c_int, [_P, c_int, c_int, POINTER(c_int32)]),
     ("moa_slot_of", c_int, [_P, c_int, c_int, c_int64, POINTER(c_int64)]),

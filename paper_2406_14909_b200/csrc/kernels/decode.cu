@@ -42,6 +42,9 @@ struct DecodeParams {
   const int32_t *win_g, *win_q, *chunks, *g_chunk;
   int n_chunks, ngl, n_sink;
   int64_t pos;
+  const int64_t *pos_b;     // ragged: per-sequence positions (null: pos)
+  const int32_t *win_bq;    // ragged: per-sequence windows [batch, nql] (null: win_q)
+  int nql;
   float scale_log2;
   float *lse;
   float *part;
@@ -65,11 +68,11 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const DecodeParams p) 
   const int g = p.chunks[3 * c], r0 = p.chunks[3 * c + 1], r1 = p.chunks[3 * c + 2];
   const int Wg = p.win_g[g];
   const int s = p.n_sink;
-  const int64_t pos = p.pos;
+  const int64_t pos = p.pos_b ? p.pos_b[b] : p.pos;  // ragged: pos < 0 = inactive (all masked)
 
   int Wj[G];
 #pragma unroll
-  for (int j = 0; j < G; ++j) Wj[j] = p.win_q[g * G + j];
+  for (int j = 0; j < G; ++j) Wj[j] = p.win_bq ? p.win_bq[(int64_t)b * p.nql + g * G + j] : p.win_q[g * G + j];
 
   // ring bookkeeping: ring row k holds position pos - m with m = (pm - k) mod W_g,
   // valid iff m <= pos - s.
@@ -278,7 +281,7 @@ int launch_t(const DecodeArgs &a, bool fused, void *stream) {
   p.kc = a.k_cache; p.vc = a.v_cache; p.rows_per_seq = a.rows_per_seq;
   p.g_off = a.d_g_off; p.win_g = a.d_win_g; p.win_q = a.d_win_q; p.chunks = a.d_chunks;
   p.g_chunk = a.d_g_chunk; p.n_chunks = a.n_chunks; p.ngl = a.ngl; p.n_sink = a.n_sink;
-  p.pos = a.pos; p.scale_log2 = a.scale * kLog2e; p.lse = a.lse; p.part = a.ws_part;
+  p.pos = a.pos; p.pos_b = a.d_pos; p.win_bq = a.d_win_bq; p.nql = a.ngl * a.G; p.scale_log2 = a.scale * kLog2e; p.lse = a.lse; p.part = a.ws_part;
   p.counters = a.counters;
   dim3 grid((unsigned)a.n_chunks, (unsigned)a.batch);
   if (fused)

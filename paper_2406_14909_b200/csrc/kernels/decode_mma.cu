@@ -94,6 +94,8 @@ struct MParams {
   const int32_t *win_g, *win_q;
   int ngl, G, n_sink, batch;
   int64_t pos;
+  const int64_t *pos_b;   // ragged: per-sequence positions (null: pos); < 0 = inactive
+  const int32_t *win_bq;  // ragged: per-sequence windows [batch, ngl * G] (null: win_q)
   float scale_log2;
   float *lse;
   float *part;
@@ -449,7 +451,6 @@ __global__ void __launch_bounds__(kThreads, CPS)
   const int qr = lane >> 2, qc = lane & 3;  // fragment row (head) / column-pair index
   const int h0 = qr, h1 = qr + 8;           // the two head rows this lane holds
   const int s = p.n_sink;
-  const int64_t pos = p.pos;
   int T = 0, n = 0;
 #ifdef MOA_DEC_TRACE
   int nseg = 0;
@@ -461,8 +462,10 @@ __global__ void __launch_bounds__(kThreads, CPS)
 #ifdef MOA_DEC_TRACE
     ++nseg;
 #endif
-    const int W0 = h0 < G ? p.win_q[rg.g * G + h0] : rg.Wg;
-    const int W1 = h1 < G ? p.win_q[rg.g * G + h1] : rg.Wg;
+    const int64_t pos = p.pos_b ? p.pos_b[rg.b] : p.pos;
+    const int32_t *wq = p.win_bq ? p.win_bq + (int64_t)rg.b * p.ngl * G : p.win_q;
+    const int W0 = h0 < G ? wq[rg.g * G + h0] : rg.Wg;
+    const int W1 = h1 < G ? wq[rg.g * G + h1] : rg.Wg;
     const bool ring_live = pos >= s && rg.Wg > 0;
     const int pm = ring_live ? (int)((pos - s) % rg.Wg) : 0;
     const int64_t slot_p = (p.k_new != nullptr) ? slot_of(pos, s, rg.Wg) : -1;
@@ -754,6 +757,8 @@ int launch_v(const DecodeMmaArgs &a, void *stream) {
   p.n_sink = a.n_sink;
   p.batch = a.batch;
   p.pos = a.pos;
+  p.pos_b = a.d_pos;
+  p.win_bq = a.d_win_bq;
   p.scale_log2 = a.scale * kLog2e;
   p.lse = a.lse;
   p.part = a.ws_part;

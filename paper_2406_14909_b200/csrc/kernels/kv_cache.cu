@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(256) cache_fill_kernel(
     const uint4 *__restrict__ k, const uint4 *__restrict__ v, int64_t row_stride_v,  // in uint4
     uint4 *__restrict__ kc, uint4 *__restrict__ vc, int64_t rows_per_seq,
     const int64_t *__restrict__ g_off, const int32_t *__restrict__ win_g, int vpr, int n_sink,
-    int64_t N) {
+    int64_t N, const int64_t *__restrict__ seq_n) {
   const int g = blockIdx.y, b = blockIdx.z;
   const int Wg = win_g[g];
   const int64_t R = (int64_t)n_sink + Wg;
@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(256) cache_fill_kernel(
   const int64_t r = idx / vpr;
   const int e = (int)(idx - r * vpr);
   if (r >= R) return;
-  const int64_t p = moa::pos_of_row(r, N - 1, n_sink, Wg);
+  const int64_t Nb = seq_n ? seq_n[b] : N;  // ragged: this sequence's prompt length (<= N)
+  const int64_t p = moa::pos_of_row(r, Nb - 1, n_sink, Wg);
   if (p < 0) return;  // row not reached by the prompt (short prompt)
   const int64_t src = ((int64_t)b * N + p) * row_stride_v + (int64_t)g * vpr + e;
   const int64_t dst = ((int64_t)b * rows_per_seq + g_off[g] + r) * vpr + e;
@@ -44,9 +45,11 @@ __global__ void kv_append_kernel(const uint4 *__restrict__ k, const uint4 *__res
                                  uint4 *__restrict__ vc, int64_t rows_per_seq,
                                  const int64_t *__restrict__ g_off,
                                  const int32_t *__restrict__ win_g, int vpr, int n_sink,
-                                 int64_t pos) {
+                                 int64_t pos, const int64_t *__restrict__ pos_b) {
   const int g = blockIdx.x, b = blockIdx.y;
-  const int64_t slot = moa::slot_of(pos, n_sink, win_g[g]);
+  const int64_t pb = pos_b ? pos_b[b] : pos;  // ragged: per-sequence position, < 0 = inactive
+  if (pb < 0) return;
+  const int64_t slot = moa::slot_of(pb, n_sink, win_g[g]);
   if (slot < 0) return;  // W_g = 0: a sink-only group stores no recent token
   const int t = threadIdx.x;
   const bool is_v = t >= vpr;
@@ -68,7 +71,7 @@ int launch_cache_fill(const CacheArgs &a, void *stream) {
   cache_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
       static_cast<const uint4 *>(a.k), static_cast<const uint4 *>(a.v), a.row_stride * a.esize / 16,
       static_cast<uint4 *>(a.k_cache), static_cast<uint4 *>(a.v_cache), a.rows_per_seq, a.d_g_off,
-      a.d_win_g, vpr, a.n_sink, a.N_or_pos);
+      a.d_win_g, vpr, a.n_sink, a.N_or_pos, a.d_seq_n);
   return (int)cudaGetLastError();
 }
 
@@ -78,7 +81,7 @@ int launch_kv_append(const CacheArgs &a, void *stream) {
   kv_append_kernel<<<grid, 2 * vpr, 0, (cudaStream_t)stream>>>(
       static_cast<const uint4 *>(a.k), static_cast<const uint4 *>(a.v), a.row_stride * a.esize / 16,
       static_cast<uint4 *>(a.k_cache), static_cast<uint4 *>(a.v_cache), a.rows_per_seq, a.d_g_off,
-      a.d_win_g, vpr, a.n_sink, a.N_or_pos);
+      a.d_win_g, vpr, a.n_sink, a.N_or_pos, a.d_pos);
   return (int)cudaGetLastError();
 }
 

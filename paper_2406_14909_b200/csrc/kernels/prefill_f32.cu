@@ -36,11 +36,13 @@ __global__ void __launch_bounds__(kRows) prefill_f32_kernel(PrefillArgs a) {
   const int h = a.d_items[2 * item], qt = a.d_items[2 * item + 1];
   const int g = h / a.G;
   const int tid = threadIdx.x;
-  const int64_t N = a.N;
+  const int64_t N = a.N;                               // row stride of a sequence (padded length)
+  const int64_t Nb = a.d_seq_n ? a.d_seq_n[b] : N;     // ragged: this sequence's length
   const int64_t i0 = (int64_t)qt * kRows;
-  const int64_t i1 = (N < i0 + kRows ? N : i0 + kRows) - 1;
+  if (i0 >= Nb) return;                                // whole tile past a ragged sequence's end
+  const int64_t i1 = (Nb < i0 + kRows ? Nb : i0 + kRows) - 1;
   const int64_t i = i0 + tid;
-  const int W = a.d_win_q[h];
+  const int W = a.d_win_bq ? a.d_win_bq[(int64_t)b * a.nql + h] : a.d_win_q[h];
   const int s = a.n_sink;
 
   const float *Q = static_cast<const float *>(a.q);

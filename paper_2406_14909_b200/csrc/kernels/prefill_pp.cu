@@ -84,6 +84,8 @@ struct PpParams {
   int bshift;            // -1 token mask, else log2(block size) (block mode)
   const int32_t *win_q;
   const int32_t *items;  // (q-head, q-block) pairs, LPT order
+  const int64_t *seq_n;  // ragged: per-sequence N_b (null: N)
+  const int32_t *win_bq; // ragged: per-sequence windows [batch, nql] (null: win_q)
 };
 
 struct PBars {
@@ -105,19 +107,21 @@ __device__ __forceinline__ int bshift_of(const PpParams &p) {
 
 struct PItem {
   int b, h, W;
-  int64_t i0;
+  int64_t i0, N;  // N: this sequence's length (ragged) or p.N; the item is empty iff i0 >= N
   BlockTiles bt;
 };
 
-template <int BS>
+template <int BS, bool RAG>
 __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
   PItem it;
   const int wi = idx / p.batch;
   it.b = idx - wi * p.batch;
   it.h = p.items[2 * wi];
   it.i0 = (int64_t)p.items[2 * wi + 1] * (2 * kM);
-  it.W = p.win_q[it.h];
-  it.bt = kv_block_tiles(it.i0, p.N, it.W, p.n_sink, bshift_of<BS>(p));
+  // ragged batches are a separate instantiation: the uniform kernel keeps its registers
+  it.N = RAG ? p.seq_n[it.b] : p.N;
+  it.W = RAG ? p.win_bq[(int64_t)it.b * p.nql + it.h] : p.win_q[it.h];
+  it.bt = kv_block_tiles(it.i0, it.N, it.W, p.n_sink, bshift_of<BS>(p));
   return it;
 }
 
@@ -207,7 +211,7 @@ __device__ int g_pp_trace_n[4];
 #define PPTR(role, tag) {}
 #endif
 
-template <int D, int BS>
+template <int D, int BS, bool RAG>
 __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_t tmem, uint32_t q_smem,
                                          uint32_t k_smem, uint32_t v_smem, int total, int j) {
   using C = PCfg<D>;
@@ -234,8 +238,11 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
     PPTR(j ? 3 : 0, 3)
     asm volatile("bar.arrive %0, 64;" ::"r"(kBarTurn0 + (j ^ 1)) : "memory");
   };
+  bool any = false;  // a CTA whose items all lie past their ragged sequences' ends has no turns
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-    const PItem it = get_pitem<BS>(p, idx);
+    const PItem it = get_pitem<BS, RAG>(p, idx);
+    if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
+    any = true;
     const bool mine = j == 0 || it.bt.has1;  // this q tile has rows in the item
     const TileRanges r = j ? it.bt.r[1] : it.bt.r[0];
     const int last_t = r.b1 > r.b0 ? r.b1 - 1 : r.a1 - 1;  // its S releases Q_j, its PV completes O_j
@@ -318,13 +325,13 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
   }
   // the other warp's last hand-over to this one is never taken: drain it, so the named
   // barrier is clean for the next kernel on this SM
-  if (j == 0) asm volatile("bar.sync %0, 64;" ::"r"(kBarTurn0) : "memory");
+  if (j == 0 && any) asm volatile("bar.sync %0, 64;" ::"r"(kBarTurn0) : "memory");
 }
 
 // ------------------------------------------------------------------------------------------
 // softmax of q tile j (warps 4j .. 4j+3): thread owns one row, all 128 columns of S_j.
 // ------------------------------------------------------------------------------------------
-template <int D, int BS>
+template <int D, int BS, bool RAG>
 __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uint32_t tmem, int total, int j,
                                              int warp, int lane) {
   using C = PCfg<D>;
@@ -338,10 +345,11 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
   int sc = 0;  // S handshakes of this tile
   int ic = 0;  // items of this tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-    const PItem it = get_pitem<BS>(p, idx);
+    const PItem it = get_pitem<BS, RAG>(p, idx);
+    if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
     if (j == 1 && !it.bt.has1) continue;
     const int64_t ti0 = it.i0 + j * kM;                     // first row of this q tile
-    const int64_t ti1 = (ti0 + kM < p.N ? ti0 + kM : p.N) - 1;  // last real row
+    const int64_t ti1 = (ti0 + kM < it.N ? ti0 + kM : it.N) - 1;  // last real row
     const int64_t i = ti0 + row;
     // first window key of this row: i-W+1 (token mask) or the block-aligned start (block mode);
     // W = 0 puts it past the row
@@ -479,7 +487,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
 // per-thread work of a tile's softmax, which bounds the ping-pong: one tile's softmax must
 // fit under the other tile's MMAs.
 // ------------------------------------------------------------------------------------------
-template <int D, int BS>
+template <int D, int BS, bool RAG>
 __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bars, uint32_t tmem, int total, int warp,
                                              int lane, float (*red)[2][kM]) {
   using C = PCfg<D>;
@@ -496,7 +504,8 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
   int sc[2] = {0, 0};  // S handshakes per tile
   int ic[2] = {0, 0};  // items per tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-    const PItem it = get_pitem<BS>(p, idx);
+    const PItem it = get_pitem<BS, RAG>(p, idx);
+    if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
     const bool has1 = it.bt.has1;
     float m_used[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     const int ns = it.bt.steps();
@@ -508,7 +517,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
       for (int j = 0; j < 2; ++j) {
         if (!u[j]) continue;
         const int64_t ti0 = it.i0 + j * kM;                         // first row of this q tile
-        const int64_t ti1 = (ti0 + kM < p.N ? ti0 + kM : p.N) - 1;  // last real row
+        const int64_t ti1 = (ti0 + kM < it.N ? ti0 + kM : it.N) - 1;  // last real row
         const int64_t i = ti0 + row;
         const int64_t j0 = (int64_t)t * kN + hf * kCols;  // key of this warp's first column
         const uint32_t sbase = tmem + lane_off + (j ? 128u : 0u);
@@ -607,7 +616,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
     for (int j = 0; j < 2; ++j) {
       if (j == 1 && !has1) continue;
       const int64_t ti0 = it.i0 + j * kM;
-      const int64_t ti1 = (ti0 + kM < p.N ? ti0 + kM : p.N) - 1;
+      const int64_t ti1 = (ti0 + kM < it.N ? ti0 + kM : it.N) - 1;
       const int64_t i = ti0 + row;
       const uint32_t ocol = tmem + lane_off + (j ? C::kColO1 : C::kColO0) + hf * kOCols;
       mbar_wait_warp(smem_u32(&bars.o_full[j]), ic[j] & 1);
@@ -648,7 +657,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
   }
 }
 
-template <int D, int BS>
+template <int D, int BS, bool RAG>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const PpParams p) {
@@ -697,16 +706,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
     if (BS >= 0)
-      softmax_split_role<D, BS>(p, bars, tmem, total, warp, lane, red);
+      softmax_split_role<D, BS, RAG>(p, bars, tmem, total, warp, lane, red);
     else
-      softmax_role<D, BS>(p, bars, tmem, total, (warp - kSoftmaxWarp0) >> 2, warp, lane);
+      softmax_role<D, BS, RAG>(p, bars, tmem, total, (warp - kSoftmaxWarp0) >> 2, warp, lane);
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
   if (warp == kWarpKV) {
     if (lane == 0) {
       int T = 0;
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-        const PItem it = get_pitem<BS>(p, idx);
+        const PItem it = get_pitem<BS, RAG>(p, idx);
+        if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
         const int g = it.h / p.G;
         const int ns = it.bt.steps();
         for (int k = 0; k < ns; ++k) {
@@ -735,7 +745,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int qc[2] = {0, 0};
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-        const PItem it = get_pitem<BS>(p, idx);
+        const PItem it = get_pitem<BS, RAG>(p, idx);
+        if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
         for (int j = 0; j < 2; ++j) {
           if (j == 1 && !it.bt.has1) continue;
           if (qc[j] > 0) mbar_wait(smem_u32(&bars.q_empty[j]), (qc[j] - 1) & 1);
@@ -748,7 +759,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // warm L2 with the next item's Q tiles (their loads wait for this item's last S MMAs)
         if (idx + (int)gridDim.x < total) {
-          const PItem nx = get_pitem<BS>(p, idx + gridDim.x);
+          const PItem nx = get_pitem<BS, RAG>(p, idx + gridDim.x);
           for (int j = 0; j < (nx.bt.has1 ? 2 : 1); ++j)
             for (int sl = 0; sl < C::kSlabs; ++sl)
               tma_prefetch_4d(&tm_q, sl * 64, nx.h, (int)(nx.i0 + j * kM), nx.b);
@@ -756,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kWarpMMA || warp == kWarpMMA1) {
-    mma_role<D, BS>(p, bars, tmem, q_smem, k_smem, v_smem, total, warp == kWarpMMA ? 0 : 1);
+    mma_role<D, BS, RAG>(p, bars, tmem, q_smem, k_smem, v_smem, total, warp == kWarpMMA ? 0 : 1);
   }
   }
 
@@ -800,12 +811,16 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   p.bshift = a.bshift;
   p.scale_log2 = a.scale * kLog2e;
   p.win_q = a.d_win_q;
+  p.seq_n = a.d_seq_n;
+  p.win_bq = a.d_win_bq;
   p.items = a.d_items2;
   // the token mask (bshift < 0) and the block mask are separate instantiations, so the
   // token path carries no block-mode arithmetic
-  auto kern = p.bshift < 0    ? prefill_pp_kernel<D, -1>
-              : p.bshift == 6 ? prefill_pp_kernel<D, 6>
-                              : prefill_pp_kernel<D, kBsRuntime>;
+  const bool rag = p.seq_n != nullptr;
+  auto kern = p.bshift < 0    ? (rag ? prefill_pp_kernel<D, -1, true> : prefill_pp_kernel<D, -1, false>)
+              : p.bshift == 6 ? (rag ? prefill_pp_kernel<D, 6, true> : prefill_pp_kernel<D, 6, false>)
+                              : (rag ? prefill_pp_kernel<D, kBsRuntime, true>
+                                     : prefill_pp_kernel<D, kBsRuntime, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return (int)e;
   const int total = p.n_items * p.batch;

@@ -21,6 +21,9 @@ namespace {
 
 thread_local std::string g_err;
 
+// next_pos of a ragged layer after its cache fill: positions are per sequence (caller-owned)
+constexpr int64_t kRaggedPos = -2;
+
 moa_status fail(moa_status st, const char *fmt, ...) {
   char buf[512];
   va_list ap;
@@ -76,7 +79,18 @@ int decode_chunk_rows_override() {
   return v > 0 ? v : 0;
 }
 
+void free_ragged(LayerPlan &p) {
+  if (p.d_rag) cudaFree(p.d_rag);
+  p.d_rag = nullptr;
+  p.d_seq_n = nullptr;
+  p.d_win_bq = nullptr;
+  p.rag_batch = 0;
+  p.rag_n.clear();
+  p.rag_win.clear();
+}
+
 void free_tables(LayerPlan &p) {
+  free_ragged(p);
   if (p.d_tables) cudaFree(p.d_tables);
   p.d_tables = nullptr;
   p.d_win_q = p.d_win_g = nullptr;
@@ -368,6 +382,68 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
   return ok();
 }
 
+moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq_len,
+                          const int32_t *window_per_seq_q_head) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  LayerPlan &p = ctx->layers[layer];
+  if (batch == 0) {
+    DeviceGuard dg(ctx->device);
+    free_ragged(p);
+    p.next_pos = p.k_cache ? 0 : -1;
+    return ok();
+  }
+  if (batch < 0 || batch > ctx->max_batch)
+    return fail(MOA_ERR_INVALID_ARG, "ragged batch %d not in [0, max_batch=%d]", batch, ctx->max_batch);
+  if (!seq_len) return fail(MOA_ERR_INVALID_ARG, "seq_len is NULL");
+  const int G = ctx->G;
+  std::vector<int64_t> rn(seq_len, seq_len + batch);
+  std::vector<int32_t> rw((size_t)batch * ctx->nql);
+  for (int b = 0; b < batch; ++b) {
+    if (rn[b] < 1 || rn[b] > p.N)
+      return fail(MOA_ERR_INVALID_ARG, "seq_len[%d]=%lld not in [1, N=%lld]", b, (long long)rn[b],
+                  (long long)p.N);
+    for (int h = 0; h < ctx->nql; ++h) {
+      const int32_t w = window_per_seq_q_head
+                            ? window_per_seq_q_head[(size_t)b * ctx->Hq + ctx->g0 * G + h]
+                            : p.win_q[h];
+      if (w < 0 || w > p.win_g[h / G])
+        return fail(MOA_ERR_INVALID_ARG,
+                    "window[%d][%d]=%d not in [0, W_g=%d] (the cache capacity set by moa_set_spans)", b,
+                    ctx->g0 * G + h, w, p.win_g[h / G]);
+      if (w == 0 && p.n_sink < 1) return fail(MOA_ERR_INVALID_ARG, "W = 0 needs n_sink >= 1");
+      if (p.bshift >= 0 && (w & ((1 << p.bshift) - 1)))
+        return fail(MOA_ERR_INVALID_ARG, "window %d is not a multiple of the block %d", w, 1 << p.bshift);
+      rw[(size_t)b * ctx->nql + h] = w;
+    }
+  }
+  DeviceGuard dg(ctx->device);
+  free_ragged(p);
+  if (ctx->device >= 0) {
+    const size_t o_w = align16((size_t)batch * 8);
+    const size_t total = o_w + rw.size() * 4;
+    std::vector<unsigned char> host(total, 0);
+    std::memcpy(host.data(), rn.data(), rn.size() * 8);
+    std::memcpy(host.data() + o_w, rw.data(), rw.size() * 4);
+    void *d = nullptr;
+    cudaError_t e = cudaMalloc(&d, total);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(ragged tables)");
+    e = cudaMemcpy(d, host.data(), total, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(d);
+      return cuda_fail(e, "cudaMemcpy(ragged tables)");
+    }
+    p.d_rag = d;
+    p.d_seq_n = static_cast<const int64_t *>(d);
+    p.d_win_bq = reinterpret_cast<const int32_t *>(static_cast<unsigned char *>(d) + o_w);
+  }
+  p.rag_batch = batch;
+  p.rag_n = std::move(rn);
+  p.rag_win = std::move(rw);
+  p.next_pos = p.k_cache ? 0 : -1;
+  return ok();
+}
+
 moa_status moa_layer_cache_bytes(const moa_ctx *ctx, int layer, int batch, size_t *k_bytes,
                                  size_t *v_bytes) {
   moa_status st = check_layer(ctx, layer, true);
@@ -521,6 +597,13 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
   a.d_items2 = p.d_items2; a.n_items2 = (int)(p.items2.size() / 2);
   a.bshift = p.bshift;
+  if (p.rag_batch) {
+    if (batch != p.rag_batch)
+      return fail(MOA_ERR_SHAPE, "layer %d is ragged over %d sequences, prefill batch %d", layer, p.rag_batch,
+                  batch);
+    a.d_seq_n = p.d_seq_n;
+    a.d_win_bq = p.d_win_bq;
+  }
   int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_pp(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
   if (!fill) {
@@ -533,9 +616,10 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   c.ngl = ctx->ngl; c.d = ctx->d; c.n_sink = p.n_sink; c.batch = batch; c.N_or_pos = N;
   c.esize = (int)esize(ctx);
   c.max_region_rows = (int64_t)p.n_sink + *std::max_element(p.win_g.begin(), p.win_g.end());
+  c.d_seq_n = p.rag_batch ? p.d_seq_n : nullptr;
   e = moa::launch_cache_fill(c, stream);
   if (e) return cuda_fail((cudaError_t)e, "cache fill launch");
-  p.next_pos = N;
+  p.next_pos = p.rag_batch ? kRaggedPos : N;
   ctx->last_cache_write = layer;
   return ok();
 }
@@ -574,9 +658,15 @@ moa_status moa_cache_fill(moa_ctx *ctx, int layer, const void *k, const void *v,
   c.ngl = ctx->ngl; c.d = ctx->d; c.n_sink = p.n_sink; c.batch = batch; c.N_or_pos = N;
   c.esize = (int)esize(ctx);
   c.max_region_rows = (int64_t)p.n_sink + *std::max_element(p.win_g.begin(), p.win_g.end());
+  if (p.rag_batch) {
+    if (N != p.N || batch != p.rag_batch)
+      return fail(MOA_ERR_SHAPE, "layer %d is ragged: cache_fill needs N=%lld (padded) and batch %d", layer,
+                  (long long)p.N, p.rag_batch);
+    c.d_seq_n = p.d_seq_n;
+  }
   int e = moa::launch_cache_fill(c, stream);
   if (e) return cuda_fail((cudaError_t)e, "cache fill launch");
-  p.next_pos = N;
+  p.next_pos = p.rag_batch ? kRaggedPos : N;
   ctx->last_cache_write = layer;
   return ok();
 }
@@ -587,6 +677,8 @@ moa_status moa_kv_append(moa_ctx *ctx, int layer, const void *k_new, const void 
   if (st) return st;
   LayerPlan &p = ctx->layers[layer];
   if (!k_new || !v_new) return fail(MOA_ERR_INVALID_ARG, "k_new/v_new must be non-NULL");
+  if (p.rag_batch)
+    return fail(MOA_ERR_STATE, "layer %d is ragged: use moa_decode_step_fused_ragged", layer);
   if (pos != p.next_pos)
     return fail(MOA_ERR_STATE, "kv_append pos=%lld but layer %d expects %lld", (long long)pos, layer,
                 (long long)p.next_pos);
@@ -620,16 +712,28 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
                                 const void *v_new, void *o, int64_t q_batch_stride,
                                 int64_t kv_batch_stride, int64_t o_batch_stride, int batch,
                                 int64_t pos, float scale, float *lse_out, void *workspace,
-                                size_t ws_bytes, moa_stream_t stream, bool fused) {
+                                size_t ws_bytes, moa_stream_t stream, bool fused,
+                                const int64_t *d_pos = nullptr) {
   moa_status st = check_launch_common(ctx, layer, batch);
   if (st) return st;
   LayerPlan &p = ctx->layers[layer];
   if (!q || !o) return fail(MOA_ERR_INVALID_ARG, "q/o must be non-NULL");
   if (fused && (!k_new || !v_new)) return fail(MOA_ERR_INVALID_ARG, "k_new/v_new must be non-NULL");
-  int64_t expect = fused ? p.next_pos : p.next_pos - 1;
-  if (pos != expect || pos < 0)
-    return fail(MOA_ERR_STATE, "decode pos=%lld but layer %d expects %lld (append before decode)",
-                (long long)pos, layer, (long long)expect);
+  if (d_pos) {  // ragged: per-sequence positions in device memory (not checkable here)
+    if (p.rag_batch && batch != p.rag_batch)
+      return fail(MOA_ERR_SHAPE, "layer %d is ragged over %d sequences, decode batch %d", layer, p.rag_batch,
+                  batch);
+    if ((uintptr_t)d_pos & 7) return fail(MOA_ERR_INVALID_ARG, "pos array must be 8-byte aligned");
+    pos = 0;
+  } else {
+    if (p.rag_batch)
+      return fail(MOA_ERR_STATE, "layer %d is ragged: use moa_decode_step_fused_ragged", layer);
+    int64_t expect = fused ? p.next_pos : p.next_pos - 1;
+    if (pos != expect || pos < 0)
+      return fail(MOA_ERR_STATE, "decode pos=%lld but layer %d expects %lld (append before decode)",
+                  (long long)pos, layer, (long long)expect);
+  }
+  const int32_t *d_win_bq = p.rag_batch ? p.d_win_bq : nullptr;
   const int64_t d = ctx->d;
   if (q_batch_stride < ctx->nql * d || o_batch_stride < ctx->nql * d)
     return fail(MOA_ERR_SHAPE, "q/o batch stride smaller than local heads * head_dim");
@@ -657,12 +761,13 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
     m.d_g_off = p.d_g_off; m.d_win_g = p.d_win_g; m.d_win_q = p.d_win_q;
     m.ngl = ctx->ngl; m.G = ctx->G; m.d = ctx->d; m.n_sink = p.n_sink; m.batch = batch;
     m.pos = pos; m.scale = scale; m.lse = lse_out; m.ws_part = static_cast<float *>(workspace);
+    m.d_pos = d_pos; m.d_win_bq = d_win_bq;
     m.counters = p.d_counters;
     m.early_read = early_read_enabled() && ctx->last_cache_write != layer &&
                    ctx->last_cache_write != moa_ctx::kAllLayers;
     int e = moa::launch_decode_mma(m, stream);
     if (e) return cuda_fail((cudaError_t)e, "decode launch");
-    if (fused) p.next_pos = pos + 1;
+    if (fused && !d_pos) p.next_pos = pos + 1;
     ctx->last_cache_write = fused ? layer : -1;
     return ok();
   }
@@ -675,11 +780,12 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
   a.max_chunks_per_group = p.max_chunks_per_group;
   a.ngl = ctx->ngl; a.G = ctx->G; a.d = ctx->d; a.n_sink = p.n_sink; a.batch = batch;
   a.pos = pos; a.scale = scale; a.lse = lse_out;
+  a.d_pos = d_pos; a.d_win_bq = d_win_bq;
   a.ws_part = static_cast<float *>(workspace);
   a.counters = p.d_counters;
   int e = moa::launch_decode(a, ctx->dtype, fused, stream);
   if (e) return cuda_fail((cudaError_t)e, "decode launch");
-  if (fused) p.next_pos = pos + 1;
+  if (fused && !d_pos) p.next_pos = pos + 1;
   ctx->last_cache_write = fused ? layer : -1;
   return ok();
 }
@@ -699,6 +805,16 @@ moa_status moa_decode_step_fused(moa_ctx *ctx, int layer, const void *q, const v
                                  size_t ws_bytes, moa_stream_t stream) {
   return decode_common(ctx, layer, q, k_new, v_new, o, q_batch_stride, kv_batch_stride,
                        o_batch_stride, batch, pos, scale, lse_out, workspace, ws_bytes, stream, true);
+}
+
+moa_status moa_decode_step_fused_ragged(moa_ctx *ctx, int layer, const void *q, const void *k_new,
+                                        const void *v_new, void *o, int64_t q_batch_stride,
+                                        int64_t kv_batch_stride, int64_t o_batch_stride, int batch,
+                                        const int64_t *pos, float scale, float *lse_out, void *workspace,
+                                        size_t ws_bytes, moa_stream_t stream) {
+  if (!pos) return fail(MOA_ERR_INVALID_ARG, "pos array is NULL");
+  return decode_common(ctx, layer, q, k_new, v_new, o, q_batch_stride, kv_batch_stride, o_batch_stride,
+                       batch, 0, scale, lse_out, workspace, ws_bytes, stream, true, pos);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -157,6 +157,13 @@ struct LayerPlan {
   const int32_t *d_chunks = nullptr;
   const int32_t *d_g_chunk = nullptr;
   int *d_counters = nullptr;     // [max_batch, ngl] decode combine tickets (zeroed at upload)
+  // ragged batch (moa_set_ragged): per-sequence prompt length N_b and windows W_{b,h}
+  int rag_batch = 0;             // 0 = uniform batch
+  std::vector<int64_t> rag_n;    // [rag_batch]
+  std::vector<int32_t> rag_win;  // [rag_batch, nql] local heads
+  void *d_rag = nullptr;
+  const int64_t *d_seq_n = nullptr;
+  const int32_t *d_win_bq = nullptr;
   // TMA tensor maps (CUtensorMap, 128 B) over the bound K / V cache of this layer:
   // 2D [bound_batch * rows_per_seq rows, d], 64-row x 64-col boxes, 128B swizzle
   alignas(64) unsigned char kmap[128] = {};    // 64-row boxes
@@ -204,6 +211,8 @@ struct PrefillArgs {
   const int32_t *d_items2;  // (h_local, q_block) pairs of the two-tile kernel
   int n_items2;
   int bshift;               // -1 token mask, else log2(block size) (block mode)
+  const int64_t *d_seq_n;   // ragged: per-sequence N_b [batch] (null: every sequence has N)
+  const int32_t *d_win_bq;  // ragged: per-sequence windows [batch, nql] (null: d_win_q)
 };
 int launch_prefill_f32(const PrefillArgs &a, void *stream);
 int launch_prefill_bf16_pp(const PrefillArgs &a, void *stream);
@@ -219,6 +228,8 @@ struct CacheArgs {
   int64_t N_or_pos;
   int esize;
   int64_t max_region_rows;  // n_sink + max_g W_g
+  const int64_t *d_seq_n;   // fill, ragged: per-sequence N_b (null: N_or_pos)
+  const int64_t *d_pos;     // append, ragged: per-sequence positions (null: N_or_pos)
 };
 int launch_cache_fill(const CacheArgs &a, void *stream);
 int launch_kv_append(const CacheArgs &a, void *stream);
@@ -237,6 +248,8 @@ struct DecodeArgs {
   int n_chunks, max_chunks_per_group;
   int ngl, G, d, n_sink, batch;
   int64_t pos;
+  const int64_t *d_pos;     // ragged: per-sequence positions [batch] (null: pos); < 0 = inactive
+  const int32_t *d_win_bq;  // ragged: per-sequence windows [batch, nql] (null: d_win_q)
   float scale;
   float *lse;
   float *ws_part;       // [batch, n_chunks, G, d + 1] split partials (o, lse2)
@@ -261,6 +274,8 @@ struct DecodeMmaArgs {
   const int32_t *d_win_g, *d_win_q;
   int ngl, G, d, n_sink, batch;
   int64_t pos;
+  const int64_t *d_pos;        // ragged: per-sequence positions [batch] (null: pos); < 0 = inactive
+  const int32_t *d_win_bq;     // ragged: per-sequence windows [batch, nql] (null: d_win_q)
   float scale;
   float *lse;
   float *ws_part;

@@ -138,6 +138,20 @@ class MoAContext:
         else:
             check(self.lib.moa_set_spans(self.ctx, layer, w, int(n_sink), int(N)), "moa_set_spans")
 
+    def set_ragged(self, layer: int, seq_len: Optional[Sequence[int]], windows=None):
+        """moa_set_ragged: per-sequence prompt lengths N_b and windows W_{b,h} ([B][Hq] nested
+        sequence or array, all heads; None = the layer's windows).  seq_len None clears."""
+        if seq_len is None:
+            check(self.lib.moa_set_ragged(self.ctx, layer, 0, None, None), "moa_set_ragged")
+            return
+        B = len(seq_len)
+        n = (c_int64 * B)(*[int(x) for x in seq_len])
+        w = None
+        if windows is not None:
+            flat = [int(x) for row in windows for x in row]
+            w = (c_int32 * len(flat))(*flat)
+        check(self.lib.moa_set_ragged(self.ctx, layer, B, n, w), "moa_set_ragged")
+
     def cache_bytes(self, batch: int):
         k, v = c_size_t(), c_size_t()
         check(self.lib.moa_cache_bytes(self.ctx, batch, byref(k), byref(v)), "moa_cache_bytes")
@@ -277,6 +291,19 @@ class MoAContext:
                                              _ptr(lse), _ptr(workspace),
                                              workspace.numel() * workspace.element_size(), _stream(stream)),
               "moa_decode_step_fused")
+
+    def decode_step_fused_ragged(self, layer: int, q, k_new, v_new, o, pos, scale: float, workspace, lse=None,
+                                 stream=None):
+        """moa_decode_step_fused_ragged: pos is a device int64 tensor [B] (per-sequence positions,
+        < 0 = inactive), read by the kernel; the caller advances it."""
+        B = q.shape[0]
+        assert pos.dtype == torch.int64 and pos.is_contiguous() and pos.numel() >= B and pos.device == q.device
+        check(self.lib.moa_decode_step_fused_ragged(self.ctx, layer, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(o),
+                                                    q.stride(0), k_new.stride(0), o.stride(0), B, _ptr(pos),
+                                                    float(scale), _ptr(lse), _ptr(workspace),
+                                                    workspace.numel() * workspace.element_size(),
+                                                    _stream(stream)),
+              "moa_decode_step_fused_ragged")
 
     # ---- cache inspection (tests) --------------------------------------------------------
     def cache_rows(self, layer: int, b: int, g: int, which: str = "k") -> torch.Tensor:

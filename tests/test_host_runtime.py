@@ -270,3 +270,39 @@ def test_bench_algorithmic_work_matches_oracle_counts():
         p = N + T - 1  # the ring is full at the last decode position of the step
         rows = sum(len(oracle.resident_positions(p, s, int(w))) for w in wg)
         assert dec == rows * d * 2 * 2 + H * d * 2 * 2 + len(wg) * d * 2 * 2 * 2
+
+
+def test_set_ragged_validation(moa):
+    """moa_set_ragged: N_b in [1, N], 0 <= W_{b,h} <= W_g of the head's group (cache
+    capacity), W = 0 needs sinks, block multiples in block mode; a sharded context
+    keeps its heads' columns; batch 0 clears; set_spans clears."""
+    from paper_2406_14909_b200 import MoAError
+    W = [8, 3, 0, 5]  # groups (G=2): W_g = 8, 5
+    c = _ctx(moa, Hq=4, Hkv=2, B=3)
+    c.set_spans(0, W, 2, 100)
+    c.set_ragged(0, [100, 40, 1], [[8, 3, 0, 5], [2, 8, 5, 1], [0, 0, 0, 0]])
+    c.set_ragged(0, [7, 9])           # windows default to the layer's
+    c.set_ragged(0, None)             # back to uniform
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_ragged(0, [101])        # longer than the padded length
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_ragged(0, [0])
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_ragged(0, [50], [[9, 0, 0, 0]])   # beyond W_g = 8
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_ragged(0, [50], [[0, 0, 6, 0]])   # beyond W_g = 5 of group 1
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c.set_ragged(0, [1, 1, 1, 1])           # more than max_batch
+    c0 = _ctx(moa, Hq=2, Hkv=1, B=1)
+    c0.set_spans(0, [4, 4], 0, 10)
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        c0.set_ragged(0, [5], [[0, 4]])         # W = 0 without sinks
+    cb = _ctx(moa, Hq=2, Hkv=1, B=1)
+    cb.set_spans(0, [128, 64], 64, 512, block=64)
+    cb.set_ragged(0, [300], [[64, 0]])
+    with pytest.raises(MoAError, match="INVALID_ARG"):
+        cb.set_ragged(0, [300], [[100, 0]])     # not a block multiple
+    # shard (groups [1, 2)): only its heads' columns are checked against its W_g
+    cs = _ctx(moa, Hq=4, Hkv=2, B=2, g0=1, g1=2)
+    cs.set_spans(0, W, 2, 100)
+    cs.set_ragged(0, [10, 20], [[99, 99, 5, 0], [99, 99, 1, 2]])

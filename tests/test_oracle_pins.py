@@ -434,3 +434,74 @@ def test_rule_losses_full_rule_zero_and_nesting():
     cnt = lambda i: min(b, N - i * b)
     want = sum(E[:, ib, jb] * cnt(ib) * cnt(jb) for ib in range(nb) for jb in range(1, ib + 1))
     assert np.allclose(Ls[:, 0], want, rtol=0, atol=1e-10)
+
+
+# --- ragged batches -------------------------------------
+
+def test_ragged_full_span_sequences_are_textbook_causal():
+    """Ragged batch whose every window covers its sequence: sequence b is plain causal
+    attention over its own first N_b rows (torch SDPA, fp64), whatever the padding holds."""
+    B, N, Hkv, G, d, s = 3, 37, 2, 2, 8, 2
+    Hq = Hkv * G
+    Q, K, V = _rand((B, N, Hq, d), 40), _rand((B, N, Hkv, d), 41), _rand((B, N, Hkv, d), 42)
+    lens = [37, 20, 1]
+    for b, n in enumerate(lens):  # garbage in the padding must not matter
+        Q[b, n:] = 1e6
+        K[b, n:] = -1e6
+        V[b, n:] = np.nan
+    wins = [[n] * Hq for n in lens]
+    O, L = oracle.prefill_ragged(Q, K, V, lens, wins, s, 0.3)
+    for b, n in enumerate(lens):
+        q = torch.from_numpy(Q[b:b + 1, :n]).permute(0, 2, 1, 3)
+        k = torch.from_numpy(K[b:b + 1, :n]).permute(0, 2, 1, 3).repeat_interleave(G, dim=1)
+        v = torch.from_numpy(V[b:b + 1, :n]).permute(0, 2, 1, 3).repeat_interleave(G, dim=1)
+        ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, scale=0.3)
+        assert np.max(np.abs(O[b, :n] - ref.permute(0, 2, 1, 3).numpy()[0])) < 1e-12
+        assert np.all(np.isnan(O[b, n:])) and np.all(np.isnan(L[b, :, n:]))
+
+
+def test_ragged_windows_match_dense_mask_of_truncated_sequence():
+    """Per-sequence windows (Eq. 2 at each N_b): each sequence equals the dense-mask
+    formulation run on that sequence alone."""
+    B, N, Hkv, G, d, s = 3, 30, 1, 3, 4, 3
+    Q, K, V = _rand((B, N, Hkv * G, d), 43), _rand((B, N, Hkv, d), 44), _rand((B, N, Hkv, d), 45)
+    lens = [30, 17, 9]
+    alpha, beta = [4.0, 8.0, 2.0], [0.2, 0.0, 0.5]
+    wins = [[oracle.window_of(oracle.span_of(a, bt, n), s) for a, bt in zip(alpha, beta)] for n in lens]
+    assert wins[1] != wins[0]  # the spans do depend on the sequence length
+    O, L = oracle.prefill_ragged(Q, K, V, lens, wins, s, 0.7)
+    for b, n in enumerate(lens):
+        O2, L2 = oracle.prefill_dense_mask(Q[b:b + 1, :n], K[b:b + 1, :n], V[b:b + 1, :n], wins[b], s, 0.7)
+        assert np.max(np.abs(O[b, :n] - O2[0])) < 1e-13
+        assert np.max(np.abs(L[b, :, :n] - L2[0])) < 1e-12
+
+
+def test_ragged_decode_rows_and_inactive_sequences():
+    """decode_ragged at per-sequence positions == row p_b of the dense-mask prefill of
+    sequence b; an inactive sequence (p < 0) gives O = 0, LSE = -inf."""
+    B, N, Hkv, G, d, s = 3, 25, 2, 2, 4, 2
+    Hq = Hkv * G
+    Q, K, V = _rand((B, N, Hq, d), 46), _rand((B, N, Hkv, d), 47), _rand((B, N, Hkv, d), 48)
+    wins = [[3, 0, 7, 30], [1, 2, 3, 4], [5, 5, 5, 5]]
+    pos = [24, 11, -1]
+    o, l = oracle.decode_ragged(Q[np.arange(B), np.maximum(pos, 0)], K, V, pos, wins, s, 0.5)
+    for b in range(2):
+        p = pos[b]
+        O2, L2 = oracle.prefill_dense_mask(Q[b:b + 1, :p + 1], K[b:b + 1, :p + 1], V[b:b + 1, :p + 1], wins[b],
+                                           s, 0.5)
+        assert np.max(np.abs(o[b] - O2[0, p])) < 1e-13
+        assert np.max(np.abs(l[b] - L2[0, :, p])) < 1e-12
+    assert np.all(o[2] == 0) and np.all(np.isneginf(l[2]))
+
+
+def test_spans_shrink_with_length_for_nonnegative_beta():
+    """Eq. 2 with beta >= 0: the span at N_b <= N never exceeds the span at N, so the
+    cache capacity resolved at the padded length holds every sequence's window
+    (the moa_set_ragged precondition)."""
+    for a in (0.0, 64.0, 1000.0, 5000.0):
+        for bt in (0.0, 0.1, 0.5, 1.0):
+            prev = -1
+            for n in range(1, 3000, 37):
+                w = oracle.window_of(oracle.span_of(a, bt, n), 64)
+                assert w >= prev
+                prev = w
