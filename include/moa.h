@@ -153,7 +153,9 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
  *   - moa_prefill / moa_prefill_attn / moa_cache_fill take N = the padded length and
  *     batch = this batch; sequence b is the prompt of its first N_b rows under its own
  *     windows; output / lse rows i >= N_b are not written.  The cache fill stores
- *     positions < N_b.
+ *     positions < N_b.  The padding rows [N_b, N) of q/k/v must hold FINITE values
+ *     (any, e.g. zeros): the kernels tile against N and give padding keys probability
+ *     exactly 0, and 0 * Inf/NaN would poison a real row.
  *   - decode goes through moa_decode_step_fused_ragged (the uniform append / decode
  *     calls return MOA_ERR_STATE).
  * Errors: MOA_ERR_INVALID_ARG (ranges above), nothing is changed on error.

@@ -83,7 +83,7 @@ struct PpParams {
   float scale_log2;
   int bshift;            // -1 token mask, else log2(block size) (block mode)
   const int32_t *win_q;
-  const int32_t *items;  // (q-head, q-block) pairs, LPT order
+  const int32_t *items;  // (q-head, q-block) pairs, LPT order; ragged: (h | b << 16, q-block)
   const int64_t *seq_n;  // ragged: per-sequence N_b (null: N)
   const int32_t *win_bq; // ragged: per-sequence windows [batch, nql] (null: win_q)
 };
@@ -107,20 +107,31 @@ __device__ __forceinline__ int bshift_of(const PpParams &p) {
 
 struct PItem {
   int b, h, W;
-  int64_t i0, N;  // N: this sequence's length (ragged) or p.N; the item is empty iff i0 >= N
+  int64_t i0, N;
   BlockTiles bt;
 };
 
 template <int BS, bool RAG>
 __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
   PItem it;
-  const int wi = idx / p.batch;
-  it.b = idx - wi * p.batch;
-  it.h = p.items[2 * wi];
-  it.i0 = (int64_t)p.items[2 * wi + 1] * (2 * kM);
-  // ragged batches are a separate instantiation: the uniform kernel keeps its registers
-  it.N = RAG ? p.seq_n[it.b] : p.N;
-  it.W = RAG ? p.win_bq[(int64_t)it.b * p.nql + it.h] : p.win_q[it.h];
+  if (RAG) {  // ragged list: (h | b << 16, q-block) of real items only, LPT order
+    const int e = p.items[2 * idx];
+    it.b = e >> 16;
+    it.h = e & 0xffff;
+    it.i0 = (int64_t)p.items[2 * idx + 1] * (2 * kM);
+    // 32-bit index from the live (b, h): W stays cheap to re-derive (a 64-bit index or a W
+    // carried in the item cost the softmax 45-100% through register spills)
+    it.W = p.win_bq[it.b * p.nql + it.h];
+  } else {
+    const int wi = idx / p.batch;
+    it.b = idx - wi * p.batch;
+    it.h = p.items[2 * wi];
+    it.i0 = (int64_t)p.items[2 * wi + 1] * (2 * kM);
+  }
+  // ragged: tiles are scheduled against the padded length (rows past N_b are computed on the
+  // finite padding and not stored, see the epilogues), only the windows are per sequence
+  it.N = p.N;
+  if (!RAG) it.W = p.win_q[it.h];
   it.bt = kv_block_tiles(it.i0, it.N, it.W, p.n_sink, bshift_of<BS>(p));
   return it;
 }
@@ -238,11 +249,8 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
     PPTR(j ? 3 : 0, 3)
     asm volatile("bar.arrive %0, 64;" ::"r"(kBarTurn0 + (j ^ 1)) : "memory");
   };
-  bool any = false;  // a CTA whose items all lie past their ragged sequences' ends has no turns
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
     const PItem it = get_pitem<BS, RAG>(p, idx);
-    if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
-    any = true;
     const bool mine = j == 0 || it.bt.has1;  // this q tile has rows in the item
     const TileRanges r = j ? it.bt.r[1] : it.bt.r[0];
     const int last_t = r.b1 > r.b0 ? r.b1 - 1 : r.a1 - 1;  // its S releases Q_j, its PV completes O_j
@@ -325,7 +333,7 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
   }
   // the other warp's last hand-over to this one is never taken: drain it, so the named
   // barrier is clean for the next kernel on this SM
-  if (j == 0 && any) asm volatile("bar.sync %0, 64;" ::"r"(kBarTurn0) : "memory");
+  if (j == 0) asm volatile("bar.sync %0, 64;" ::"r"(kBarTurn0) : "memory");
 }
 
 // ------------------------------------------------------------------------------------------
@@ -346,7 +354,6 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
   int ic = 0;  // items of this tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
     const PItem it = get_pitem<BS, RAG>(p, idx);
-    if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
     if (j == 1 && !it.bt.has1) continue;
     const int64_t ti0 = it.i0 + j * kM;                     // first row of this q tile
     const int64_t ti1 = (ti0 + kM < it.N ? ti0 + kM : it.N) - 1;  // last real row
@@ -451,6 +458,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
     ++ic;
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
+    const bool store = i <= ti1 && (!RAG || i < p.seq_n[it.b]);  // ragged: rows past N_b are not outputs
     __nv_bfloat16 *orow =
         static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride + (int64_t)it.h * D;
 #pragma unroll
@@ -458,7 +466,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       float r[32];
       tmem_ld32_f(ocol + c * 32, r);
       tmem_wait_ld();
-      if (i <= ti1) {
+      if (store) {
         uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
 #pragma unroll
         for (int v4 = 0; v4 < 4; ++v4) {
@@ -471,7 +479,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
         }
       }
     }
-    if (p.lse && i <= ti1)
+    if (p.lse && store)
       p.lse[((int64_t)it.b * p.nql + it.h) * p.N + i] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
     tc_fence_before();
     __syncwarp();
@@ -505,7 +513,6 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
   int ic[2] = {0, 0};  // items per tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
     const PItem it = get_pitem<BS, RAG>(p, idx);
-    if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
     const bool has1 = it.bt.has1;
     float m_used[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     const int ns = it.bt.steps();
@@ -627,6 +634,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
       pair_sync();  // both read before the slot is reused by the next item's row max
       tc_fence_after();
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      const bool store = i <= ti1 && (!RAG || i < p.seq_n[it.b]);  // ragged: rows past N_b are not outputs
       __nv_bfloat16 *orow = static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride +
                             (int64_t)it.h * D + hf * kOCols;
 #pragma unroll
@@ -634,7 +642,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
         float r[32];
         tmem_ld32_f(ocol + c * 32, r);
         tmem_wait_ld();
-        if (i <= ti1) {
+        if (store) {
           uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
 #pragma unroll
           for (int v4 = 0; v4 < 4; ++v4) {
@@ -647,7 +655,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
           }
         }
       }
-      if (p.lse && i <= ti1 && hf == 0)
+      if (p.lse && store && hf == 0)
         p.lse[((int64_t)it.b * p.nql + it.h) * p.N + i] =
             lt > 0.f ? (m_used[j] + __log2f(lt)) * kLn2 : -INFINITY;
       tc_fence_before();
@@ -671,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t q_smem = smem_base;                        // Q0, Q1
   const uint32_t k_smem = q_smem + 2 * C::kTileBytes;       // kNK tiles
   const uint32_t v_smem = k_smem + C::kNK * C::kTileBytes;  // kNV tiles
-  const int total = p.n_items * p.batch;
+  const int total = RAG ? p.n_items : p.n_items * p.batch;
 
   if (tid == 0) {
     for (int j = 0; j < 2; ++j) {
@@ -716,8 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int T = 0;
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
         const PItem it = get_pitem<BS, RAG>(p, idx);
-        if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
-        const int g = it.h / p.G;
+            const int g = it.h / p.G;
         const int ns = it.bt.steps();
         for (int k = 0; k < ns; ++k) {
           int t;
@@ -746,8 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int qc[2] = {0, 0};
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
         const PItem it = get_pitem<BS, RAG>(p, idx);
-        if (RAG && it.i0 >= it.N) continue;  // ragged: past this sequence's end (every role skips it)
-        for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < 2; ++j) {
           if (j == 1 && !it.bt.has1) continue;
           if (qc[j] > 0) mbar_wait(smem_u32(&bars.q_empty[j]), (qc[j] - 1) & 1);
           ++qc[j];
@@ -804,7 +810,7 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   p.o_row_stride = a.o_row_stride;
   p.N = a.N;
   p.batch = a.batch;
-  p.n_items = a.n_items2;
+  p.n_items = a.d_seq_n ? a.n_items_rag : a.n_items2;
   p.nql = a.nql;
   p.G = a.G;
   p.n_sink = a.n_sink;
@@ -813,7 +819,7 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   p.win_q = a.d_win_q;
   p.seq_n = a.d_seq_n;
   p.win_bq = a.d_win_bq;
-  p.items = a.d_items2;
+  p.items = a.d_seq_n ? a.d_items_rag : a.d_items2;
   // the token mask (bshift < 0) and the block mask are separate instantiations, so the
   // token path carries no block-mode arithmetic
   const bool rag = p.seq_n != nullptr;
@@ -823,7 +829,7 @@ int launch_pp(const PrefillArgs &a, void *stream) {
                                      : prefill_pp_kernel<D, kBsRuntime, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return (int)e;
-  const int total = p.n_items * p.batch;
+  const int total = rag ? p.n_items : p.n_items * p.batch;
   const int grid = total < num_sms_pp() ? total : num_sms_pp();
   kern<<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, p);
   return (int)cudaGetLastError();

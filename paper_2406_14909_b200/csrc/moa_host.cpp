@@ -87,6 +87,8 @@ void free_ragged(LayerPlan &p) {
   p.rag_batch = 0;
   p.rag_n.clear();
   p.rag_win.clear();
+  p.rag_items2.clear();
+  p.d_rag_items2 = nullptr;
 }
 
 void free_tables(LayerPlan &p) {
@@ -396,6 +398,8 @@ moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq
   if (batch < 0 || batch > ctx->max_batch)
     return fail(MOA_ERR_INVALID_ARG, "ragged batch %d not in [0, max_batch=%d]", batch, ctx->max_batch);
   if (!seq_len) return fail(MOA_ERR_INVALID_ARG, "seq_len is NULL");
+  if (ctx->nql > 0xffff || batch > 0x7fff)
+    return fail(MOA_ERR_UNSUPPORTED, "ragged work items pack (h, b) into 16 + 15 bits");
   const int G = ctx->G;
   std::vector<int64_t> rn(seq_len, seq_len + batch);
   std::vector<int32_t> rw((size_t)batch * ctx->nql);
@@ -417,14 +421,50 @@ moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq
       rw[(size_t)b * ctx->nql + h] = w;
     }
   }
+  // two-tile prefill items of the real (b, h, q_block) work only (the kernel tiles against the
+  // padded N, so a block costs what it costs there), in the uniform order of moa_set_spans:
+  // heads by total kv-tile count over the batch, heaviest first; inside a head the items
+  // heaviest first, q block then sequence (a uniform batch gives exactly the uniform list)
+  struct It { int b, h, qb, cnt; int64_t hcost; };
+  std::vector<It> its;
+  for (int h = 0; h < ctx->nql; ++h) {
+    const size_t first = its.size();
+    int64_t hc = 0;
+    for (int b = 0; b < batch; ++b) {
+      const int nqb = (int)((rn[b] + 2 * moa::kTile - 1) / (2 * moa::kTile));
+      for (int qb = 0; qb < nqb; ++qb) {
+        const moa::BlockTiles bt =
+            moa::kv_block_tiles((int64_t)qb * 2 * moa::kTile, p.N, rw[(size_t)b * ctx->nql + h], p.n_sink,
+                                p.bshift);
+        const int c = bt.r[0].count() + (bt.has1 ? bt.r[1].count() : 0);
+        hc += c;
+        its.push_back({b, h, qb, c, 0});
+      }
+    }
+    for (size_t k = first; k < its.size(); ++k) its[k].hcost = hc;
+  }
+  std::stable_sort(its.begin(), its.end(), [](const It &x, const It &y) {
+    if (x.hcost != y.hcost) return x.hcost > y.hcost;
+    if (x.h != y.h) return x.h < y.h;
+    if (x.cnt != y.cnt) return x.cnt > y.cnt;
+    if (x.qb != y.qb) return x.qb < y.qb;
+    return x.b < y.b;
+  });
+  std::vector<int32_t> ri(its.size() * 2);
+  for (size_t i = 0; i < its.size(); ++i) {
+    ri[2 * i] = its[i].h | (its[i].b << 16);
+    ri[2 * i + 1] = its[i].qb;
+  }
   DeviceGuard dg(ctx->device);
   free_ragged(p);
   if (ctx->device >= 0) {
     const size_t o_w = align16((size_t)batch * 8);
-    const size_t total = o_w + rw.size() * 4;
+    const size_t o_i = align16(o_w + rw.size() * 4);
+    const size_t total = o_i + ri.size() * 4;
     std::vector<unsigned char> host(total, 0);
     std::memcpy(host.data(), rn.data(), rn.size() * 8);
     std::memcpy(host.data() + o_w, rw.data(), rw.size() * 4);
+    std::memcpy(host.data() + o_i, ri.data(), ri.size() * 4);
     void *d = nullptr;
     cudaError_t e = cudaMalloc(&d, total);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(ragged tables)");
@@ -436,7 +476,9 @@ moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq
     p.d_rag = d;
     p.d_seq_n = static_cast<const int64_t *>(d);
     p.d_win_bq = reinterpret_cast<const int32_t *>(static_cast<unsigned char *>(d) + o_w);
+    p.d_rag_items2 = reinterpret_cast<const int32_t *>(static_cast<unsigned char *>(d) + o_i);
   }
+  p.rag_items2 = std::move(ri);
   p.rag_batch = batch;
   p.rag_n = std::move(rn);
   p.rag_win = std::move(rw);
@@ -603,6 +645,8 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
                   batch);
     a.d_seq_n = p.d_seq_n;
     a.d_win_bq = p.d_win_bq;
+    a.d_items_rag = p.d_rag_items2;
+    a.n_items_rag = (int)(p.rag_items2.size() / 2);
   }
   int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_pp(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");

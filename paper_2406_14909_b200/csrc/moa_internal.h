@@ -161,7 +161,9 @@ struct LayerPlan {
   int rag_batch = 0;             // 0 = uniform batch
   std::vector<int64_t> rag_n;    // [rag_batch]
   std::vector<int32_t> rag_win;  // [rag_batch, nql] local heads
+  std::vector<int32_t> rag_items2;  // two-tile prefill items of the ragged batch (h | b << 16, q_block)
   void *d_rag = nullptr;
+  const int32_t *d_rag_items2 = nullptr;
   const int64_t *d_seq_n = nullptr;
   const int32_t *d_win_bq = nullptr;
   // TMA tensor maps (CUtensorMap, 128 B) over the bound K / V cache of this layer:
@@ -213,6 +215,8 @@ struct PrefillArgs {
   int bshift;               // -1 token mask, else log2(block size) (block mode)
   const int64_t *d_seq_n;   // ragged: per-sequence N_b [batch] (null: every sequence has N)
   const int32_t *d_win_bq;  // ragged: per-sequence windows [batch, nql] (null: d_win_q)
+  const int32_t *d_items_rag;  // ragged two-tile items (h | b << 16, q_block), real items only, LPT
+  int n_items_rag;
 };
 int launch_prefill_f32(const PrefillArgs &a, void *stream);
 int launch_prefill_bf16_pp(const PrefillArgs &a, void *stream);

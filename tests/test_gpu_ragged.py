@@ -53,6 +53,10 @@ def _prefill_case(moa, dtype, B, N, lens, Hq, Hkv, d, s, alpha, beta, seed, bloc
     Q = normal((B, N, Hq, d), seed, dtype)
     K = normal((B, N, Hkv, d), seed + 1, dtype)
     V = normal((B, N, Hkv, d), seed + 2, dtype)
+    for b, n in enumerate(lens):  # padding: any finite values (header contract), here large ones
+        Q[b, n:] = 3.0e4
+        K[b, n:] = -3.0e4
+        V[b, n:] = 3.0e4
     o = torch.full((B, N, Hq, d), 7.0, dtype=dtype, device=dev)  # sentinel: rows >= N_b untouched
     lse = torch.full((B, Hq, N), 7.0, dtype=torch.float32, device=dev)
     tau = 1 / math.sqrt(d)
