@@ -172,3 +172,70 @@ def test_ragged_layer_refuses_uniform_decode(moa):
         ctx.decode_step_fused(0, q, kn, kn, q.clone(), 0, 0.1, ws)
     with pytest.raises(MoAError, match="STATE"):
         ctx.kv_append(0, kn, kn, 0)
+
+
+def test_c2_full_layer_ragged_prefill_and_decode(moa):
+    """A full C2 layer (B=8, N=4096, 32 heads, d=128, 64 sinks) as a ragged batch with
+    N_b uniform in [N/4, N] and Eq. 2 windows at N_b (the launch configuration of
+    tools/time_ragged.py): sampled rows of every sequence vs oracle.prefill_rows on the
+    truncated sequence, the ragged cache images bitwise, then 3 fused ragged decode steps
+    vs oracle.decode on sampled sequences."""
+    from moa_workloads import CONFIGS, prefill_qkv, rule_table
+    cfg = CONFIGS["C2"]
+    dev = torch.device("cuda")
+    B, N, s, d, layer = cfg.batch, cfg.N, cfg.n_sink, cfg.head_dim, 20
+    t = rule_table("C2")
+    rng = np.random.default_rng(7)
+    lens = rng.integers(N // 4, N + 1, size=B).tolist()
+    lens[1] = N
+    cap = moa.resolve_spans(t["alpha"][layer], t["beta"][layer], N, s)
+    wins = [[min(w, c) for w, c in zip(moa.resolve_spans(t["alpha"][layer], t["beta"][layer], n, s), cap)]
+            for n in lens]
+    ctx = moa.MoAContext(1, cfg.hq, cfg.hkv, d, B)
+    ctx.set_spans(0, cap, s, N)
+    ctx.set_ragged(0, lens, wins)
+    ctx.alloc_cache(B)
+    q, k, v = prefill_qkv(cfg, layer, device=dev)
+    o = torch.empty_like(q)
+    lse = torch.empty(B, cfg.hq, N, dtype=torch.float32, device=dev)
+    tau = 1 / math.sqrt(d)
+    ctx.prefill(0, q, k, v, o, tau, lse)
+    torch.cuda.synchronize()
+    for b in (0, 1, B - 1):
+        n = lens[b]
+        rows = []
+        for h in range(0, cfg.hq, 3):
+            W = wins[b][h]
+            base = {0, s - 1, s, W - 1, W, W + 1, 127, 128, n - 2, n - 1}
+            base |= set(int(x) for x in rng.integers(0, n, 4))
+            rows += [(0, h, i) for i in sorted(base) if 0 <= i < n]
+        O, L = oracle.prefill_rows(f64(q[b:b + 1, :n]), f64(k[b:b + 1, :n]), f64(v[b:b + 1, :n]), wins[b], s, tau,
+                                   rows)
+        got = np.stack([f64(o[b, i, h]) for _, h, i in rows])
+        gl = np.array([float(lse[b, h, i]) for _, h, i in rows])
+        assert np.abs(got - O).max() < 2e-2, b
+        assert np.abs(gl - L).max() < 2e-3, b
+        wg = oracle.group_windows(cap, cfg.group)
+        img = oracle.cache_image(bits(k[b:b + 1, :n]), bits(v[b:b + 1, :n]), n - 1, wg, s)
+        for g in range(0, cfg.hkv, 5):
+            Ki, Vi, valid = img[(0, g)]
+            assert np.array_equal(bits(ctx.cache_rows(0, b, g, "k"))[valid], Ki[valid]), (b, g)
+            assert np.array_equal(bits(ctx.cache_rows(0, b, g, "v"))[valid], Vi[valid]), (b, g)
+    # decode: new tokens at positions N_b (history = prompt rows + the new rows)
+    ws = ctx.alloc_workspace(B)
+    pos = torch.tensor(lens, dtype=torch.int64, device=dev)
+    od = torch.empty(B, cfg.hq, d, dtype=torch.bfloat16, device=dev)
+    T = 3
+    kq = normal((T, B, cfg.hq, d), 77, torch.bfloat16)
+    kn = normal((T, B, cfg.hkv, d), 78, torch.bfloat16)
+    vn = normal((T, B, cfg.hkv, d), 79, torch.bfloat16)
+    for t_ in range(T):
+        ctx.decode_step_fused_ragged(0, kq[t_].to(dev), kn[t_].to(dev), vn[t_].to(dev), od, pos, tau, ws)
+        torch.cuda.synchronize()
+        for b in (0, 1, B - 1):
+            n = lens[b]
+            Kh = np.concatenate([f64(k[b:b + 1, :n]), f64(kn[:t_ + 1, b]).reshape(1, t_ + 1, cfg.hkv, d)], 1)
+            Vh = np.concatenate([f64(v[b:b + 1, :n]), f64(vn[:t_ + 1, b]).reshape(1, t_ + 1, cfg.hkv, d)], 1)
+            ref, _ = oracle.decode(f64(kq[t_, b:b + 1]), Kh, Vh, n + t_, wins[b], s, tau)
+            assert np.abs(f64(od[b:b + 1]) - ref).max() < 2e-2, (t_, b)
+        pos += 1
