@@ -239,3 +239,45 @@ def test_c2_full_layer_ragged_prefill_and_decode(moa):
             ref, _ = oracle.decode(f64(kq[t_, b:b + 1]), Kh, Vh, n + t_, wins[b], s, tau)
             assert np.abs(f64(od[b:b + 1]) - ref).max() < 2e-2, (t_, b)
         pos += 1
+
+
+def test_ragged_kv_sharded_contexts_on_one_gpu(moa):
+    """Two contexts serving kv-groups [0,2) and [2,4) of a ragged batch (each keeps its
+    heads' columns of the full [B][Hq] window table), on head-sliced views: prefill and a
+    fused ragged decode step, concatenated by heads, equal the oracle for all heads."""
+    from paper_2406_14909_b200 import dist as mdist
+    dev = torch.device("cuda")
+    B, N, Hq, Hkv, d, s = 3, 300, 8, 4, 128, 4
+    cap = [3, 200, 0, 77, 128, 129, 1, 300]
+    lens = [300, 140, 33]
+    wins = [cap, [3, 100, 0, 60, 128, 20, 1, 140], [0, 33, 0, 5, 10, 29, 1, 33]]
+    G = Hq // Hkv
+    q = normal((B, N, Hq, d), 311, torch.bfloat16)
+    k = normal((B, N + 1, Hkv, d), 312, torch.bfloat16)
+    v = normal((B, N + 1, Hkv, d), 313, torch.bfloat16)
+    qd = normal((B, Hq, d), 314, torch.bfloat16)
+    qg, qdg = q.to(dev), qd.to(dev)
+    kg, vg = k[:, :N].contiguous().to(dev), v[:, :N].contiguous().to(dev)
+    # decode token of sequence b sits at position N_b
+    kd = torch.stack([k[b, n] for b, n in enumerate(lens)]).to(dev)
+    vd = torch.stack([v[b, n] for b, n in enumerate(lens)]).to(dev)
+    o = torch.empty_like(qg)
+    od = torch.empty_like(qdg)
+    pos = torch.tensor(lens, dtype=torch.int64, device=dev)
+    tau = 1 / math.sqrt(d)
+    for sh in mdist.plan_shards(2, Hkv, B, "kv"):
+        ctx = mdist.make_context(sh, 1, Hq, Hkv, d, device=0)
+        ctx.set_spans(0, cap, s, N)
+        ctx.set_ragged(0, lens, wins)
+        ctx.alloc_cache(B)
+        ws = ctx.alloc_workspace(B)
+        ctx.prefill(0, mdist.local_slice_q(qg, sh, G), mdist.local_slice_kv(kg, sh), mdist.local_slice_kv(vg, sh),
+                    mdist.local_slice_q(o, sh, G), tau)
+        ctx.decode_step_fused_ragged(0, mdist.local_slice_q(qdg, sh, G), mdist.local_slice_kv(kd, sh),
+                                     mdist.local_slice_kv(vd, sh), mdist.local_slice_q(od, sh, G), pos, tau, ws)
+    torch.cuda.synchronize()
+    O, _ = oracle.prefill_ragged(f64(q), f64(k[:, :N]), f64(v[:, :N]), lens, wins, s, tau)
+    for b, n in enumerate(lens):
+        assert np.abs(f64(o)[b, :n] - O[b, :n]).max() < 2e-2, b
+    Od, _ = oracle.decode_ragged(f64(qd), f64(k), f64(v), lens, wins, s, tau)
+    assert np.abs(f64(od) - Od).max() < 2e-2
