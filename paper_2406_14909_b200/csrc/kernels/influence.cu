@@ -84,7 +84,10 @@ __device__ __forceinline__ void block_products(const __nv_bfloat16 *ks, const __
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreadsInf) influence_kernel(InfluenceArgs a) {
+#ifndef MOA_INF_MIN_BLOCKS
+#define MOA_INF_MIN_BLOCKS 3  // 3 CTAs (12 warps) per SM: 148.8 vs 127.9 TFLOP/s at 1 (180 regs, 2 CTAs), 105 at 4 (spills)
+#endif
+__global__ void __launch_bounds__(kThreadsInf, MOA_INF_MIN_BLOCKS) influence_kernel(InfluenceArgs a) {
   extern __shared__ __align__(16) uint8_t inf_dsm[];
   __nv_bfloat16 *kv_s = reinterpret_cast<__nv_bfloat16 *>(inf_dsm);  // [stage][K | V][kBuf]
   __shared__ float red[4];
