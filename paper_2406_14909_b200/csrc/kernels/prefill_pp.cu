@@ -84,6 +84,7 @@ struct PpParams {
   int bshift;            // -1 token mask, else log2(block size) (block mode)
   const int32_t *win_q;
   const int32_t *items;  // (q-head, q-block) pairs, LPT order; ragged: (h | b << 16, q-block)
+  int o_v8;              // output rows 32-byte aligned: 256-bit stores in the epilogue
   const int64_t *seq_n;  // ragged: per-sequence N_b (null: N)
   const int32_t *win_bq; // ragged: per-sequence windows [batch, nql] (null: win_q)
 };
@@ -111,6 +112,37 @@ struct PItem {
   BlockTiles bt;
 };
 
+// 32 output columns of one row (this thread's), normalised and packed to bf16: two 256-bit
+// stores (a full 32-byte sector per lane) when the output rows are 32-byte aligned, else
+// four 128-bit ones.  Row-per-thread stores cost the softmax warps 8-13 % of the kernel.
+__device__ __forceinline__ void store_o_chunk32(__nv_bfloat16 *dst, const float (&r)[32], float inv, int v8) {
+  if (v8) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t w[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) w[e] = pack_bf16x2(r[16 * h + 2 * e] * inv, r[16 * h + 2 * e + 1] * inv);
+      asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 16 * h), "r"(w[0]),
+                   "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                   : "memory");
+    }
+  } else {
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+#pragma unroll
+    for (int v4 = 0; v4 < 4; ++v4) {
+      uint4 w;
+      w.x = pack_bf16x2(r[8 * v4 + 0] * inv, r[8 * v4 + 1] * inv);
+      w.y = pack_bf16x2(r[8 * v4 + 2] * inv, r[8 * v4 + 3] * inv);
+      w.z = pack_bf16x2(r[8 * v4 + 4] * inv, r[8 * v4 + 5] * inv);
+      w.w = pack_bf16x2(r[8 * v4 + 6] * inv, r[8 * v4 + 7] * inv);
+      d4[v4] = w;
+    }
+  }
+}
+
+#ifndef MOA_PP_OSTORE
+#define MOA_PP_OSTORE 1  // diagnostics: 0 skips the O / lse stores (epilogue cost study)
+#endif
 template <int BS, bool RAG>
 __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
   PItem it;
@@ -458,7 +490,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
     ++ic;
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    const bool store = i <= ti1 && (!RAG || i < p.seq_n[it.b]);  // ragged: rows past N_b are not outputs
+    const bool store = MOA_PP_OSTORE && i <= ti1 && (!RAG || i < p.seq_n[it.b]);  // ragged: rows past N_b are not outputs
     __nv_bfloat16 *orow =
         static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride + (int64_t)it.h * D;
 #pragma unroll
@@ -467,16 +499,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       tmem_ld32_f(ocol + c * 32, r);
       tmem_wait_ld();
       if (store) {
-        uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
-#pragma unroll
-        for (int v4 = 0; v4 < 4; ++v4) {
-          uint4 w;
-          w.x = pack_bf16x2(r[8 * v4 + 0] * inv, r[8 * v4 + 1] * inv);
-          w.y = pack_bf16x2(r[8 * v4 + 2] * inv, r[8 * v4 + 3] * inv);
-          w.z = pack_bf16x2(r[8 * v4 + 4] * inv, r[8 * v4 + 5] * inv);
-          w.w = pack_bf16x2(r[8 * v4 + 6] * inv, r[8 * v4 + 7] * inv);
-          dst[v4] = w;
-        }
+        store_o_chunk32(orow + c * 32, r, inv, p.o_v8);
       }
     }
     if (p.lse && store)
@@ -634,7 +657,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
       pair_sync();  // both read before the slot is reused by the next item's row max
       tc_fence_after();
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
-      const bool store = i <= ti1 && (!RAG || i < p.seq_n[it.b]);  // ragged: rows past N_b are not outputs
+      const bool store = MOA_PP_OSTORE && i <= ti1 && (!RAG || i < p.seq_n[it.b]);  // ragged: rows past N_b are not outputs
       __nv_bfloat16 *orow = static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride +
                             (int64_t)it.h * D + hf * kOCols;
 #pragma unroll
@@ -643,16 +666,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
         tmem_ld32_f(ocol + c * 32, r);
         tmem_wait_ld();
         if (store) {
-          uint4 *dst = reinterpret_cast<uint4 *>(orow + c * 32);
-#pragma unroll
-          for (int v4 = 0; v4 < 4; ++v4) {
-            uint4 w;
-            w.x = pack_bf16x2(r[8 * v4 + 0] * inv, r[8 * v4 + 1] * inv);
-            w.y = pack_bf16x2(r[8 * v4 + 2] * inv, r[8 * v4 + 3] * inv);
-            w.z = pack_bf16x2(r[8 * v4 + 4] * inv, r[8 * v4 + 5] * inv);
-            w.w = pack_bf16x2(r[8 * v4 + 6] * inv, r[8 * v4 + 7] * inv);
-            dst[v4] = w;
-          }
+          store_o_chunk32(orow + c * 32, r, inv, p.o_v8);
         }
       }
       if (p.lse && store && hf == 0)
@@ -818,6 +832,7 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   p.scale_log2 = a.scale * kLog2e;
   p.win_q = a.d_win_q;
   p.seq_n = a.d_seq_n;
+  p.o_v8 = (((uintptr_t)a.o | (uintptr_t)(a.o_row_stride * 2)) & 31) == 0;
   p.win_bq = a.d_win_bq;
   p.items = a.d_seq_n ? a.d_items_rag : a.d_items2;
   // the token mask (bshift < 0) and the block mask are separate instantiations, so the
