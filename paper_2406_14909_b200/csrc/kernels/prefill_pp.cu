@@ -494,12 +494,14 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
     __nv_bfloat16 *orow =
         static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride + (int64_t)it.h * D;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      float r[32];
+    for (int c = 0; c < D / 32; c += 2) {  // two TMEM loads in flight per wait
+      float r[32], r2[32];
       tmem_ld32_f(ocol + c * 32, r);
+      tmem_ld32_f(ocol + (c + 1) * 32, r2);
       tmem_wait_ld();
       if (store) {
         store_o_chunk32(orow + c * 32, r, inv, p.o_v8);
+        store_o_chunk32(orow + (c + 1) * 32, r2, inv, p.o_v8);
       }
     }
     if (p.lse && store)
@@ -661,12 +663,15 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
       __nv_bfloat16 *orow = static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride +
                             (int64_t)it.h * D + hf * kOCols;
 #pragma unroll
-      for (int c = 0; c < kOCols / 32; ++c) {
-        float r[32];
+      for (int c = 0; c < kOCols / 32; c += 2) {  // two TMEM loads in flight per wait
+        float r[32], r2[32];
+        const bool two = c + 1 < kOCols / 32;  // (D = 64: one chunk per half)
         tmem_ld32_f(ocol + c * 32, r);
+        if (two) tmem_ld32_f(ocol + (c + 1) * 32, r2);
         tmem_wait_ld();
         if (store) {
           store_o_chunk32(orow + c * 32, r, inv, p.o_v8);
+          if (two) store_o_chunk32(orow + (c + 1) * 32, r2, inv, p.o_v8);
         }
       }
       if (p.lse && store && hf == 0)
