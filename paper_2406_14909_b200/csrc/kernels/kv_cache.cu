@@ -15,9 +15,12 @@
 namespace moa {
 namespace {
 
-// cache_fill: grid (ceil(max_rows * vpr / 256), ngl, batch), 256 threads.
+// cache_fill: grid (ceil(max_rows / (kFillRows * 256 / vpr)), ngl, batch), 256 threads.
 // Row r of the region receives prompt position pos_of_row(r, N-1) (sinks
-// [0, min(s,N)), ring = the last W_g non-sink positions).
+// [0, min(s,N)), ring = the last W_g non-sink positions).  A thread copies the same
+// 16-byte column of kFillRows rows (256 / vpr rows apart): all its loads are issued before
+// its stores, so each thread keeps 2 * kFillRows * 16 bytes in flight.
+constexpr int kFillRows = 4;
 __global__ void __launch_bounds__(256) cache_fill_kernel(
     const uint4 *__restrict__ k, const uint4 *__restrict__ v, int64_t row_stride_v,  // in uint4
     uint4 *__restrict__ kc, uint4 *__restrict__ vc, int64_t rows_per_seq,
@@ -26,17 +29,31 @@ __global__ void __launch_bounds__(256) cache_fill_kernel(
   const int g = blockIdx.y, b = blockIdx.z;
   const int Wg = win_g[g];
   const int64_t R = (int64_t)n_sink + Wg;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t r = idx / vpr;
-  const int e = (int)(idx - r * vpr);
-  if (r >= R) return;
+  const int rpb = 256 / vpr;  // rows per pass of the block
+  const int e = threadIdx.x % vpr;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb * kFillRows + threadIdx.x / vpr;
+  if (r0 >= R) return;
   const int64_t Nb = seq_n ? seq_n[b] : N;  // ragged: this sequence's prompt length (<= N)
-  const int64_t p = moa::pos_of_row(r, Nb - 1, n_sink, Wg);
-  if (p < 0) return;  // row not reached by the prompt (short prompt)
-  const int64_t src = ((int64_t)b * N + p) * row_stride_v + (int64_t)g * vpr + e;
-  const int64_t dst = ((int64_t)b * rows_per_seq + g_off[g] + r) * vpr + e;
-  kc[dst] = __ldg(k + src);
-  vc[dst] = __ldg(v + src);
+  uint4 kk[kFillRows], vv[kFillRows];
+  int64_t dst[kFillRows];
+#pragma unroll
+  for (int u = 0; u < kFillRows; ++u) {
+    const int64_t r = r0 + (int64_t)u * rpb;
+    const int64_t p = r < R ? moa::pos_of_row(r, Nb - 1, n_sink, Wg) : -1;
+    dst[u] = -1;
+    if (p >= 0) {  // (p < 0: row not reached by the prompt, or past the region)
+      const int64_t src = ((int64_t)b * N + p) * row_stride_v + (int64_t)g * vpr + e;
+      kk[u] = __ldg(k + src);
+      vv[u] = __ldg(v + src);
+      dst[u] = ((int64_t)b * rows_per_seq + g_off[g] + r) * vpr + e;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kFillRows; ++u)
+    if (dst[u] >= 0) {
+      kc[dst[u]] = kk[u];
+      vc[dst[u]] = vv[u];
+    }
 }
 
 // kv_append: grid (ngl, batch), vpr threads per K and V (blockDim = 2 * vpr).
@@ -66,8 +83,9 @@ __global__ void kv_append_kernel(const uint4 *__restrict__ k, const uint4 *__res
 
 int launch_cache_fill(const CacheArgs &a, void *stream) {
   const int vpr = a.d * a.esize / 16;
-  const int64_t vecs = a.max_region_rows * vpr;
-  dim3 grid((unsigned)((vecs + 255) / 256), (unsigned)a.ngl, (unsigned)a.batch);
+  const int64_t rows_per_block = (int64_t)(256 / vpr) * kFillRows;
+  dim3 grid((unsigned)((a.max_region_rows + rows_per_block - 1) / rows_per_block), (unsigned)a.ngl,
+            (unsigned)a.batch);
   cache_fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
       static_cast<const uint4 *>(a.k), static_cast<const uint4 *>(a.v), a.row_stride * a.esize / 16,
       static_cast<uint4 *>(a.k_cache), static_cast<uint4 *>(a.v_cache), a.rows_per_seq, a.d_g_off,
