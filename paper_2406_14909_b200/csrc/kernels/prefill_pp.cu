@@ -112,9 +112,12 @@ struct PItem {
   BlockTiles bt;
 };
 
+#ifndef MOA_PP_OST_HINT
+#define MOA_PP_OST_HINT ".L1::no_allocate"  // O rows are never re-read here: C2 +2.5 %, C4 +1.8 % vs none
+#endif
 // 32 output columns of one row (this thread's), normalised and packed to bf16: two 256-bit
 // stores (a full 32-byte sector per lane) when the output rows are 32-byte aligned, else
-// four 128-bit ones.  Row-per-thread stores cost the softmax warps 8-13 % of the kernel.
+// four 128-bit ones; no L1 allocation (nothing here re-reads O).  Row-per-thread stores cost the softmax warps 8-13 % of the kernel.
 __device__ __forceinline__ void store_o_chunk32(__nv_bfloat16 *dst, const float (&r)[32], float inv, int v8) {
   if (v8) {
 #pragma unroll
@@ -122,20 +125,20 @@ __device__ __forceinline__ void store_o_chunk32(__nv_bfloat16 *dst, const float 
       uint32_t w[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) w[e] = pack_bf16x2(r[16 * h + 2 * e] * inv, r[16 * h + 2 * e + 1] * inv);
-      asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 16 * h), "r"(w[0]),
+      asm volatile("st.global" MOA_PP_OST_HINT ".v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 16 * h), "r"(w[0]),
                    "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                    : "memory");
     }
   } else {
-    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
 #pragma unroll
     for (int v4 = 0; v4 < 4; ++v4) {
-      uint4 w;
-      w.x = pack_bf16x2(r[8 * v4 + 0] * inv, r[8 * v4 + 1] * inv);
-      w.y = pack_bf16x2(r[8 * v4 + 2] * inv, r[8 * v4 + 3] * inv);
-      w.z = pack_bf16x2(r[8 * v4 + 4] * inv, r[8 * v4 + 5] * inv);
-      w.w = pack_bf16x2(r[8 * v4 + 6] * inv, r[8 * v4 + 7] * inv);
-      d4[v4] = w;
+      const uint32_t x = pack_bf16x2(r[8 * v4 + 0] * inv, r[8 * v4 + 1] * inv);
+      const uint32_t y = pack_bf16x2(r[8 * v4 + 2] * inv, r[8 * v4 + 3] * inv);
+      const uint32_t z = pack_bf16x2(r[8 * v4 + 4] * inv, r[8 * v4 + 5] * inv);
+      const uint32_t w = pack_bf16x2(r[8 * v4 + 6] * inv, r[8 * v4 + 7] * inv);
+      asm volatile("st.global" MOA_PP_OST_HINT ".v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 8 * v4), "r"(x), "r"(y),
+                   "r"(z), "r"(w)
+                   : "memory");
     }
   }
 }

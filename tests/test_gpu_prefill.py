@@ -322,3 +322,27 @@ def test_block_prefill_then_token_decode(moa):
     Kh, Vh = torch.cat([k, kd[:, None]], 1), torch.cat([v, vd[:, None]], 1)
     Od, _ = oracle.decode(f64(qd), f64(Kh), f64(Vh), N, W, s, scale)
     assert np.abs(f64(od) - Od).max() < 2e-2
+
+
+def test_output_rows_not_32_byte_aligned(moa):
+    """The epilogue uses 256-bit stores only for 32-byte aligned output rows; an output view
+    offset by 16 bytes takes the 128-bit path and must give bitwise the same result."""
+    dev = torch.device("cuda")
+    B, N, Hq, Hkv, d, s = 2, 300, 4, 2, 128, 4
+    W = [3, 200, 0, 77]
+    q = normal((B, N, Hq, d), 321, torch.bfloat16).to(dev)
+    k = normal((B, N, Hkv, d), 322, torch.bfloat16).to(dev)
+    v = normal((B, N, Hkv, d), 323, torch.bfloat16).to(dev)
+    ctx = moa.MoAContext(1, Hq, Hkv, d, B, dtype=torch.bfloat16)
+    ctx.set_spans(0, W, s, N)
+    o1 = torch.empty_like(q)
+    flat = torch.zeros(q.numel() + 8, dtype=torch.bfloat16, device=dev)
+    o2 = flat[8:].view(B, N, Hq, d)  # 16 bytes past a 256-byte aligned allocation
+    assert o2.data_ptr() % 32 == 16
+    tau = 1 / math.sqrt(d)
+    ctx.prefill_attn(0, q, k, v, o1, tau)
+    ctx.prefill_attn(0, q, k, v, o2, tau)
+    torch.cuda.synchronize()
+    assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+    O, _ = oracle.prefill(f64(q), f64(k), f64(v), W, s, tau)
+    assert np.abs(f64(o2) - O).max() < 2e-2
