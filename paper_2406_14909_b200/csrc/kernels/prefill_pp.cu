@@ -49,6 +49,10 @@ constexpr int kThreads = 384;  // warp 11 idles (warpgroup-aligned register real
 constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10, kWarpMMA1 = 11, kSoftmaxWarp0 = 0;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef MOA_PP_REG_SOFTMAX
+#define MOA_PP_REG_SOFTMAX 208  // setmaxnreg split: 8 softmax warps x 208 + 4 other warps x 88 <= 64K
+#define MOA_PP_REG_OTHER 88
+#endif
 #ifndef MOA_PP_POLY_EVERY
 #define MOA_PP_POLY_EVERY 4
 #endif
@@ -734,13 +738,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = bars.tmem_base;
 
   if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(MOA_PP_REG_SOFTMAX) : "memory");
     if (BS >= 0)
       softmax_split_role<D, BS, RAG>(p, bars, tmem, total, warp, lane, red);
     else
       softmax_role<D, BS, RAG>(p, bars, tmem, total, (warp - kSoftmaxWarp0) >> 2, warp, lane);
   } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(MOA_PP_REG_OTHER) : "memory");
   if (warp == kWarpKV) {
     if (lane == 0) {
       int T = 0;
