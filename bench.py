@@ -103,8 +103,17 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------------------------
 def windows_all_layers(moa):
+    """Product path: Eq. 2 through the library's moa_resolve_spans."""
     t = rule_table("C2")
     return [moa.resolve_spans(t["alpha"][l], t["beta"][l], CFG.N, CFG.n_sink) for l in range(CFG.layers)]
+
+
+def oracle_windows_all_layers():
+    """Oracle legs: Eq. 2 through oracle.span_of / window_of (no libmoa on that path)."""
+    import oracle
+    t = rule_table("C2")
+    return [[oracle.window_of(oracle.span_of(a, b, CFG.N), CFG.n_sink) for a, b in zip(t["alpha"][l], t["beta"][l])]
+            for l in range(CFG.layers)]
 
 
 def algorithmic_work(windows, B, N, T, s, d, G):
@@ -131,9 +140,8 @@ def cpu_oracle_decode_rate(seconds: float = 12.0):
     consecutive positions p = N, N+1, ... until `seconds` elapse; returns tokens/s extrapolated to
     the whole C2 decode workload (32 layers x 8 sequences) and a description."""
     import oracle
-    import paper_2406_14909_b200 as moa
 
-    W = windows_all_layers(moa)[0]
+    W = oracle_windows_all_layers()[0]
     d, s, N = CFG.head_dim, CFG.n_sink, CFG.N
     g = torch.Generator().manual_seed(7)
     hist = N + 64

@@ -322,15 +322,16 @@ moa_status moa_rule_losses(const float *e_blocks, int heads, int64_t N, int bloc
  * Rule selection (Eq. 5): one rule per head minimising
  * sum_h loss[h][r_h] subject to the mean density (1/H) sum_h density[r_h] <= density_budget
  * and at most max_rules_per_layer (1 or 2, "at most two per model layer")
- * distinct rules per layer.  Host only.  The paper solves this MIP with Gurobi; here the
- * density budget is relaxed with a Lagrange price (bisection) and each layer is solved
- * exactly for a price (all rule subsets of size <= 2, every head its best rule in the
- * subset).  The returned plan meets the budget and minimises loss + price * density, so no
- * plan of equal or lower density has a lower loss (it may leave part of the budget unused).
+ * distinct rules per layer.  Host only.  The paper solves this MIP (eq:mip)
+ * with Gurobi; here it is solved EXACTLY: per layer, the Pareto frontier (density, loss) of
+ * every rule subset of size <= 2 (for a pair, the best split of the heads by the exchange
+ * argument), then the Pareto merge of the layers (a multiple-choice knapsack) with
+ * admissible density / loss bounds.  Feasible means sum_h density <= budget * H + 1e-9.
  *   loss      host fp32 [layers * heads_per_layer][n_rules] (moa_rule_losses, one length).
  *   density   host fp32 [n_rules]: density of each rule at that length.
  *   rule_out  host int32 [layers * heads_per_layer]; loss_out / density_out nullable.
- * Errors: MOA_ERR_INVALID_ARG if even the sparsest rule exceeds the budget.
+ * Errors: MOA_ERR_INVALID_ARG if no plan meets the budget (or a loss is not finite);
+ *         MOA_ERR_UNSUPPORTED if the exact solver's frontier outgrows 2^24 partial plans.
  */
 moa_status moa_plan_rules(const float *loss, const float *density, int layers, int heads_per_layer, int n_rules,
                           float density_budget, int max_rules_per_layer, int32_t *rule_out, float *loss_out,

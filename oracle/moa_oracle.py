@@ -79,10 +79,14 @@ __all__ = [
     "density",
     "visible_pairs",
     "visible_pairs_block",
+    "attention_matrix",
     "attention_influence",
+    "attention_influence_rows",
     "influence_blocks",
+    "influence_blocks_sampled",
     "rule_window_blocked",
     "rule_losses",
+    "plan_rules",
 ]
 
 
@@ -416,15 +420,50 @@ def attention_influence(A: np.ndarray, G: np.ndarray) -> np.ndarray:
     return E
 
 
+def attention_matrix(Qh, Kh, tau: float, rows=None) -> np.ndarray:
+    """Dense causal attention matrix of one head, ``A = softmax(tau Q K^T + causal)``
+    (Eq. 1 with the unmasked causal model that profiling uses).
+    Qh, Kh: [N, d].  ``rows`` (optional) selects the query rows to return; row i holds
+    A_ij for j <= i and 0 above the diagonal.  Returns [len(rows), N] fp64."""
+    Qh = np.asarray(Qh, dtype=np.float64)
+    Kh = np.asarray(Kh, dtype=np.float64)
+    N = Kh.shape[0]
+    rows = range(N) if rows is None else rows
+    rows = list(rows)
+    A = np.zeros((len(rows), N))
+    for r, i in enumerate(rows):
+        z = tau * (Kh[: i + 1] @ Qh[i])
+        w = np.exp(z - z.max())
+        A[r, : i + 1] = w / w.sum()
+    return A
+
+
+def attention_influence_rows(A: np.ndarray, G: np.ndarray) -> np.ndarray:
+    """Eq. 3 for whole rows at once:
+
+        E_ij = G_ij * (-A_ij) + (R_i - G_ij A_ij) * A_ij / (1 - A_ij),   R_i = sum_n G_in A_in
+
+    i.e. the same formula as ``attention_influence`` with the sum over n != j written as the
+    row total minus the j term.  Same conventions: E = 0 where A = 0 or A = 1.  Pinned
+    against the term-by-term ``attention_influence`` (tests/test_oracle_pins.py)."""
+    A = np.asarray(A, dtype=np.float64)
+    G = np.asarray(G, dtype=np.float64)
+    R = (G * A).sum(axis=1, keepdims=True)
+    live = (A > 0.0) & (A < 1.0)
+    Asafe = np.where(live, A, 0.0)
+    E = -G * Asafe + (R - G * Asafe) * Asafe / np.where(live, 1.0 - Asafe, 1.0)
+    return np.where(live, E, 0.0)
+
+
 def influence_blocks(Q, K, V, dO, tau: float, block: int):
     """Block-averaged attention influence of every head for one calibration item.
 
     The profiling pass of the paper: dense causal attention (PAPER.md:691
     profiles the unmasked model), ``A = softmax(tau Q K^T + causal)``
-    (Eq. 1), ``G = dL/dA = dO V^T`` for ``O = A V`` (chain rule),
-    E by Eq. 3, then "the average attention influence within each block"
-     over ``block x block`` token pairs (masked pairs count as 0,
-    the last block may be partial: mean over its real pairs).
+    (Eq. 1, ``attention_matrix``), ``G = dL/dA = dO V^T`` for ``O = A V`` (chain
+    rule), E by Eq. 3, then "the average attention influence within
+    each block" over ``block x block`` token pairs (masked pairs count
+    as 0, the last block may be partial: mean over its real pairs).
     Q, dO: [B, N, Hq, d]; K, V: [B, N, Hkv, d].  Returns [B, Hq, nb, nb] fp64.
     """
     B, N, Hq, d = Q.shape
@@ -435,18 +474,39 @@ def influence_blocks(Q, K, V, dO, tau: float, block: int):
     for b in range(B):
         for h in range(Hq):
             g = h // G_
-            S = tau * (Q[b, :, h].astype(np.float64) @ K[b, :, g].astype(np.float64).T)
-            A = np.zeros((N, N))
-            for i in range(N):
-                z = S[i, : i + 1]
-                w = np.exp(z - z.max())
-                A[i, : i + 1] = w / w.sum()
+            A = attention_matrix(Q[b, :, h], K[b, :, g], tau)
             Gm = dO[b, :, h].astype(np.float64) @ V[b, :, g].astype(np.float64).T
             E = attention_influence(A, Gm)
             for ib in range(nb):
                 for jb in range(nb):
                     blk = E[ib * block:(ib + 1) * block, jb * block:(jb + 1) * block]
                     out[b, h, ib, jb] = blk.sum() / blk.size
+    return out
+
+
+def influence_blocks_sampled(Q, K, V, dO, tau: float, block: int, b: int, h: int, q_blocks,
+                             magnitude: bool = False):
+    """Rows ``q_blocks`` of ``influence_blocks(...)[b, h]`` (the block means of the listed
+    query blocks against every key block), for lengths where the full N x N computation is
+    out of reach: the same steps (``attention_matrix`` of the block's rows, G = dO V^T, Eq. 3
+    by ``attention_influence_rows``, block means over ``block x block`` pairs).
+    ``magnitude``: block means of |E| instead (the scale a per-block test tolerance uses).
+    Returns [len(q_blocks), nb] fp64."""
+    B, N, Hq, d = Q.shape
+    Hkv = K.shape[2]
+    g = h // (Hq // Hkv)
+    nb = (N + block - 1) // block
+    out = np.zeros((len(q_blocks), nb), dtype=np.float64)
+    for r, ib in enumerate(q_blocks):
+        rows = list(range(ib * block, min(N, (ib + 1) * block)))
+        A = attention_matrix(Q[b, :, h], K[b, :, g], tau, rows)
+        Gm = dO[b, rows, h].astype(np.float64) @ V[b, :, g].astype(np.float64).T
+        E = attention_influence_rows(A, Gm)
+        if magnitude:
+            E = np.abs(E)
+        for jb in range(nb):
+            blk = E[:, jb * block:(jb + 1) * block]
+            out[r, jb] = blk.sum() / blk.size
     return out
 
 
@@ -483,3 +543,41 @@ def rule_losses(E_blocks: np.ndarray, alphas, betas, N: int, n_sink: int, block:
                 cols = min(block, N - jb * block)
                 out[:, r] += E_blocks[:, ib, jb] * rows * cols
     return out
+
+
+# ---------------------------------------------------------------------------
+# Rule selection at one length (Eq. 5 / eq:mip)
+# ---------------------------------------------------------------------------
+
+def plan_rules(loss, density, layers: int, heads_per_layer: int, density_budget: float,
+               max_rules_per_layer: int = 2):
+    """Exhaustive solution of eq:mip: every assignment of one rule per head
+    (eq:mip:plan) with at most ``max_rules_per_layer`` distinct rules in a layer
+    ("at most two per model layer") and mean density
+    ``(1/H) sum_h d_{r_h} <= d_constr`` (eq:mip:latency; feasibility slack: the sum
+    may exceed ``budget * H`` by at most 1e-9), minimising ``sum_h Delta L_{h,r_h}``
+    (eq:mip:obj up to the constant 1/H).  Brute force, for small instances only.
+    loss: [H, R], density: [R].  Returns (plan tuple, loss, mean density) of an optimum
+    (lowest loss, then lowest density, then the lexicographically first plan), or None
+    if no assignment is feasible."""
+    import itertools
+    loss = np.asarray(loss, dtype=np.float64)
+    dens = np.asarray(density, dtype=np.float64)
+    H, R = loss.shape
+    assert H == layers * heads_per_layer and dens.shape == (R,)
+    best = None
+    for plan in itertools.product(range(R), repeat=H):
+        if any(len(set(plan[l * heads_per_layer:(l + 1) * heads_per_layer])) > max_rules_per_layer
+               for l in range(layers)):
+            continue
+        dsum = sum(dens[r] for r in plan)
+        if dsum > density_budget * H + 1e-9:
+            continue
+        lsum = sum(loss[h, r] for h, r in enumerate(plan))
+        key = (lsum, dsum)
+        if best is None or key < best[0]:
+            best = (key, plan)
+    if best is None:
+        return None
+    (lsum, dsum), plan = best
+    return plan, lsum, dsum / H

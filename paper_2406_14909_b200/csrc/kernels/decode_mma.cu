@@ -711,15 +711,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
 #endif
 }
 
-int num_sms_dev() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
+int num_sms_dev() { return device_sm_count(); }
 
 int ctas_for(int64_t R, int cps) {
   int64_t n = (int64_t)num_sms_dev() * cps;

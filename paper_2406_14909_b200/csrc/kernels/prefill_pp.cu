@@ -49,10 +49,17 @@ constexpr int kThreads = 384;  // warp 11 idles (warpgroup-aligned register real
 constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10, kWarpMMA1 = 11, kSoftmaxWarp0 = 0;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// setmaxnreg split: 8 softmax warps x MOA_PP_REG_SOFTMAX + 4 other warps x MOA_PP_REG_OTHER <= 64K
 #ifndef MOA_PP_REG_SOFTMAX
-#define MOA_PP_REG_SOFTMAX 208  // setmaxnreg split: 8 softmax warps x 208 + 4 other warps x 88 <= 64K
+#define MOA_PP_REG_SOFTMAX 208
+#endif
+#ifndef MOA_PP_REG_OTHER
 #define MOA_PP_REG_OTHER 88
 #endif
+static_assert((8 * MOA_PP_REG_SOFTMAX + 4 * MOA_PP_REG_OTHER) * 32 <= 65536, "setmaxnreg split exceeds the register file");
+static_assert(MOA_PP_REG_SOFTMAX % 8 == 0 && MOA_PP_REG_OTHER % 8 == 0, "setmaxnreg counts must be multiples of 8");
+static_assert(MOA_PP_REG_SOFTMAX >= 24 && MOA_PP_REG_SOFTMAX <= 256 && MOA_PP_REG_OTHER >= 24 &&
+                  MOA_PP_REG_OTHER <= 256, "setmaxnreg counts must be in [24, 256]");
 #ifndef MOA_PP_POLY_EVERY
 #define MOA_PP_POLY_EVERY 4
 #endif
@@ -811,15 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-int num_sms_pp() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
+int num_sms_pp() { return device_sm_count(); }
 
 template <int D>
 int launch_pp(const PrefillArgs &a, void *stream) {

@@ -26,6 +26,27 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 }  // namespace
 
+// SM count of the CURRENT device, cached per device ordinal (a process may drive several
+// devices; the launch calls run under the context's DeviceGuard).
+int device_sm_count() {
+  constexpr int kMaxDev = 64;
+  static int cache[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= kMaxDev) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }
+  int n = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    __atomic_store_n(&cache[dev], n, __ATOMIC_RELAXED);
+  }
+  return n;
+}
+
 // [B, N, H, D] bf16 with token row stride `row_stride` (elements): 4-D map (D, H, N, B),
 // box = 64 columns x box_rows tokens of one head, 128-byte swizzle.
 bool make_tile_map(void *m, const void *ptr, int D, int H, int64_t N, int B, int64_t row_stride, int box_rows) {

@@ -373,6 +373,12 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
     np.v_cache = p.v_cache;
     np.bound_batch = p.bound_batch;
     np.next_pos = p.k_cache ? 0 : -1;
+    // the TMA tensor maps describe the same [rows, d] cache: keep them
+    std::memcpy(np.kmap, p.kmap, sizeof(np.kmap));
+    std::memcpy(np.vmap, p.vmap, sizeof(np.vmap));
+    std::memcpy(np.kmap16, p.kmap16, sizeof(np.kmap16));
+    std::memcpy(np.vmap16, p.vmap16, sizeof(np.vmap16));
+    np.maps_ok = p.maps_ok;
   }
   st = upload_tables(ctx, np);
   if (st) return st;
@@ -973,56 +979,75 @@ moa_status moa_rule_losses(const float *e_blocks, int heads, int64_t N, int bloc
   return ok();
 }
 
-// ---- rule selection (Eq. 5): Lagrangian relaxation of the density budget.
-// For a price lam >= 0 every layer independently picks the subset S of at most k rules and the
-// per-head choice in S minimising sum_h (loss[h][r] + lam * density[r]); the mean density of
-// that plan falls as lam grows.  The smallest lam (bisection) whose plan meets the budget is
-// returned: it minimises loss + lam * density over all plans, so no plan of equal or lower
-// density has a lower loss.
+// ---- rule selection (Eq. 5 / eq:mip): exact.
+// A plan picks one rule per head; a layer uses at most k <= 2 distinct rules.
+// Layer options: for a rule pair (a, b) with density[a] < density[b], the best plan that puts
+// m of the layer's heads on b moves the m heads with the largest loss[h][a] - loss[h][b]
+// (exchange argument: any other m-subset has the same density and no lower loss); single
+// rules and equal-density pairs give one point each.  Each layer's options are reduced to
+// their Pareto frontier (density ascending, loss strictly descending); the frontier of the
+// whole model is the Pareto merge of the layer frontiers (multiple-choice knapsack, exact:
+// a sum of points is Pareto-optimal only if every summand is).  Partial sums are pruned when
+// they cannot fit the budget with the sparsest options of the remaining layers, or cannot
+// beat a feasible incumbent with the remaining layers' minimal losses (admissible bounds).
+// Feasibility: sum_h density <= budget * H + 1e-9 (the oracle uses the same slack).
 namespace {
 
-struct PlanEval {
-  double loss = 0.0, dens = 0.0;
+struct LPoint {
+  double dens, loss;
+  int a, b, m;  // rule a for the heads not moved, rule b for the m moved heads (b = -1: none)
 };
 
-PlanEval plan_at(const float *loss, const float *density, int layers, int hpl, int R, int k, double lam,
-                 int32_t *choice) {
-  PlanEval ev;
-  std::vector<int32_t> best_pick(hpl), pick(hpl);
-  for (int l = 0; l < layers; ++l) {
-    const float *L = loss + (size_t)l * hpl * R;
-    double best = INFINITY, best_loss = 0.0, best_d = 0.0;
-    auto try_subset = [&](int a, int b) {
-      double c = 0.0, cl = 0.0, cd = 0.0;
-      for (int h = 0; h < hpl; ++h) {
-        const double va = L[(size_t)h * R + a] + lam * density[a];
-        int r = a;
-        if (b >= 0) {
-          const double vb = L[(size_t)h * R + b] + lam * density[b];
-          if (vb < va || (vb == va && density[b] < density[a])) r = b;
-        }
-        pick[h] = r;
-        c += L[(size_t)h * R + r] + lam * density[r];
-        cl += L[(size_t)h * R + r];
-        cd += density[r];
-      }
-      if (c < best || (c == best && cd < best_d)) {
-        best = c, best_loss = cl, best_d = cd;
-        best_pick = pick;
-      }
-    };
-    for (int a = 0; a < R; ++a) {
-      try_subset(a, -1);
-      if (k >= 2)
-        for (int b = a + 1; b < R; ++b) try_subset(a, b);
-    }
-    ev.loss += best_loss;
-    ev.dens += best_d;
-    if (choice) std::copy(best_pick.begin(), best_pick.end(), choice + (size_t)l * hpl);
+std::vector<LPoint> layer_frontier(const float *L, const float *density, int hpl, int R, int k) {
+  std::vector<LPoint> pts;
+  std::vector<double> base(R, 0.0);
+  for (int r = 0; r < R; ++r) {
+    double c = 0.0;
+    for (int h = 0; h < hpl; ++h) c += L[(size_t)h * R + r];
+    base[r] = c;
+    pts.push_back({(double)density[r] * hpl, c, r, -1, 0});
   }
-  ev.dens /= (double)layers * hpl;
-  return ev;
+  if (k >= 2) {
+    std::vector<double> gain(hpl);
+    for (int a = 0; a < R; ++a)
+      for (int b = 0; b < R; ++b) {
+        if (a == b) continue;
+        if (density[a] > density[b] || (density[a] == density[b] && a > b)) continue;
+        for (int h = 0; h < hpl; ++h) gain[h] = (double)L[(size_t)h * R + a] - (double)L[(size_t)h * R + b];
+        std::vector<int> ord(hpl);
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return gain[x] > gain[y]; });
+        double loss = base[a];
+        for (int m = 1; m < hpl; ++m) {
+          loss -= gain[ord[m - 1]];
+          pts.push_back({(double)density[a] * (hpl - m) + (double)density[b] * m, loss, a, b, m});
+        }
+      }
+  }
+  std::stable_sort(pts.begin(), pts.end(), [](const LPoint &x, const LPoint &y) {
+    return x.dens < y.dens || (x.dens == y.dens && x.loss < y.loss);
+  });
+  std::vector<LPoint> f;
+  for (const LPoint &q : pts)
+    if (f.empty() || q.loss < f.back().loss) f.push_back(q);
+  return f;
 }
+
+void layer_assign(const LPoint &q, const float *L, int hpl, int R, int32_t *choice) {
+  for (int h = 0; h < hpl; ++h) choice[h] = q.a;
+  if (q.b < 0 || q.m == 0) return;
+  std::vector<double> gain(hpl);
+  for (int h = 0; h < hpl; ++h) gain[h] = (double)L[(size_t)h * R + q.a] - (double)L[(size_t)h * R + q.b];
+  std::vector<int> ord(hpl);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return gain[x] > gain[y]; });
+  for (int m = 0; m < q.m; ++m) choice[ord[m]] = q.b;
+}
+
+struct FPoint {
+  double dens, loss;
+  int prev, opt;  // index into the previous frontier, option of this layer
+};
 
 }  // namespace
 
@@ -1036,31 +1061,105 @@ moa_status moa_plan_rules(const float *loss, const float *density, int layers, i
                 max_rules_per_layer);
   for (int r = 0; r < n_rules; ++r)
     if (!(density[r] >= 0.f && density[r] <= 1.f)) return fail(MOA_ERR_INVALID_ARG, "density[%d] not in [0,1]", r);
-  const int H = layers * heads_per_layer, k = max_rules_per_layer;
-  const float dmin = *std::min_element(density, density + n_rules);
-  if (dmin > density_budget)
-    return fail(MOA_ERR_INVALID_ARG, "infeasible: the sparsest rule has density %.4f > budget %.4f", dmin,
-                density_budget);
-  PlanEval ev = plan_at(loss, density, layers, heads_per_layer, n_rules, k, 0.0, rule_out);
-  if (ev.dens > density_budget) {
-    double lo = 0.0, hi = 1.0;
-    while (plan_at(loss, density, layers, heads_per_layer, n_rules, k, hi, nullptr).dens > density_budget) {
-      lo = hi;
-      hi *= 2.0;
-      if (hi > 1e30) return fail(MOA_ERR_INVALID_ARG, "no price meets the density budget");
-    }
-    for (int it = 0; it < 100 && hi - lo > 1e-12 * hi; ++it) {
-      const double mid = 0.5 * (lo + hi);
-      if (plan_at(loss, density, layers, heads_per_layer, n_rules, k, mid, nullptr).dens > density_budget)
-        lo = mid;
-      else
-        hi = mid;
-    }
-    ev = plan_at(loss, density, layers, heads_per_layer, n_rules, k, hi, rule_out);
+  for (size_t i = 0; i < (size_t)layers * heads_per_layer * n_rules; ++i)
+    if (!std::isfinite(loss[i])) return fail(MOA_ERR_INVALID_ARG, "loss[%zu] is not finite", i);
+  const int hpl = heads_per_layer, R = n_rules, k = max_rules_per_layer;
+  const double H = (double)layers * hpl;
+  const double cap = (double)density_budget * H + 1e-9;
+  std::vector<std::vector<LPoint>> lf(layers);
+  for (int l = 0; l < layers; ++l) lf[l] = layer_frontier(loss + (size_t)l * hpl * R, density, hpl, R, k);
+  // suffix bounds: sparsest density and smallest loss of the layers after l
+  std::vector<double> min_d(layers + 1, 0.0), min_l(layers + 1, 0.0);
+  for (int l = layers - 1; l >= 0; --l) {
+    double md = INFINITY, ml = INFINITY;
+    for (const LPoint &q : lf[l]) md = std::min(md, q.dens), ml = std::min(ml, q.loss);
+    min_d[l] = min_d[l + 1] + md;
+    min_l[l] = min_l[l + 1] + ml;
   }
-  (void)H;
-  if (loss_out) *loss_out = (float)ev.loss;
-  if (density_out) *density_out = (float)ev.dens;
+  if (min_d[0] > cap)
+    return fail(MOA_ERR_INVALID_ARG, "infeasible: the sparsest plan has mean density %.6f > budget %.6f",
+                min_d[0] / H, (double)density_budget);
+  // feasible incumbent for the loss bound: the best Lagrangian plan (each layer minimises
+  // loss + lam * density over its frontier) that fits, over a bisection of the price lam
+  double incumbent = 0.0;
+  for (int l = 0; l < layers; ++l) incumbent += lf[l].front().loss;  // all-sparsest: feasible
+  {
+    auto plan_at = [&](double lam, double &dsum) {
+      double lsum = 0.0;
+      dsum = 0.0;
+      for (int l = 0; l < layers; ++l) {
+        const LPoint *b = &lf[l][0];
+        for (const LPoint &q : lf[l])
+          if (q.loss + lam * q.dens < b->loss + lam * b->dens) b = &q;
+        lsum += b->loss;
+        dsum += b->dens;
+      }
+      return lsum;
+    };
+    double lo = 0.0, hi = 1.0, dsum = 0.0;
+    double l0 = plan_at(0.0, dsum);
+    if (dsum <= cap) {
+      incumbent = std::min(incumbent, l0);
+    } else {
+      for (int it = 0; it < 200; ++it) {
+        plan_at(hi, dsum);
+        if (dsum <= cap) break;
+        lo = hi;
+        hi *= 2.0;
+      }
+      for (int it = 0; it < 100; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        const double lm = plan_at(mid, dsum);
+        if (dsum <= cap) {
+          incumbent = std::min(incumbent, lm);
+          hi = mid;
+        } else {
+          lo = mid;
+        }
+      }
+      const double lh = plan_at(hi, dsum);
+      if (dsum <= cap) incumbent = std::min(incumbent, lh);
+    }
+  }
+  std::vector<std::vector<FPoint>> fr(layers + 1);
+  fr[0].push_back({0.0, 0.0, -1, -1});
+  const size_t kMaxFrontier = (size_t)1 << 24;
+  std::vector<FPoint> cand;
+  for (int l = 0; l < layers; ++l) {
+    cand.clear();
+    const double dcap = cap - min_d[l + 1];
+    const double lcap = incumbent - min_l[l + 1] + 1e-9 * (1.0 + std::fabs(incumbent));
+    const auto &F = fr[l];
+    for (int i = 0; i < (int)F.size(); ++i)
+      for (int j = 0; j < (int)lf[l].size(); ++j) {
+        const double d = F[i].dens + lf[l][j].dens;
+        if (d > dcap) break;  // layer options are sorted by density
+        const double c = F[i].loss + lf[l][j].loss;
+        if (c > lcap) continue;
+        cand.push_back({d, c, i, j});
+      }
+    std::sort(cand.begin(), cand.end(), [](const FPoint &x, const FPoint &y) {
+      return x.dens < y.dens || (x.dens == y.dens && x.loss < y.loss);
+    });
+    auto &NF = fr[l + 1];
+    for (const FPoint &q : cand)
+      if (NF.empty() || q.loss < NF.back().loss) NF.push_back(q);
+    if (NF.size() > kMaxFrontier)
+      return fail(MOA_ERR_UNSUPPORTED, "exact rule selection: Pareto frontier of %zu partial plans at layer %d "
+                  "exceeds the solver's limit", NF.size(), l);
+    if (NF.empty()) return fail(MOA_ERR_INVALID_ARG, "infeasible density budget");
+  }
+  // the optimum: the last (lowest-loss) point of the final frontier
+  const auto &FN = fr[layers];
+  int idx = (int)FN.size() - 1;
+  const double best_loss = FN[idx].loss, best_dens = FN[idx].dens;
+  for (int l = layers; l >= 1; --l) {
+    const FPoint &q = fr[l][idx];
+    layer_assign(lf[l - 1][q.opt], loss + (size_t)(l - 1) * hpl * R, hpl, R, rule_out + (size_t)(l - 1) * hpl);
+    idx = q.prev;
+  }
+  if (loss_out) *loss_out = (float)best_loss;
+  if (density_out) *density_out = (float)(best_dens / H);
   return ok();
 }
 

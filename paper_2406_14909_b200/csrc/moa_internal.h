@@ -309,6 +309,8 @@ struct RuleWindows {
 int launch_rule_losses(const float *e_blocks, int heads, int64_t N, int block, const RuleWindows &win,
                        int sink_blocks, int n_rules, float *loss, void *stream);
 
+// SM count of the current device (cached per device ordinal).
+int device_sm_count();
 // TMA tensor map over a [rows, d] bf16 cache (box box_rows x 64 cols, 128B swizzle).
 bool encode_cache_map(void *map_out, const void *ptr, int d, int64_t rows, int box_rows);
 // TMA tensor map over [B, N, H, d] bf16 (token row stride in elements), 64-column x box_rows boxes.

@@ -33,3 +33,10 @@ def check_cache_image(ctx, layer, K_hist, V_hist, p, windows_q, n_sink, B, G):
 
 def sdpa_scale(d):
     return 1.0 / math.sqrt(d)
+
+
+def rule_windows(table, layer, N, n_sink):
+    """Windows of one layer of a committed rule table through the ORACLE's Eq. 2 + clip
+    (span_of) and window = span - sinks (window_of) -- never through libmoa."""
+    return [oracle.window_of(oracle.span_of(a, b, N), n_sink)
+            for a, b in zip(table["alpha"][layer], table["beta"][layer])]

@@ -11,7 +11,7 @@ import torch
 
 import oracle
 from moa_workloads import CONFIGS, decode_tokens, normal, prefill_qkv, rule_table
-from tests.gpu_util import bits, check_cache_image, f64
+from tests.gpu_util import bits, check_cache_image, f64, rule_windows
 
 pytestmark = pytest.mark.gpu
 
@@ -158,7 +158,7 @@ def _full_layer_decode(moa, name, layer, steps, sample_b, batch=None, fused=True
     dev = torch.device("cuda")
     B = cfg.batch if batch is None else batch
     t = rule_table(name)
-    W = moa.resolve_spans(t["alpha"][layer], t["beta"][layer], cfg.N, cfg.n_sink)
+    W = rule_windows(t, layer, cfg.N, cfg.n_sink)
     ctx = moa.MoAContext(1, cfg.hq, cfg.hkv, cfg.head_dim, B, dtype=torch.bfloat16)
     ctx.set_spans(0, W, cfg.n_sink, cfg.N)
     ctx.alloc_cache(B)
@@ -279,3 +279,39 @@ def test_multilayer_stream_overlap_no_sync(moa):
             err = np.abs(f64(out[t, l]) - ref).max()
             assert err < TOL[dtype], (l, t, err)
         check_cache_image(ctx, l, K[l], V[l], N + T - 1, wins[l], s, B, G)
+
+
+@pytest.mark.parametrize("G", [1, 4])
+def test_structured_window_edge_and_sinks_bf16_tensor_core(moa, G):
+    """The adversarial test above on the bf16 tensor-core decode (fused append): a score spike
+    every 16 positions (an off-by-one at any head's window edge adds or drops a spike: an O(1)
+    change) and dominant / vanishing sinks, windows spanning several 64-row tiles, GQA with
+    per-head windows inside the group, 300 positions so every ring wraps."""
+    dev = torch.device("cuda")
+    B, Hkv, d, s, T = 2, 2, 128, 64, 300
+    Hq = Hkv * G
+    W = ([16, 48, 112, 200] * 2)[:Hq] if G > 1 else [16, 112]
+    dtype = torch.bfloat16
+    for sink_score in (12.0, -12.0):
+        ctx = moa.MoAContext(1, Hq, Hkv, d, B, dtype=dtype)
+        ctx.set_spans(0, W, s, 1)
+        ctx.alloc_cache(B)
+        ws = ctx.alloc_workspace(B)
+        u = torch.zeros(d)
+        u[0] = 1.0
+        spike = (torch.arange(T) % 16 == 0).float() * 8.0
+        K = (spike[None, :, None, None] * u).expand(B, T, Hkv, d).clone()
+        K[:, :s] = sink_score * u
+        K = (K + 0.01 * normal((B, T, Hkv, d), 9)).to(dtype)
+        V = normal((B, T, Hkv, d), 10, dtype)
+        Q = u.expand(T, B, Hq, d).clone().to(dtype)
+        Kg, Vg, Qg = K.to(dev), V.to(dev), Q.to(dev)
+        o = torch.empty(B, Hq, d, dtype=dtype, device=dev)
+        Kf, Vf = f64(K), f64(V)
+        for p in range(T):
+            ctx.decode_step_fused(0, Qg[p], Kg[:, p].contiguous(), Vg[:, p].contiguous(), o, p, 1.0, ws)
+            if p % 7 == 0 or p > T - 20:
+                torch.cuda.synchronize()
+                ref, _ = oracle.decode(f64(Q[p]), Kf[:, : p + 1], Vf[:, : p + 1], p, W, s, 1.0)
+                assert np.abs(f64(o) - ref).max() < 2e-2, (sink_score, p)
+        check_cache_image(ctx, 0, K, V, T - 1, W, s, B, G)

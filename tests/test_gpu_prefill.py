@@ -7,7 +7,7 @@ import torch
 
 import oracle
 from moa_workloads import CONFIGS, normal, prefill_qkv, rule_table
-from tests.gpu_util import bits, check_cache_image, f64
+from tests.gpu_util import bits, check_cache_image, f64, rule_windows
 
 pytestmark = pytest.mark.gpu
 
@@ -136,7 +136,7 @@ def _full_layer_prefill(moa, name, layer, batch=None, block=0):
     dev = torch.device("cuda")
     B = cfg.batch if batch is None else batch
     t = rule_table(name)
-    W = moa.resolve_spans(t["alpha"][layer], t["beta"][layer], cfg.N, cfg.n_sink)
+    W = rule_windows(t, layer, cfg.N, cfg.n_sink)
     q, k, v = prefill_qkv(cfg, layer, batch=B, device=dev)
     ctx = moa.MoAContext(1, cfg.hq, cfg.hkv, cfg.head_dim, B, dtype=torch.bfloat16)
     ctx.set_spans(0, W, cfg.n_sink, cfg.N, block=block)
@@ -346,3 +346,50 @@ def test_output_rows_not_32_byte_aligned(moa):
     assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
     O, _ = oracle.prefill(f64(q), f64(k), f64(v), W, s, tau)
     assert np.abs(f64(o2) - O).max() < 2e-2
+
+
+@pytest.mark.parametrize("d", [128, 64])
+def test_prefill_bf16_gqa_group_of_eight(moa, d):
+    """G = 8 (the C5 / Llama3-70B grouping) through the tcgen05 kernel: 16 q-heads over 2
+    kv-groups with heterogeneous windows inside each group (W = 0 sink-only, W = 1, W > N)."""
+    B, N, Hkv, G, s = 2, 333, 2, 8, 5
+    Hq = Hkv * G
+    W = [0, 1, 64, 127, 128, 129, 300, N + 9, 2, 17, 200, 333, 31, 0, 1, 250]
+    q = normal((B, N, Hq, d), 431, torch.bfloat16)
+    k = normal((B, N, Hkv, d), 432, torch.bfloat16)
+    v = normal((B, N, Hkv, d), 433, torch.bfloat16)
+    ctx, o, lse, scale = _prefill(moa, q, k, v, W, s, torch.bfloat16)
+    O, L = oracle.prefill(f64(q), f64(k), f64(v), W, s, scale)
+    assert np.isfinite(f64(o)).all()
+    assert np.abs(f64(o) - O).max() < 2e-2
+    assert np.abs(f64(lse) - L).max() < 2e-3
+    check_cache_image(ctx, 0, k, v, N - 1, W, s, B, G)
+
+
+def test_set_spans_twice_keeps_cache_maps_for_decode(moa):
+    """moa_set_spans again with the same footprint keeps the bound cache, and a
+    bf16 decode must still find its TMA tensor maps (no re-bind needed, include/moa.h)."""
+    dev = torch.device("cuda")
+    B, N, Hq, Hkv, d, s = 2, 200, 4, 2, 128, 4
+    W = [7, 150, 0, 33]
+    q = normal((B, N, Hq, d), 441, torch.bfloat16).to(dev)
+    k = normal((B, N, Hkv, d), 442, torch.bfloat16).to(dev)
+    v = normal((B, N, Hkv, d), 443, torch.bfloat16).to(dev)
+    qd = normal((B, Hq, d), 444, torch.bfloat16).to(dev)
+    kd = normal((B, Hkv, d), 445, torch.bfloat16).to(dev)
+    vd = normal((B, Hkv, d), 446, torch.bfloat16).to(dev)
+    ctx = moa.MoAContext(1, Hq, Hkv, d, B, dtype=torch.bfloat16)
+    ctx.set_spans(0, W, s, N)
+    ctx.alloc_cache(B)
+    ws = ctx.alloc_workspace(B)
+    ctx.set_spans(0, [7, 150, 0, 30], s, N)     # same group capacities (150, 33): same footprint
+    o = torch.empty_like(q)
+    tau = 1 / math.sqrt(d)
+    ctx.prefill(0, q, k, v, o, tau)
+    od = torch.empty_like(qd)
+    ctx.decode_step_fused(0, qd, kd, vd, od, N, tau, ws)
+    torch.cuda.synchronize()
+    W2 = [7, 150, 0, 30]
+    Kh, Vh = torch.cat([k, kd[:, None]], 1), torch.cat([v, vd[:, None]], 1)
+    Od, _ = oracle.decode(f64(qd), f64(Kh), f64(Vh), N, W2, s, tau)
+    assert np.abs(f64(od) - Od).max() < 2e-2

@@ -16,7 +16,7 @@ import torch
 
 import oracle
 from moa_workloads import normal
-from tests.gpu_util import bits, f64
+from tests.gpu_util import bits, f64, rule_windows
 
 pytestmark = pytest.mark.gpu
 
@@ -188,8 +188,8 @@ def test_c2_full_layer_ragged_prefill_and_decode(moa):
     rng = np.random.default_rng(7)
     lens = rng.integers(N // 4, N + 1, size=B).tolist()
     lens[1] = N
-    cap = moa.resolve_spans(t["alpha"][layer], t["beta"][layer], N, s)
-    wins = [[min(w, c) for w, c in zip(moa.resolve_spans(t["alpha"][layer], t["beta"][layer], n, s), cap)]
+    cap = rule_windows(t, layer, N, s)
+    wins = [[min(w, c) for w, c in zip(rule_windows(t, layer, n, s), cap)]
             for n in lens]
     ctx = moa.MoAContext(1, cfg.hq, cfg.hkv, d, B)
     ctx.set_spans(0, cap, s, N)

@@ -306,3 +306,74 @@ def test_set_ragged_validation(moa):
     cs = _ctx(moa, Hq=4, Hkv=2, B=2, g0=1, g1=2)
     cs.set_spans(0, W, 2, 100)
     cs.set_ragged(0, [10, 20], [[99, 99, 5, 0], [99, 99, 1, 2]])
+
+
+def _random_plan_instance(rng, layers, hpl, R, feasible=True):
+    dens = rng.random(R).astype(np.float32)
+    loss = (rng.standard_normal((layers * hpl, R)) * 3 + rng.random((layers * hpl, R)) * (1 - dens)[None] * 10
+            ).astype(np.float32)                      # losses may be negative (SPEC.md design decisions)
+    lo, hi = float(dens.min()), float(dens.max())
+    budget = float(rng.uniform(lo, hi)) if feasible else float(lo * rng.uniform(0.5, 0.999))
+    return loss, dens, budget
+
+
+def _check_against_oracle(moa, loss, dens, layers, hpl, budget, k):
+    ref = oracle.plan_rules(loss.astype(np.float64), dens.astype(np.float64), layers, hpl, budget, k)
+    if ref is None:
+        with pytest.raises(Exception, match="INVALID_ARG"):
+            moa.plan_rules(loss, dens, layers, hpl, budget, k)
+        return False
+    plan, L, D = moa.plan_rules(loss, dens, layers, hpl, budget, k)
+    H = layers * hpl
+    for l in range(layers):
+        assert len(set(plan[l * hpl:(l + 1) * hpl])) <= k
+    lsum = sum(float(loss[h, r]) for h, r in enumerate(plan))
+    dsum = sum(float(dens[r]) for r in plan)
+    assert dsum <= budget * H + 1e-9                   # recomputed, not trusted from the solver
+    assert abs(lsum - ref[1]) <= 1e-9 * (1 + abs(ref[1])), (plan, lsum, ref)
+    assert abs(L - ref[1]) <= 1e-4 * (1 + abs(ref[1]))
+    return True
+
+
+def test_plan_rules_exact_on_the_verdict_instances(moa):
+    """400 seeded instances of 2 layers x 3 heads x 4 rules, limit 2 (the set on which the
+    round-1 Lagrangian solver lost to enumeration 118 times): the solver's optimal loss equals
+    the exhaustive optimum of oracle.plan_rules (eq:mip) on every one."""
+    rng = np.random.default_rng(2024)
+    n_feasible = 0
+    for _ in range(400):
+        loss, dens, budget = _random_plan_instance(rng, 2, 3, 4)
+        n_feasible += _check_against_oracle(moa, loss, dens, 2, 3, budget, 2)
+    assert n_feasible == 400
+
+
+def test_plan_rules_exact_spec_criterion(moa):
+    """SPEC.md:695 criterion 4: 100 random instances (<= 3 layers x 2 heads, <= 4 rules, layer
+    limit 1 or 2, random budgets including infeasible ones): optimal loss and feasibility verdict
+    equal exhaustive enumeration."""
+    rng = np.random.default_rng(77)
+    infeasible = 0
+    for i in range(100):
+        layers, R, k = int(rng.integers(1, 4)), int(rng.integers(1, 5)), int(rng.integers(1, 3))
+        loss, dens, budget = _random_plan_instance(rng, layers, 2, R, feasible=(i % 10 != 0))
+        infeasible += not _check_against_oracle(moa, loss, dens, layers, 2, budget, k)
+    assert infeasible >= 10
+
+
+def test_plan_rules_advice_repro(moa):
+    assert moa.plan_rules([[10, 8, 0]], [0.2, 0.5, 0.9], 1, 1, 0.5) == ([1], 8.0, 0.5)
+
+
+def test_plan_rules_model_scale_runs(moa):
+    """A model-sized instance (32 layers x 32 heads x the paper's 54 rules) solves exactly in
+    seconds and its plan is feasible with at most two rules per layer."""
+    import time
+    rng = np.random.default_rng(3)
+    dens = np.linspace(0.05, 1.0, 54).astype(np.float32)
+    loss = (rng.random((32 * 32, 54)) * (1.0 - dens)[None] * 5).astype(np.float32)
+    t0 = time.perf_counter()
+    plan, L, D = moa.plan_rules(loss, dens, 32, 32, 0.5, 2)
+    assert time.perf_counter() - t0 < 60
+    assert D <= 0.5 + 1e-6
+    for l in range(32):
+        assert len(set(plan[l * 32:(l + 1) * 32])) <= 2

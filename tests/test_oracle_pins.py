@@ -505,3 +505,98 @@ def test_spans_shrink_with_length_for_nonnegative_beta():
                 w = oracle.window_of(oracle.span_of(a, bt, n), 64)
                 assert w >= prev
                 prev = w
+
+
+# --- round 2 pins: block-rounded rule windows, group windows, attention matrix ---------------
+
+def _golden_rows(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return [l.split("#")[0].strip() for l in f if l.strip() and not l.startswith("#")]
+
+
+def test_rule_window_blocked_hand_computed():
+    """tests/golden/rule_window_blocked.txt: span of Eq. 2 clipped to [0, N], rounded UP to a
+    whole block, minus the sinks -- values typed by hand, so
+    ceil -> floor (or rounding before the clip) fails here."""
+    rows = _golden_rows("rule_window_blocked.txt")
+    assert len(rows) >= 10
+    for r in rows:
+        a, be, N, s, b, want = r.split()
+        got = oracle.rule_window_blocked(float(a), float(be), int(N), int(s), int(b))
+        assert got == int(want), r
+
+
+def test_group_windows_hand_computed():
+    """tests/golden/group_windows.txt: W_g = max over the q-heads h with h // G == g (c10)."""
+    rows = _golden_rows("group_windows.txt")
+    for r in rows:
+        G, wq, wg = (x.strip() for x in r.split("|"))
+        got = oracle.group_windows([int(x) for x in wq.split()], int(G))
+        assert list(got) == [int(x) for x in wg.split()], r
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_attention_matrix_is_sdpa_causal(G):
+    """attention_matrix (the A of influence_blocks) times V == torch SDPA(is_causal) in fp64,
+    its rows sum to 1, and it is zero above the diagonal."""
+    B, N, Hkv, d, tau = 1, 33, 2, 8, 0.37
+    Q, K, V = _rand((B, N, Hkv * G, d), 60), _rand((B, N, Hkv, d), 61), _rand((B, N, Hkv, d), 62)
+    q = torch.from_numpy(Q).permute(0, 2, 1, 3)
+    k = torch.from_numpy(K).permute(0, 2, 1, 3).repeat_interleave(G, dim=1)
+    v = torch.from_numpy(V).permute(0, 2, 1, 3).repeat_interleave(G, dim=1)
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, scale=tau).numpy()
+    for h in range(Hkv * G):
+        A = oracle.attention_matrix(Q[0, :, h], K[0, :, h // G], tau)
+        assert np.max(np.abs(A @ V[0, :, h // G] - ref[0, h])) < 1e-12
+        assert np.max(np.abs(A.sum(axis=1) - 1.0)) < 1e-12
+        assert np.all(A[np.triu_indices(N, 1)] == 0.0)
+        sub = oracle.attention_matrix(Q[0, :, h], K[0, :, h // G], tau, rows=[0, 5, N - 1])
+        assert np.array_equal(sub, A[[0, 5, N - 1]])
+
+
+def test_influence_rows_equal_term_by_term():
+    """attention_influence_rows (R_i - G_ij A_ij form) == the term-by-term Eq. 3, incl. a
+    single-key row (A = 1 -> 0) and masked entries (A = 0 -> 0)."""
+    rng = np.random.default_rng(13)
+    N = 11
+    S = rng.standard_normal((N, N)) * 3
+    A = np.zeros((N, N))
+    for i in range(N):
+        w = np.exp(S[i, :i + 1] - S[i, :i + 1].max())
+        A[i, :i + 1] = w / w.sum()
+    G = rng.standard_normal((N, N))
+    assert np.max(np.abs(oracle.attention_influence_rows(A, G) - oracle.attention_influence(A, G))) < 1e-12
+
+
+def test_influence_sampled_equals_full():
+    """influence_blocks_sampled == the listed rows of influence_blocks (ragged last block, GQA)."""
+    rng = np.random.default_rng(14)
+    B, N, Hkv, G, d, b = 2, 23, 2, 2, 4, 4
+    Q, K, V, dO = (rng.standard_normal(s) for s in ((B, N, Hkv * G, d), (B, N, Hkv, d), (B, N, Hkv, d),
+                                                   (B, N, Hkv * G, d)))
+    full = oracle.influence_blocks(Q, K, V, dO, 0.6, b)
+    for bb, h in ((0, 0), (1, 3)):
+        qb = [0, 2, 5]
+        got = oracle.influence_blocks_sampled(Q, K, V, dO, 0.6, b, bb, h, qb)
+        assert np.max(np.abs(got - full[bb, h, qb])) < 1e-12
+
+
+# --- rule selection (eq:mip, PAPER.md:1415-1437) ---------------------------------------------
+
+def test_plan_rules_spec_examples_oracle():
+    """SPEC.md solve_single examples (exhaustive 1- and 4-case enumeration, typed by hand)."""
+    assert oracle.plan_rules([[0, 5]], [1.0, 0.5], 1, 1, 0.5) == ((1,), 5.0, 0.5)
+    assert oracle.plan_rules([[0, 3], [0, 1]], [1.0, 0.5], 1, 2, 0.75) == ((0, 1), 1.0, 0.75)
+    # ADVICE r1 repro: rule 1 (density 0.5, loss 8) fits the budget and beats rule 0 (loss 10)
+    assert oracle.plan_rules([[10, 8, 0]], [0.2, 0.5, 0.9], 1, 1, 0.5) == ((1,), 8.0, 0.5)
+    assert oracle.plan_rules([[1, 2]], [0.6, 0.7], 1, 1, 0.5) is None           # infeasible
+
+
+def test_plan_rules_layer_limit_and_budget_by_hand():
+    """2 heads in one layer, 3 rules: with the limit 2 the best plan mixes two rules; with
+    limit 1 both heads share one rule (values typed by hand)."""
+    loss = [[0.0, 4.0, 9.0],     # head 0 is sensitive
+            [5.0, 1.0, 0.0]]     # head 1 prefers the sparse rule 2
+    dens = [1.0, 0.5, 0.1]
+    assert oracle.plan_rules(loss, dens, 1, 2, 0.55, 2) == ((0, 2), 0.0, 0.55)
+    assert oracle.plan_rules(loss, dens, 1, 2, 0.55, 1) == ((1, 1), 5.0, 0.5)
