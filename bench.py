@@ -39,6 +39,7 @@ import torch  # noqa: E402
 from moa_workloads import CONFIGS, decode_tokens, prefill_qkv, rule_table  # noqa: E402
 
 CFG = CONFIGS["C2"]
+DECODE_CHUNK = 256   # rows per rank-invariant decode chunk in the kv-sharded run (moa_set_decode_split)
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -347,17 +348,24 @@ def run_ours(args, rank, world, local_rank):
 
 def run_kv_shard(rank, world, dev, scale, T=64):
     """North-star partition across GPUs: the SAME batch of 8 sequences, its
-    kv-groups split over the ranks (each rank's cache holds only its groups), and after every
-    layer the head outputs all-gathered with NCCL (torch.distributed.all_gather_into_tensor
-    over NVLink) into the full [B, Hq, d] layout.  Strong scaling: decode tokens/s of the
-    whole job with and without the per-layer all-gather, device-timed, max over ranks."""
+    kv-groups split over the ranks in cost-balanced contiguous ranges (dist.plan_shards on
+    the in-window rows of every group, summed over layers; each rank's cache holds only its
+    groups), the rank-invariant decode split (so the gathered heads are the 1-GPU bits), and
+    after every layer the head outputs all-gathered with NCCL (all_gather_into_tensor over
+    NVLink, preallocated buffers: the kernel writes its heads straight into the send slab).
+    Model-faithful order: layer l+1 starts after layer l's heads are gathered (its q would
+    come from them).  Strong scaling: decode tokens/s of the whole job with and without the
+    all-gather, device-timed, max over ranks."""
     import paper_2406_14909_b200 as moa
     from paper_2406_14909_b200 import dist as mdist
 
     L, B, N, d, s, G = CFG.layers, CFG.batch, CFG.N, CFG.head_dim, CFG.n_sink, CFG.group
-    shard = mdist.plan_shards(world, CFG.hkv, B, "kv")[rank]
     windows = windows_all_layers(moa)
+    cost = mdist.group_costs(windows, s, G)
+    shards = mdist.plan_shards(world, CFG.hkv, B, "kv", group_cost=cost)
+    shard = shards[rank]
     ctx = mdist.make_context(shard, L, CFG.hq, CFG.hkv, d, device=dev.index)
+    ctx.set_decode_split(DECODE_CHUNK)
     for l in range(L):
         ctx.set_spans(l, windows[l], s, N)
     ctx.alloc_cache(B)
@@ -367,8 +375,8 @@ def run_kv_shard(rank, world, dev, scale, T=64):
     vp = torch.randn(B, N, CFG.hkv, d, device=dev, generator=g).to(torch.bfloat16)
     kl, vl = mdist.local_slice_kv(kp, shard), mdist.local_slice_kv(vp, shard)
     qd, kd, vd = decode_tokens(CFG, 0, T, device=dev)
-    hq_l = (shard.g1 - shard.g0) * G
-    od = torch.empty(B, hq_l, d, dtype=torch.bfloat16, device=dev)
+    hg = mdist.HeadGather(shards, rank, B, G, d, device=dev)
+    od = hg.local_out()
     stream = torch.cuda.current_stream()
 
     def phase(gather):
@@ -384,8 +392,11 @@ def run_kv_shard(rank, world, dev, scale, T=64):
             kt, vt = mdist.local_slice_kv(kd[t], shard), mdist.local_slice_kv(vd[t], shard)
             for l in range(L):
                 ctx.decode_step_fused(l, ql, kt, vt, od, N + t, scale, ws)
-                if gather:
-                    mdist.gather_heads(od, shard)  # [B, Hq, d] on every rank
+                if gather and world > 1:
+                    ready = torch.cuda.Event()
+                    ready.record(stream)
+                    _, done = hg.gather(ready)      # comm stream: all-gather + head permute
+                    stream.wait_event(done)         # layer l+1 consumes the gathered heads
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
@@ -398,13 +409,17 @@ def run_kv_shard(rank, world, dev, scale, T=64):
     phase(True)
     with_ag = phase(True)
     compute = phase(False)
-    return {"mode": f"kv-groups over {world} rank(s) ({CFG.hkv // world} groups each), same batch of {B}",
+    loads = [mdist.shard_cost(sh, cost) for sh in shards]
+    return {"mode": f"kv-groups over {world} rank(s), cost-balanced contiguous ranges "
+                    f"{[(sh.g0, sh.g1) for sh in shards]}, same batch of {B}",
+            "rank_load_max_over_mean": max(loads) / (sum(loads) / len(loads)),
+            "decode_split": f"rank-invariant, {DECODE_CHUNK}-row chunks (moa_set_decode_split)",
             "decode_tokens_per_s": B * T / (with_ag / 1e3),
             "decode_tokens_per_s_no_allgather": B * T / (compute / 1e3),
             "allgather_us_per_layer": (with_ag - compute) * 1e3 / (T * L),
             "tokens": T, "scaling": "strong",
-            "note": "NCCL all_gather_into_tensor of each layer's head outputs (torch.distributed), device-timed, "
-                    "max over ranks"}
+            "note": "NCCL all_gather_into_tensor of each layer's head outputs (torch.distributed, own stream, "
+                    "preallocated), serialised before the next layer; device-timed, max over ranks"}
 
 
 def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
@@ -501,11 +516,26 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kv-shard", action="store_true", help="also run the kv-group sharded decode at N = 1")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # self-launch: one rank per GPU under torchrun (the driver's own launch sets WORLD_SIZE)
+        import socket
+        import subprocess
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # communicator evidence on stderr: NCCL prints "nranks N" when each rank's comm is built
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         backend = "nccl" if args.impl == "ours" else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local_rank)

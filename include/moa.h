@@ -262,6 +262,34 @@ moa_status moa_decode_step_fused_ragged(moa_ctx *ctx, int layer, const void *q, 
                                         const int64_t *pos, float scale, float *lse_out, void *workspace,
                                         size_t ws_bytes, moa_stream_t stream);
 
+/*
+ * Decode split mode (bf16 decode).  The decode kernel spreads a layer's cache rows over
+ * the SMs; the LSE partials of a (sequence, kv-group) region are merged in a fixed order.
+ *   chunk_rows = 0 (default): balanced split -- every CTA streams the same number of rows,
+ *       so where a region is cut depends on the batch, the other regions and the SM count.
+ *   chunk_rows > 0 (a multiple of 64): rank-invariant split -- every region is cut into
+ *       chunks of chunk_rows rows from its first row and each chunk is one partial; the
+ *       arithmetic on a region's rows then depends on that region alone, so a context
+ *       serving a kv-group shard (moa_create's [g0, g1)) or a subset of the sequences
+ *       computes bit-identical outputs to the unsharded context (SURVEY §4 tier 4;
+ *       heads are independent).  256 is a good value.
+ * Applies to every layer (also layers set later); changes moa_workspace_bytes.  Must not
+ * be called while a layer is ragged (MOA_ERR_STATE).  MOA_ERR_INVALID_ARG for other values.
+ */
+moa_status moa_set_decode_split(moa_ctx *ctx, int chunk_rows);
+
+/*
+ * Advance device-resident positions: pos[b] += delta for b < batch where pos[b] >= 0
+ * (inactive sequences stay inactive).  The companion of moa_decode_step_fused_ragged for
+ * CUDA-graph capture of a whole token step (every layer's fused decode, then this call):
+ * a replayed graph moves every sequence to its next position with no host involvement
+ * (the decode call takes the position by pointer, PAPER.md:704 one token per step).
+ *   pos    DEVICE int64 [batch], 8-byte aligned, caller-owned.
+ * Stream-ordered, no allocation, no host synchronisation; MOA_ERR_INVALID_ARG for a NULL
+ * or misaligned pointer or batch < 1.
+ */
+moa_status moa_advance_pos(int64_t *pos, int batch, int64_t delta, moa_stream_t stream);
+
 /* ---------------- host-side introspection (planning contexts too) ---------------- */
 
 /* Window of a local q-head / cache capacity W_g of a local group. */

@@ -46,6 +46,8 @@ _SIGS = [
                                 c_size_t, _P]),
     ("moa_decode_step_fused", c_int, [_P, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int, c_int64,
                                       c_float, _P, _P, c_size_t, _P]),
+    ("moa_advance_pos", c_int, [_P, c_int, c_int64, _P]),
+    ("moa_set_decode_split", c_int, [_P, c_int]),
     ("moa_decode_step_fused_ragged", c_int, [_P, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int, _P,
                                              c_float, _P, _P, c_size_t, _P]),
     ("moa_get_window", c_int, [_P, c_int, c_int, POINTER(c_int32)]),

@@ -90,6 +90,8 @@ struct MParams {
   __nv_bfloat16 *kc, *vc;
   int64_t rows_per_seq, R;       // rows per sequence, total rows
   int64_t seg_cost, ctot;        // CTA split: a segment costs seg_cost rows; total cost
+  int chunk;                     // rank-invariant split: rows per chunk (0: balanced row split)
+  const int *gc_off;             // chunk mode: first chunk of each local group in a sequence [ngl + 1]
   const int64_t *g_off;
   const int32_t *win_g, *win_q;
   int ngl, G, n_sink, batch;
@@ -137,17 +139,65 @@ __device__ __forceinline__ int64_t cta_of(const MParams &p, int64_t x, int r) {
   return ((x + p.seg_cost * r) * (int64_t)gridDim.x) / p.ctot;
 }
 
+// a / b for a >= 0, b > 0: the 32-bit divide (a short instruction sequence) whenever both fit,
+// which is every config here; 64-bit division is a long dependent subroutine
+__device__ __forceinline__ int64_t udiv(int64_t a, int64_t b) {
+  return ((uint64_t)a | (uint64_t)b) >> 32 ? a / b : (int64_t)((uint32_t)a / (uint32_t)b);
+}
+
 struct Region {
   int b, g, Wg;
   int64_t start, end;  // absolute rows [start, end)
 };
+
+// Rank-invariant split (p.chunk > 0): region (b, g) is cut into chunks of p.chunk rows from
+// its first row, whatever the batch, the SM count or the other regions are; a chunk is one
+// segment with its own partial slot, so the arithmetic on a region's rows (tile boundaries,
+// warp row sets, online-softmax order, partial and combine order) depends only on the region
+// -- a kv-group shard on another GPU computes bit-identical outputs (SURVEY §4 tier 4).
+// CTAs take contiguous chunk ranges balanced by cost (rows + seg_cost per chunk).
+// s_gc[g] = first chunk of group g inside one sequence, s_gc[ngl] = chunks per sequence.
+__device__ __forceinline__ int64_t chunk_row(const MParams &p, const int64_t *g_off, const int *gc, int64_t J) {
+  const int cps = gc[p.ngl];
+  const int64_t b = udiv(J, cps);
+  if (b >= p.batch) return p.R;
+  const int jj = (int)(J - b * cps);
+  int lo = 0, hi = p.ngl - 1;  // last g with gc[g] <= jj
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (gc[mid] <= jj) lo = mid; else hi = mid - 1;
+  }
+  return b * p.rows_per_seq + g_off[lo] + (int64_t)(jj - gc[lo]) * p.chunk;
+}
+// first chunk J with cost prefix rows(J) + seg_cost * J >= T.  Sequences share one layout, so
+// the sequence is one division; inside it the group is a binary search over the group starts
+// and the chunk one more division (chunks of a group before its last are full).  Every thread
+// evaluates this before the kernel's first wait: it must stay a few hundred instructions.
+__device__ __forceinline__ int64_t chunk_cut(const MParams &p, const int64_t *g_off, const int *gc, int64_t T) {
+  const int cps = gc[p.ngl];
+  const int64_t seq_cost = p.rows_per_seq + p.seg_cost * cps;
+  const int64_t b = udiv(T, seq_cost);
+  if (b >= p.batch) return (int64_t)p.batch * cps;
+  const int64_t r = T - b * seq_cost;
+  if (r == 0) return b * cps;
+  int lo = 0, hi = p.ngl - 1;  // last g whose first chunk starts at cost < r
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (g_off[mid] + p.seg_cost * gc[mid] < r) lo = mid; else hi = mid - 1;
+  }
+  const int64_t gp = g_off[lo] + p.seg_cost * gc[lo];
+  const int64_t step = p.chunk + p.seg_cost;
+  const int64_t k = udiv(r - gp + step - 1, step);
+  const int nc = gc[lo + 1] - gc[lo];
+  return b * cps + (k >= nc ? gc[lo + 1] : gc[lo] + k);
+}
 
 constexpr int kMaxGroups = 128;
 
 // region (b, g) holding absolute row x; g_off / win_g are staged in shared memory
 __device__ __forceinline__ Region region_of(const MParams &p, const int64_t *g_off, const int *win_g, int64_t x) {
   Region r;
-  r.b = (int)(x / p.rows_per_seq);
+  r.b = (int)udiv(x, p.rows_per_seq);
   const int64_t within = x - (int64_t)r.b * p.rows_per_seq;
   int lo = 0, hi = p.ngl - 1;  // last g with g_off[g] <= within
   while (lo < hi) {
@@ -159,6 +209,13 @@ __device__ __forceinline__ Region region_of(const MParams &p, const int64_t *g_o
   r.start = (int64_t)r.b * p.rows_per_seq + g_off[lo];
   r.end = r.start + p.n_sink + r.Wg;
   return r;
+}
+
+// end of the segment starting at row x of region r (the CTA range ends at X1)
+__device__ __forceinline__ int64_t seg_end_of(const MParams &p, const Region &r, int64_t x, int64_t X1) {
+  int64_t e = r.end < X1 ? r.end : X1;
+  if (p.chunk && x + p.chunk < e) e = x + p.chunk;  // x is a chunk boundary in chunk mode
+  return e;
 }
 
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -211,7 +268,7 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 // merge costs ~ceil(slots/8) L2 round trips per head.
 template <int D>
 __device__ __forceinline__ void combine_region_warp(const MParams &p, const int64_t *g_off, const int *win_g,
-                                                    int ridx, int lane) {
+                                                    const int *gc, int ridx, int lane) {
   constexpr int PS = part_stride<D>();
   constexpr int NE = D / 32;
   constexpr int KB = 8;
@@ -219,9 +276,16 @@ __device__ __forceinline__ void combine_region_warp(const MParams &p, const int6
   const int G = p.G;
   const int64_t start = (int64_t)b * p.rows_per_seq + g_off[g];
   const int64_t end = start + p.n_sink + win_g[g];
-  const int64_t c_first = cta_of(p, start, ridx), c_last = cta_of(p, end - 1, ridx);
-  const int64_t sl0 = c_first + ridx;
-  const int nsl = (int)(c_last - c_first + 1);
+  int64_t sl0;
+  int nsl;
+  if (p.chunk) {
+    sl0 = (int64_t)b * gc[p.ngl] + gc[g];
+    nsl = gc[g + 1] - gc[g];
+  } else {
+    const int64_t c_first = cta_of(p, start, ridx), c_last = cta_of(p, end - 1, ridx);
+    sl0 = c_first + ridx;
+    nsl = (int)(c_last - c_first + 1);
+  }
   for (int j = 0; j < G; ++j) {
     const float *base = p.part + (sl0 * G + j) * PS;
     float mx = -INFINITY, L = 0.f, O[NE];
@@ -276,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
   __shared__ uint64_t full_bar[C::kStages], empty_bar[C::kStages];
   __shared__ int64_t s_goff[kMaxGroups];
   __shared__ int s_wing[kMaxGroups];
+  __shared__ int s_gc[kMaxGroups + 1];
   __shared__ __align__(16) __nv_bfloat16 s_q[2][16 * QS];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -296,9 +361,20 @@ __global__ void __launch_bounds__(kThreads, CPS)
     s_wing[g] = p.win_g[g];
   }
   __syncthreads();
+  if (p.chunk)
+    for (int g = tid; g <= p.ngl; g += kThreads) s_gc[g] = p.gc_off[g];
+  __syncthreads();
   const int64_t n_cta = gridDim.x;
-  const int64_t X0 = cut_row(p, s_goff, ((int64_t)blockIdx.x * p.ctot + n_cta - 1) / n_cta);
-  const int64_t X1 = cut_row(p, s_goff, ((int64_t)(blockIdx.x + 1) * p.ctot + n_cta - 1) / n_cta);
+  int64_t X0, X1;
+  if (p.chunk) {
+    const int64_t J0 = chunk_cut(p, s_goff, s_gc, ((int64_t)blockIdx.x * p.ctot + n_cta - 1) / n_cta);
+    const int64_t J1 = chunk_cut(p, s_goff, s_gc, ((int64_t)(blockIdx.x + 1) * p.ctot + n_cta - 1) / n_cta);
+    X0 = chunk_row(p, s_goff, s_gc, J0);
+    X1 = chunk_row(p, s_goff, s_gc, J1);
+  } else {
+    X0 = cut_row(p, s_goff, ((int64_t)blockIdx.x * p.ctot + n_cta - 1) / n_cta);
+    X1 = cut_row(p, s_goff, ((int64_t)(blockIdx.x + 1) * p.ctot + n_cta - 1) / n_cta);
+  }
   // Programmatic dependent launch.  Everything above overlapped the previous kernel's tail.
   // The consumers and the epilogue warp wait for the stream predecessor (q, k_new, the
   // workspace, the tickets and o may be its inputs/outputs) before they trigger the next
@@ -323,9 +399,11 @@ __global__ void __launch_bounds__(kThreads, CPS)
       TRACE(2);
       int T = 0;
       bool trig = false;
+      Region rg;
+      rg.end = -1;
       for (int64_t x = X0; x < X1;) {
-        const Region rg = region_of(p, s_goff, s_wing, x);
-        const int64_t seg_end = rg.end < X1 ? rg.end : X1;
+        if (x >= rg.end) rg = region_of(p, s_goff, s_wing, x);
+        const int64_t seg_end = seg_end_of(p, rg, x, X1);
         for (int64_t t0 = x; t0 < seg_end; t0 += kRows, ++T) {
           const int st = T % C::kStages;
           if (T >= C::kStages) {
@@ -367,34 +445,51 @@ __global__ void __launch_bounds__(kThreads, CPS)
     const int G = p.G;
     int64_t xs = X0;  // staging cursor (runs two segments ahead of the consumers)
     int ns = 0;
+    int buf_region[2] = {-1, -1};  // region whose q rows each staging buffer holds
+    Region r;
+    r.end = -1;
     auto stage_next = [&]() {
       if (xs >= X1) return;
-      const Region r = region_of(p, s_goff, s_wing, xs);
-      const __nv_bfloat16 *qb = p.q + (int64_t)r.b * p.q_bs + (int64_t)r.g * G * D;
-      __nv_bfloat16 *sq = s_q[ns & 1];
-      for (int v = lane; v < G * (D / 8); v += 32) {
-        const int h = v / (D / 8), e = (v - h * (D / 8)) * 8;
-        *reinterpret_cast<uint4 *>(sq + h * QS + e) = *reinterpret_cast<const uint4 *>(qb + h * D + e);
+      if (xs >= r.end) r = region_of(p, s_goff, s_wing, xs);
+      const int ridx = r.b * p.ngl + r.g;
+      if (buf_region[ns & 1] != ridx) {  // consecutive chunks of one region share their q rows
+        const __nv_bfloat16 *qb = p.q + (int64_t)r.b * p.q_bs + (int64_t)r.g * G * D;
+        __nv_bfloat16 *sq = s_q[ns & 1];
+        for (int v = lane; v < G * (D / 8); v += 32) {
+          const int h = v / (D / 8), e = (v - h * (D / 8)) * 8;
+          *reinterpret_cast<uint4 *>(sq + h * QS + e) = *reinterpret_cast<const uint4 *>(qb + h * D + e);
+        }
+        buf_region[ns & 1] = ridx;
       }
       named_bar_arrive(kBarQFull + (ns & 1), kHandoff);
-      xs = r.end < X1 ? r.end : X1;
+      xs = seg_end_of(p, r, xs, X1);
       ++ns;
     };
     stage_next();
     stage_next();
     int n = 0;
+    int run = 0;  // segments of the current region this CTA has finished (one ticket per run)
+    Region rg;
+    rg.end = -1;
+    int64_t slot = 0;
     for (int64_t x = X0; x < X1; ++n) {
-      const Region rg = region_of(p, s_goff, s_wing, x);
-      const int64_t seg_end = rg.end < X1 ? rg.end : X1;
+      if (x >= rg.end) {
+        rg = region_of(p, s_goff, s_wing, x);
+        slot = p.chunk ? (int64_t)rg.b * s_gc[p.ngl] + s_gc[rg.g] + (x - rg.start) / p.chunk
+                       : (int64_t)blockIdx.x + rg.b * p.ngl + rg.g;
+      } else {
+        ++slot;  // next chunk of the same region (chunk mode only)
+      }
+      const int64_t seg_end = seg_end_of(p, rg, x, X1);
       named_bar_sync(kBarSegDone + (n & 1), kHandoff);
       // every consumer warp's partial of segment n is in shared memory (mbarrier release/
-      // acquire): merge the kCW of them by LSE into this CTA's slot of the region
+      // acquire): merge the kCW of them by LSE into this segment's slot
       const int ridx = rg.b * p.ngl + rg.g;
       {
         constexpr int PS = part_stride<D>();
         constexpr int NE = D / 32;
         const float *sp = s_part + (size_t)(n & 1) * kCW * G * PS;
-        float *gp = p.part + ((int64_t)blockIdx.x + ridx) * G * PS;
+        float *gp = p.part + slot * G * PS;
         for (int j = 0; j < G; ++j) {
           float ls[kCW], mx = -INFINITY;
 #pragma unroll
@@ -421,22 +516,31 @@ __global__ void __launch_bounds__(kThreads, CPS)
         }
         __syncwarp();
       }
+      ++run;
+      const bool run_ends = seg_end >= rg.end || seg_end >= X1;
       int last = 0;
-      if (lane == 0) {
-        __threadfence();  // cumulative: orders the consumers' partials before the ticket
-        const int64_t c_first = cta_of(p, rg.start, ridx), c_last = cta_of(p, rg.end - 1, ridx);
+      if (run_ends && lane == 0) {
+        __threadfence();  // cumulative: orders the partials of the run before the ticket
+        int contributors;
+        if (p.chunk) {
+          contributors = s_gc[rg.g + 1] - s_gc[rg.g];
+        } else {
+          const int64_t c_first = cta_of(p, rg.start, ridx), c_last = cta_of(p, rg.end - 1, ridx);
+          contributors = (int)(c_last - c_first + 1);
+        }
         int *ctr = p.counters + ridx;
-        const int ticket = atomicAdd(ctr, 1);
-        if (ticket == (int)(c_last - c_first)) {
+        const int ticket = atomicAdd(ctr, run);
+        if (ticket + run == contributors) {
           *ctr = 0;  // self-reset for the next launch
           last = 1;
         }
       }
+      if (run_ends) run = 0;
       last = __shfl_sync(0xffffffffu, last, 0);
       stage_next();  // q of segment n+2 into the buffer segment n used
       if (last) {
         __threadfence();
-        combine_region_warp<D>(p, s_goff, s_wing, ridx, lane);
+        combine_region_warp<D>(p, s_goff, s_wing, s_gc, ridx, lane);
       }
       x = seg_end;
     }
@@ -455,27 +559,36 @@ __global__ void __launch_bounds__(kThreads, CPS)
 #ifdef MOA_DEC_TRACE
   int nseg = 0;
 #endif
+  // per-region state, recomputed only when a segment starts a new region (a CTA's consecutive
+  // chunks of one region reuse it: no global loads or 64-bit divisions between them)
+  Region rg;
+  rg.end = -1;
+  int64_t pos = 0, slot_p = -1;
+  int W0 = 0, W1 = 0, pm = 0, slot_r = -1, pos32 = 0, ring_age_max = 0;
+  bool ring_live = false, seg_full = false;
+  const int G = p.G;
   for (int64_t x = X0; x < X1; ++n) {
-    const Region rg = region_of(p, s_goff, s_wing, x);
-    const int64_t seg_end = rg.end < X1 ? rg.end : X1;
-    const int G = p.G;
+    if (x >= rg.end) {
+      rg = region_of(p, s_goff, s_wing, x);
+      pos = p.pos_b ? p.pos_b[rg.b] : p.pos;
+      const int32_t *wq = p.win_bq ? p.win_bq + (int64_t)rg.b * p.ngl * G : p.win_q;
+      W0 = h0 < G ? wq[rg.g * G + h0] : rg.Wg;
+      W1 = h1 < G ? wq[rg.g * G + h1] : rg.Wg;
+      ring_live = pos >= s && rg.Wg > 0;
+      pm = ring_live ? (int)((pos - s) % rg.Wg) : 0;
+      slot_p = (p.k_new != nullptr) ? slot_of(pos, s, rg.Wg) : -1;
+      slot_r = (int)slot_p;  // region row of the fused token (-1: none)
+      pos32 = pos < (int64_t)0x7fffffff ? (int)pos : 0x7fffffff;
+      ring_age_max = (int)((pos - s) < (int64_t)0x7fffffff ? (pos - s) : (int64_t)0x7fffffff);
+      // every sink and ring row holds a position and every real head sees the whole ring
+      const int minW = (W0 < W1 ? W0 : W1);
+      seg_full = pos - s >= (int64_t)rg.Wg - 1 && pos >= s &&
+                 __reduce_min_sync(0xffffffffu, (unsigned)minW) >= (unsigned)rg.Wg;
+    }
+    const int64_t seg_end = seg_end_of(p, rg, x, X1);
 #ifdef MOA_DEC_TRACE
     ++nseg;
 #endif
-    const int64_t pos = p.pos_b ? p.pos_b[rg.b] : p.pos;
-    const int32_t *wq = p.win_bq ? p.win_bq + (int64_t)rg.b * p.ngl * G : p.win_q;
-    const int W0 = h0 < G ? wq[rg.g * G + h0] : rg.Wg;
-    const int W1 = h1 < G ? wq[rg.g * G + h1] : rg.Wg;
-    const bool ring_live = pos >= s && rg.Wg > 0;
-    const int pm = ring_live ? (int)((pos - s) % rg.Wg) : 0;
-    const int64_t slot_p = (p.k_new != nullptr) ? slot_of(pos, s, rg.Wg) : -1;
-    const int slot_r = (int)slot_p;  // region row of the fused token (-1: none)
-    const int pos32 = pos < (int64_t)0x7fffffff ? (int)pos : 0x7fffffff;
-    const int ring_age_max = (int)((pos - s) < (int64_t)0x7fffffff ? (pos - s) : (int64_t)0x7fffffff);
-    // every sink and ring row holds a position and every real head sees the whole ring
-    const int minW = (W0 < W1 ? W0 : W1);
-    const bool seg_full = pos - s >= (int64_t)rg.Wg - 1 && pos >= s &&
-                          __reduce_min_sync(0xffffffffu, (unsigned)minW) >= (unsigned)rg.Wg;
 
     // Q fragments (A operand, 16 x D, rows >= G are zero) from the staged rows, unscaled bf16
     uint32_t qa[KS][4];
@@ -740,7 +853,10 @@ int launch_v(const DecodeMmaArgs &a, void *stream) {
     return e ? (int64_t)std::atoll(e) : (int64_t)128;
   }();
   p.seg_cost = seg_cost;
-  p.ctot = p.R + seg_cost * ((int64_t)a.batch * a.ngl - 1);
+  p.chunk = a.chunk;
+  p.gc_off = a.d_gc_off;
+  p.ctot = a.chunk ? p.R + seg_cost * (int64_t)a.batch * a.chunks_per_seq
+                   : p.R + seg_cost * ((int64_t)a.batch * a.ngl - 1);
   p.g_off = a.d_g_off;
   p.win_g = a.d_win_g;
   p.win_q = a.d_win_q;
@@ -800,8 +916,10 @@ int launch_d(const DecodeMmaArgs &a, void *stream) {
 
 }  // namespace
 
-size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d) {
-  const size_t slots = (size_t)num_sms_dev() * kCtasPerSm + (size_t)batch * ngl + 1;  // (CTA, region) slots
+size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d, int chunks_per_seq) {
+  // one slot per (CTA, region) pair (balanced split) or per chunk (rank-invariant split)
+  const size_t slots = chunks_per_seq > 0 ? (size_t)batch * chunks_per_seq + 1
+                                          : (size_t)num_sms_dev() * kCtasPerSm + (size_t)batch * ngl + 1;
   return ((slots * G * (d + 4) * 4) + 255) & ~size_t(255);
 }
 

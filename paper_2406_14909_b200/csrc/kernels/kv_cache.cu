@@ -103,4 +103,14 @@ int launch_kv_append(const CacheArgs &a, void *stream) {
   return (int)cudaGetLastError();
 }
 
+__global__ void advance_pos_kernel(int64_t *pos, int batch, int64_t delta) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch && pos[b] >= 0) pos[b] += delta;
+}
+
+int launch_advance_pos(int64_t *pos, int batch, int64_t delta, void *stream) {
+  advance_pos_kernel<<<(batch + 127) / 128, 128, 0, (cudaStream_t)stream>>>(pos, batch, delta);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace moa

@@ -97,7 +97,7 @@ void free_tables(LayerPlan &p) {
   p.d_tables = nullptr;
   p.d_win_q = p.d_win_g = nullptr;
   p.d_g_off = nullptr;
-  p.d_items = p.d_items2 = p.d_chunks = p.d_g_chunk = nullptr;
+  p.d_items = p.d_items2 = p.d_chunks = p.d_g_chunk = p.d_gc_off = nullptr;
   p.d_counters = nullptr;
 }
 
@@ -112,7 +112,8 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   size_t o_items2 = align16(o_items + p.items.size() * 4);
   size_t o_chunks = align16(o_items2 + p.items2.size() * 4);
   size_t o_gch = align16(o_chunks + p.chunks.size() * 4);
-  size_t o_cnt = align16(o_gch + p.g_chunk.size() * 4);
+  size_t o_gco = align16(o_gch + p.g_chunk.size() * 4);
+  size_t o_cnt = align16(o_gco + p.gc_off.size() * 4);
   size_t total = align16(o_cnt + (size_t)ctx->max_batch * ctx->ngl * 4);
   std::vector<unsigned char> host(total, 0);
   std::memcpy(host.data() + o_winq, p.win_q.data(), p.win_q.size() * 4);
@@ -122,6 +123,7 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   std::memcpy(host.data() + o_items2, p.items2.data(), p.items2.size() * 4);
   std::memcpy(host.data() + o_chunks, p.chunks.data(), p.chunks.size() * 4);
   std::memcpy(host.data() + o_gch, p.g_chunk.data(), p.g_chunk.size() * 4);
+  std::memcpy(host.data() + o_gco, p.gc_off.data(), p.gc_off.size() * 4);
   DeviceGuard dg(ctx->device);
   free_tables(p);
   void *d = nullptr;
@@ -141,6 +143,7 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   p.d_items2 = reinterpret_cast<const int32_t *>(b + o_items2);
   p.d_chunks = reinterpret_cast<const int32_t *>(b + o_chunks);
   p.d_g_chunk = reinterpret_cast<const int32_t *>(b + o_gch);
+  p.d_gc_off = reinterpret_cast<const int32_t *>(b + o_gco);
   p.d_counters = reinterpret_cast<int *>(b + o_cnt);
   return MOA_OK;
 }
@@ -204,6 +207,7 @@ moa_status moa_create(moa_ctx **out, int device, moa_dtype dtype, int num_layers
   c->ngl = kv_group_end - kv_group_begin;
   c->nql = c->ngl * G;
   c->layers.resize(num_layers);
+  if (const char *e = std::getenv("MOA_DEC_CHUNK")) c->dec_chunk = std::max(0, std::atoi(e));  // tuning
   *out = c;
   return ok();
 }
@@ -351,6 +355,14 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
   c = std::max<int64_t>(64, std::min<int64_t>(c, 4096));
   if (int ov = decode_chunk_rows_override()) c = ov;
   np.chunk_rows = (int)c;
+  np.dec_cps = 0;
+  np.gc_off.assign(ctx->ngl + 1, 0);
+  if (ctx->dec_chunk > 0)
+    for (int g = 0; g < ctx->ngl; ++g) {
+      np.gc_off[g] = np.dec_cps;
+      np.dec_cps += (int)(((int64_t)n_sink + np.win_g[g] + ctx->dec_chunk - 1) / ctx->dec_chunk);
+    }
+  np.gc_off[ctx->ngl] = np.dec_cps;
   np.g_chunk.resize(ctx->ngl + 1);
   np.max_chunks_per_group = 0;
   for (int g = 0; g < ctx->ngl; ++g) {
@@ -538,7 +550,8 @@ moa_status moa_workspace_bytes(const moa_ctx *ctx, int batch, size_t *bytes) {
       mx = std::max(mx, moa::decode_ws_bytes(batch, (int)(p.chunks.size() / 3), ctx->G, ctx->d));
   if (ctx->dtype == MOA_BF16 && ctx->device >= 0) {
     DeviceGuard dg(ctx->device);
-    mx = std::max(mx, moa::decode_mma_ws_bytes(batch, ctx->ngl, ctx->G, ctx->d));
+    for (const auto &p : ctx->layers)
+      if (p.set) mx = std::max(mx, moa::decode_mma_ws_bytes(batch, ctx->ngl, ctx->G, ctx->d, p.dec_cps));
   }
   *bytes = mx;
   return ok();
@@ -795,7 +808,7 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(MOA_ERR_INVALID_ARG, "scale must be finite > 0");
   const int n_chunks = (int)(p.chunks.size() / 3);
   const bool mma_path = ctx->dtype == MOA_BF16;
-  size_t need = mma_path ? moa::decode_mma_ws_bytes(batch, ctx->ngl, ctx->G, ctx->d)
+  size_t need = mma_path ? moa::decode_mma_ws_bytes(batch, ctx->ngl, ctx->G, ctx->d, p.dec_cps)
                          : moa::decode_ws_bytes(batch, n_chunks, ctx->G, ctx->d);
   if (!workspace || ws_bytes < need)
     return fail(MOA_ERR_OOM, "workspace of %zu bytes < %zu needed", ws_bytes, need);
@@ -813,6 +826,9 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
     m.pos = pos; m.scale = scale; m.lse = lse_out; m.ws_part = static_cast<float *>(workspace);
     m.d_pos = d_pos; m.d_win_bq = d_win_bq;
     m.counters = p.d_counters;
+    m.chunk = ctx->dec_chunk;
+    m.chunks_per_seq = p.dec_cps;
+    m.d_gc_off = p.d_gc_off;
     m.early_read = early_read_enabled() && ctx->last_cache_write != layer &&
                    ctx->last_cache_write != moa_ctx::kAllLayers;
     int e = moa::launch_decode_mma(m, stream);
@@ -865,6 +881,37 @@ moa_status moa_decode_step_fused_ragged(moa_ctx *ctx, int layer, const void *q, 
   if (!pos) return fail(MOA_ERR_INVALID_ARG, "pos array is NULL");
   return decode_common(ctx, layer, q, k_new, v_new, o, q_batch_stride, kv_batch_stride, o_batch_stride,
                        batch, 0, scale, lse_out, workspace, ws_bytes, stream, true, pos);
+}
+
+moa_status moa_set_decode_split(moa_ctx *ctx, int chunk_rows) {
+  if (!ctx) return fail(MOA_ERR_INVALID_ARG, "ctx is NULL");
+  if (chunk_rows != 0 && (chunk_rows < 64 || chunk_rows > (1 << 20) || chunk_rows % 64))
+    return fail(MOA_ERR_INVALID_ARG, "chunk_rows %d: 0 or a multiple of 64 in [64, 2^20]", chunk_rows);
+  for (const auto &p : ctx->layers)
+    if (p.rag_batch) return fail(MOA_ERR_STATE, "set the decode split before moa_set_ragged");
+  ctx->dec_chunk = chunk_rows;
+  for (auto &p : ctx->layers) {
+    if (!p.set) continue;
+    p.dec_cps = 0;
+    p.gc_off.assign(ctx->ngl + 1, 0);
+    if (chunk_rows > 0)
+      for (int g = 0; g < ctx->ngl; ++g) {
+        p.gc_off[g] = p.dec_cps;
+        p.dec_cps += (int)(((int64_t)p.n_sink + p.win_g[g] + chunk_rows - 1) / chunk_rows);
+      }
+    p.gc_off[ctx->ngl] = p.dec_cps;
+    moa_status st = upload_tables(ctx, p);
+    if (st) return st;
+  }
+  return ok();
+}
+
+moa_status moa_advance_pos(int64_t *pos, int batch, int64_t delta, moa_stream_t stream) {
+  if (!pos || ((uintptr_t)pos & 7)) return fail(MOA_ERR_INVALID_ARG, "pos must be a non-NULL 8-byte aligned pointer");
+  if (batch < 1) return fail(MOA_ERR_INVALID_ARG, "batch %d invalid", batch);
+  int e = moa::launch_advance_pos(pos, batch, delta, stream);
+  if (e) return cuda_fail((cudaError_t)e, "advance_pos launch");
+  return ok();
 }
 
 // ---------------------------------------------------------------------------------------------

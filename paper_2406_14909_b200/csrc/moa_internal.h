@@ -147,6 +147,9 @@ struct LayerPlan {
   std::vector<int32_t> g_chunk;  // first chunk of each group, size ngl + 1
   int chunk_rows = 0;
   int max_chunks_per_group = 0;
+  int dec_cps = 0;               // bf16 decode: rank-invariant chunks per sequence (ctx->dec_chunk rows each)
+  std::vector<int32_t> gc_off;   // first rank-invariant chunk of each group in a sequence, size ngl + 1
+  const int32_t *d_gc_off = nullptr;
   // device copies of the tables (one allocation)
   void *d_tables = nullptr;
   const int32_t *d_win_q = nullptr;
@@ -192,6 +195,8 @@ struct moa_ctx {
   // (after a bind); lets a decode launch stream its cache before its stream predecessor ends
   static constexpr int kAllLayers = -2;
   int last_cache_write = kAllLayers;
+  // bf16 decode split: rows per rank-invariant chunk (0: balanced row split, not rank-invariant)
+  int dec_chunk = 0;
 };
 
 namespace moa {
@@ -237,6 +242,7 @@ struct CacheArgs {
 };
 int launch_cache_fill(const CacheArgs &a, void *stream);
 int launch_kv_append(const CacheArgs &a, void *stream);
+int launch_advance_pos(int64_t *pos, int batch, int64_t delta, void *stream);
 
 struct DecodeArgs {
   const void *q;
@@ -285,9 +291,12 @@ struct DecodeMmaArgs {
   float *ws_part;
   int *counters;
   int early_read;              // see decode_common: predecessor does not write this layer's cache
+  int chunk;                   // rank-invariant split: rows per chunk (0: balanced row split)
+  int chunks_per_seq;          // sum_g ceil((s + W_g) / chunk)
+  const int32_t *d_gc_off;     // first chunk of each local group inside a sequence [ngl + 1]
 };
 int launch_decode_mma(const DecodeMmaArgs &a, void *stream);
-size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d);
+size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d, int chunks_per_seq);
 
 // attention influence of the profiling stage (kernels/influence.cu)
 struct InfluenceArgs {

@@ -95,6 +95,12 @@ def plan_rules(loss, density, layers: int, heads_per_layer: int, density_budget:
     return list(out), lo.value, do.value
 
 
+def advance_pos(pos: torch.Tensor, delta: int = 1, stream=None):
+    """moa_advance_pos: pos[b] += delta on the device for active sequences (pos >= 0)."""
+    assert pos.dtype == torch.int64 and pos.is_contiguous() and pos.is_cuda
+    check(_lib.lib().moa_advance_pos(_ptr(pos), pos.numel(), int(delta), _stream(stream)), "moa_advance_pos")
+
+
 class MoAContext:
     """One context per (process, device): span tables, cache layout, launches."""
 
@@ -137,6 +143,10 @@ class MoAContext:
                   "moa_set_spans_blocked")
         else:
             check(self.lib.moa_set_spans(self.ctx, layer, w, int(n_sink), int(N)), "moa_set_spans")
+
+    def set_decode_split(self, chunk_rows: int):
+        """moa_set_decode_split: 0 = balanced split (default), > 0 = rank-invariant chunks."""
+        check(self.lib.moa_set_decode_split(self.ctx, int(chunk_rows)), "moa_set_decode_split")
 
     def set_ragged(self, layer: int, seq_len: Optional[Sequence[int]], windows=None):
         """moa_set_ragged: per-sequence prompt lengths N_b and windows W_{b,h} ([B][Hq] nested

@@ -17,3 +17,13 @@ def pytest_configure(config):
 def cuda_available():
     import torch
     return torch.cuda.is_available()
+
+
+@pytest.fixture(scope="module")
+def moa():
+    """The product package (libmoa.so through ctypes); GPU tests only."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2406_14909_b200 as m
+    return m

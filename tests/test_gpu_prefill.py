@@ -382,14 +382,14 @@ def test_set_spans_twice_keeps_cache_maps_for_decode(moa):
     ctx.set_spans(0, W, s, N)
     ctx.alloc_cache(B)
     ws = ctx.alloc_workspace(B)
-    ctx.set_spans(0, [7, 150, 0, 30], s, N)     # same group capacities (150, 33): same footprint
+    ctx.set_spans(0, [9, 150, 33, 0], s, N)     # same group capacities (150, 33): same footprint
     o = torch.empty_like(q)
     tau = 1 / math.sqrt(d)
     ctx.prefill(0, q, k, v, o, tau)
     od = torch.empty_like(qd)
     ctx.decode_step_fused(0, qd, kd, vd, od, N, tau, ws)
     torch.cuda.synchronize()
-    W2 = [7, 150, 0, 30]
+    W2 = [9, 150, 33, 0]
     Kh, Vh = torch.cat([k, kd[:, None]], 1), torch.cat([v, vd[:, None]], 1)
     Od, _ = oracle.decode(f64(qd), f64(Kh), f64(Vh), N, W2, s, tau)
     assert np.abs(f64(od) - Od).max() < 2e-2

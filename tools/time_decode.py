@@ -75,6 +75,7 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--trace", action="store_true", help="read the per-CTA stamps (MOA_LIB=libmoa_trace.so)")
     ap.add_argument("--read-peak", action="store_true", help="also time a plain 4 GiB read (torch sum)")
+    ap.add_argument("--graph", action="store_true", help="also replay a CUDA graph of one token step")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     L = a.layers or cfg.layers
@@ -137,9 +138,36 @@ def main():
         tot, k = phase(mode)
         print(f"per-launch events={mode!s:5}  phase {tot:7.2f} us/launch ({by / tot / 1e3:7.1f} GB/s)   "
               f"kernel events {k:7.2f} us ({by / k / 1e3 if k == k else float('nan'):7.1f} GB/s)", flush=True)
+    if a.graph:
+        # one token step (all layers, fused decode with device positions, then moa_advance_pos)
+        # captured once in a CUDA graph and replayed T times
+        pos = torch.full((B,), N, dtype=torch.int64, device=dev)
+        q0, k0, v0 = qd[0].clone(), kd[0].clone(), vd[0].clone()
+        g = torch.cuda.CUDAGraph()
+        reset()
+        s_ = torch.cuda.Stream()
+        with torch.cuda.stream(s_):
+            with torch.cuda.graph(g, stream=s_):
+                for l in range(L):
+                    ctx.decode_step_fused_ragged(l, q0, k0, v0, od, pos, scale, ws)
+                moa.advance_pos(pos)
+        for rep in range(3):
+            reset()
+            pos.fill_(N)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for t_ in range(T):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tot = e0.elapsed_time(e1) * 1e3 / (T * L)
+            print(f"graph replay (token step = {L} layers + advance)  {tot:7.2f} us/launch ({by / tot / 1e3:7.1f} GB/s)",
+                  flush=True)
     if a.trace:
         dump_trace()
-    print(f"bytes/launch {by / 1e6:.1f} MB, batch {B}, variant {os.environ.get('MOA_DEC_VARIANT', '0')}")
+    print(f"bytes/launch {by / 1e6:.1f} MB, batch {B}, variant {os.environ.get('MOA_DEC_VARIANT', '0')}, "
+          f"chunk {os.environ.get('MOA_DEC_CHUNK', 'default')}")
     if a.read_peak:
         del kp, vp
         x = torch.empty(2 * 1024**3, dtype=torch.bfloat16, device=dev).uniform_()
