@@ -39,7 +39,7 @@ import torch  # noqa: E402
 from moa_workloads import CONFIGS, decode_tokens, prefill_qkv, rule_table  # noqa: E402
 
 CFG = CONFIGS["C2"]
-DECODE_CHUNK = 256   # rows per rank-invariant decode chunk in the kv-sharded run (moa_set_decode_split)
+DECODE_CHUNK = 512   # rows per rank-invariant decode chunk in the kv-sharded run (moa_set_decode_split)
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
