@@ -989,16 +989,20 @@ moa_status moa_attention_influence(const void *q, const void *k, const void *v, 
   if (block != 64) return fail(MOA_ERR_UNSUPPORTED, "block %d: only the paper's 64 is implemented", block);
   if (q_row_stride < (int64_t)num_q_heads * head_dim || kv_row_stride < (int64_t)num_kv_heads * head_dim)
     return fail(MOA_ERR_SHAPE, "row strides smaller than heads * head_dim");
-  if (((uintptr_t)k & 15) || ((uintptr_t)v & 15) || ((uintptr_t)q & 3) || ((uintptr_t)dout & 3) ||
-      (kv_row_stride * 2) % 16 || (q_row_stride * 2) % 4)
-    return fail(MOA_ERR_INVALID_ARG, "k/v must be 16-byte aligned (row stride too), q/dout 4-byte aligned");
+  if (((uintptr_t)k & 15) || ((uintptr_t)v & 15) || ((uintptr_t)q & 15) || ((uintptr_t)dout & 15) ||
+      (kv_row_stride * 2) % 16 || (q_row_stride * 2) % 16)
+    return fail(MOA_ERR_INVALID_ARG, "q/k/v/dout and their row strides must be 16-byte aligned (TMA)");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(MOA_ERR_INVALID_ARG, "scale must be finite > 0");
   moa::InfluenceArgs a{};
   a.q = q; a.k = k; a.v = v; a.dout = dout;
   a.q_row_stride = q_row_stride; a.kv_row_stride = kv_row_stride;
   a.batch = batch; a.N = N; a.nql = num_q_heads; a.G = num_q_heads / num_kv_heads; a.d = head_dim;
   a.scale = scale; a.e_blocks = e_blocks; a.accumulate = accumulate ? 1 : 0;
-  int e = moa::launch_influence(a, stream);
+  static const bool legacy = [] {  // diagnostics: MOA_INF_LEGACY=1 runs the round-1 mma.sync kernel (A/B)
+    const char *s = std::getenv("MOA_INF_LEGACY");
+    return s && s[0] == '1';
+  }();
+  int e = legacy ? moa::launch_influence(a, stream) : moa::launch_influence_tc(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "influence launch");
   return ok();
 }

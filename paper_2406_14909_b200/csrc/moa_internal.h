@@ -309,7 +309,8 @@ struct InfluenceArgs {
   float *e_blocks;  // [B, Hq, nb, nb] fp32
   int accumulate;
 };
-int launch_influence(const InfluenceArgs &a, void *stream);
+int launch_influence(const InfluenceArgs &a, void *stream);     // mma.sync reference design (A/B only)
+int launch_influence_tc(const InfluenceArgs &a, void *stream);  // tcgen05 + TMEM + TMA (the product)
 // Eq. 4 rule losses: window of every rule in blocks (passed by value, <= kMaxRules rules)
 constexpr int kMaxRules = 128;
 struct RuleWindows {

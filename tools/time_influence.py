@@ -2,9 +2,15 @@
 
     python tools/time_influence.py [N] [heads] [d]
 
-FLOP count: the two passes each run S = Q K^T and G = dO V^T on every causal 64 x 64
-block pair: 4 GEMMs x 2 x 64 * 64 * d per pair.
+FLOP counts (per head):
+  algorithmic -- the method's own products, S = Q K^T and G = dO V^T over the causal token
+                 pairs: 4 d per pair, sum_i (i + 1) = N (N + 1) / 2 pairs;
+  executed    -- what the kernel issues: both passes run both products on every 64-key tile
+                 of the 128-row q tiles up to the diagonal (the diagonal tiles in full).
+The roofline fraction uses the algorithmic count against the bf16 dense burst peak
+(MEASURED_PEAKS.json).  MOA_INF_LEGACY=1 times the round-1 mma.sync kernel instead.
 """
+import json
 import math
 import os
 import sys
@@ -28,15 +34,24 @@ def main(N=8192, H=32, d=128):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    reps = 3
+    reps = 5
     for _ in range(reps):
         moa.attention_influence(q, k, v, do, sc, out=out)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    pairs = nb * (nb + 1) // 2
-    flops = 4 * 2 * 64 * 64 * d * pairs * H
-    print(f"influence N={N} heads={H} d={d}: {ms:.3f} ms per item-layer, {flops / ms / 1e9:.1f} TFLOP/s (mma.sync)")
+    alg = 4 * d * (N * (N + 1) // 2) * H
+    ntile = (N + 127) // 128
+    exe_tiles = sum(min((min(128 * qt + 127, N - 1)) // 64 + 1, nb) for qt in range(ntile))
+    exe = 2 * 2 * 2 * 128 * 64 * d * exe_tiles * H
+    peak = 1645.0
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peak = json.load(open(pk)).get("bf16_tflops", peak)
+    kind = "mma.sync (legacy)" if os.environ.get("MOA_INF_LEGACY") == "1" else "tcgen05"
+    print(f"influence N={N} heads={H} d={d} [{kind}]: {ms:.3f} ms per item-layer; algorithmic "
+          f"{alg / ms / 1e9:.1f} TFLOP/s = {alg / ms / 1e9 / peak:.3f} of the {peak:.0f} TF bf16 burst; "
+          f"executed {exe / ms / 1e9:.1f} TFLOP/s", flush=True)
 
 
 if __name__ == "__main__":
