@@ -10,31 +10,33 @@
 //          sum_{n != j} G_in A_in A_ij / (1 - A_ij); E = 0 where A_ij = 1, a row's only key)
 //   out[b, h, ib, jb] (+)= mean of E over the 64 x 64 token pairs of block (ib, jb)
 //
-// Work item = 256 query rows of one (batch, q-head): q tiles j = 0, 1 of 128 rows, processed
-// in two passes over the causal key tiles of 64 keys (one kv tile = one key block):
+// Work item = one 128-row q tile of one (batch, q-head), two passes over its causal key tiles
+// of 128 keys:
 //   pass 0  row statistics: m = max_k tau s_k (log2 units); the first key attaining it (the
 //           "star", js, with G_js = Gs) is kept out of the sums, Lr = sum_{k != js} 2^(x_k - m)
 //           and Ur = sum_{k != js} G_k 2^(x_k - m), so l = 1 + Lr and R = (Gs + Ur) / l, and
 //           1 - A_js = Lr / l, R - G_js = (Ur - Gs Lr) / l keep fp32 accuracy on rows that are
 //           nearly one-hot (a sink-dominated row) where 1 - A in fp32 would cancel;
 //   pass 1  E_ij = p (C1 - G_ij l) / ((l - p) l) with p = 2^(x_ij - m), C1 = Gs + Ur (the star:
-//           E = (Ur - Gs Lr) / (Lr l)), summed per row over the tile, then over the 64 rows
-//           of a block: one block mean per (row block, kv tile).
-// Per kv tile and q tile the tensor core computes S = Q K^T and G = dO V^T (two SS MMAs,
-// M = 128, N = 64, into TMEM, double-buffered); the elementwise warps read their row of S and
-// G (thread = row = TMEM lane) and never touch A, G or E in memory.
+//           E = (Ur - Gs Lr) / (Lr l)), summed per row over a key block, then over the 64 rows
+//           of a query block: one block mean per (query block, key block).
+// Per kv tile the tensor core computes S = Q K^T and G = dO V^T (two SS MMAs, M = N = 128, K =
+// d, into TMEM, double-buffered: the next tile's products are computed while the elementwise
+// warps work on this one); the elementwise warps read their row of S and G (thread = row =
+// TMEM lane) and never touch A, G or E in memory.
 //
 // Warps (320 threads, one CTA per SM, persistent over items in LPT order):
-//   0-3  elementwise, q tile 0      4-7  elementwise, q tile 1
-//   8    TMA producer (Q, dO tiles per item; K, V tiles per step, both passes)
+//   0-7  elementwise: warp w reads TMEM lanes 32 (w % 4) .. + 31 (its 32 rows) and the key half
+//        w / 4 (columns 64 h .. 64 h + 63 of each 128-key tile = one 64-key block); the two
+//        warps of a row quarter merge their pass-0 statistics once per item
+//   8    TMA producer (Q, dO per item; K, V per step, both passes)
 //   9    TMEM allocator + MMA issue (one elected lane)
-// The two q tiles share every K/V tile, and while one tile's warps are in their elementwise
-// work the tensor core computes the other tile's products.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "../moa_internal.h"
 #include "common.cuh"
@@ -46,14 +48,24 @@ namespace {
 using namespace ptx;
 
 constexpr int kIM = 128;        // q rows per tile (MMA M)
-constexpr int kIN = 64;         // keys per kv tile (MMA N) = the paper's block
+constexpr int kIN = 128;        // keys per kv tile (MMA N)
+constexpr int kCols = 64;       // keys per elementwise warp and tile (= the paper's block)
 constexpr int kIThreads = 320;
 constexpr int kWTma = 8, kWMma = 9;
-#ifndef MOA_INF_KV_STAGES
-#define MOA_INF_KV_STAGES 3
+constexpr int kKVStagesMax = 4;
+constexpr uint32_t kITmemCols = 512;  // buffer u: S (128 cols) | G (128 cols)
+#ifndef MOA_INF_POLY_EVERY
+#define MOA_INF_POLY_EVERY 2
 #endif
-constexpr int kKVStages = MOA_INF_KV_STAGES;
-constexpr uint32_t kITmemCols = 512;  // [tile j][buffer u]: S (64 cols) | G (64 cols)
+constexpr int kPolyEvery = MOA_INF_POLY_EVERY;  // exponential pair c on the FMA pipe iff c % kPolyEvery == kPolyEvery - 1
+constexpr int kPairRound = 32;  // kv tiles between the two warps of a query block meeting
+constexpr float kRefLazy = 8.f;   // pass 0: refresh the exponent reference when the max grows by > 2^8
+constexpr float kStarLazy = 4.f;  // pass 0: move the designated key when a key beats it by > 2^4
+// diagnostics (tools/build_variant.py): 1 = elementwise warps only load and release S/G (the
+// MMA / TMA floor), 2 = no MMAs issued (the elementwise floor, on stale TMEM)
+#ifndef MOA_INF_DIAG
+#define MOA_INF_DIAG 0
+#endif
 
 template <int D>
 struct ICfg {
@@ -62,48 +74,44 @@ struct ICfg {
   static constexpr int kQSlab = kIM * 128;
   static constexpr int kKTile = kIN * D * 2;  // K or V tile bytes
   static constexpr int kKSlab = kIN * 128;
-  static constexpr int kSmem = 4 * kQTile + kKVStages * 2 * kKTile;  // Q0 dO0 Q1 dO1 | stages (K V)
+  // K/V ring depth: what fits beside the Q and dO tiles (227 KB per CTA)
+  static constexpr int kStages = D == 128 ? 2 : 4;
+  static constexpr int kSmem = 2 * kQTile + kStages * 2 * kKTile;  // Q dO | stages (K V)
 };
 
 struct IBars {
-  uint64_t q_full[2], q_empty[2];
-  uint64_t kv_full[kKVStages], kv_empty[kKVStages];
-  uint64_t s_full[2][2], s_free[2][2];
+  uint64_t q_full, q_empty;
+  uint64_t kv_full[kKVStagesMax], kv_empty[kKVStagesMax];
+  uint64_t s_full[2], s_free[2];
   uint32_t tmem_base;
 };
 
 struct IParams {
   float *out;
   int64_t N;
-  int batch, nql, G, nqb, nb, total, accumulate;
+  int batch, nql, G, nqt, nb, total, accumulate;
   float sl2;  // tau * log2(e)
 };
 
 struct IItem {
   int b, h;
   int64_t i0;
-  bool has1;
-  int tl[2];  // last kv tile of q tile j
+  int tl;  // last kv tile (of 128 keys)
 };
 
 __device__ __forceinline__ IItem get_iitem(const IParams &p, int idx) {
   IItem it;
   const int bh = p.batch * p.nql;
-  const int qb = p.nqb - 1 - idx / bh;  // longest causal rows first (LPT)
+  const int qt = p.nqt - 1 - idx / bh;  // longest causal rows of every head first (LPT)
   const int r = idx - (idx / bh) * bh;
   it.b = r / p.nql;
   it.h = r - it.b * p.nql;
-  it.i0 = (int64_t)qb * 2 * kIM;
-  it.has1 = it.i0 + kIM < p.N;
-  for (int j = 0; j < 2; ++j) {
-    int64_t last = it.i0 + (int64_t)(j + 1) * kIM - 1;
-    if (last > p.N - 1) last = p.N - 1;
-    it.tl[j] = (int)(last / kIN);
-  }
+  it.i0 = (int64_t)qt * kIM;
+  int64_t last = it.i0 + kIM - 1;
+  if (last > p.N - 1) last = p.N - 1;
+  it.tl = (int)(last / kIN);
   return it;
 }
-
-__device__ __forceinline__ uint32_t s_col(uint32_t tmem, int j, int u) { return tmem + 256u * j + 128u * u; }
 
 // ---------------------------------------------------------------- MMA issue (warp 9)
 template <int D>
@@ -111,195 +119,338 @@ __device__ __forceinline__ void inf_mma_role(const IParams &p, IBars &bars, uint
                                              uint32_t kv_smem) {
   using C = ICfg<D>;
   constexpr uint32_t idesc = idesc_bf16_f32(kIM, kIN, false);
-  int qc[2] = {0, 0}, sc[2] = {0, 0}, kvc = 0;
+  int qc = 0, sc = 0, kvc = 0;
+  const uint64_t qdesc = smem_desc_sw128(q_smem, 16, 1024), ddesc = smem_desc_sw128(q_smem + C::kQTile, 16, 1024);
   for (int idx = blockIdx.x; idx < p.total; idx += gridDim.x) {
     const IItem it = get_iitem(p, idx);
-    const int nt = 1 + (it.has1 ? it.tl[1] : it.tl[0]);
-    for (int j = 0; j < 2; ++j) {
-      if (j == 1 && !it.has1) continue;
-      mbar_wait_warp(smem_u32(&bars.q_full[j]), qc[j] & 1);
-      ++qc[j];
-    }
+    mbar_wait_warp(smem_u32(&bars.q_full), qc & 1);
+    ++qc;
     for (int pass = 0; pass < 2; ++pass) {
-      for (int t = 0; t < nt; ++t) {
-        const int st = kvc % kKVStages;
-        mbar_wait_warp(smem_u32(&bars.kv_full[st]), (kvc / kKVStages) & 1);
+      for (int t = 0; t <= it.tl; ++t, ++kvc, ++sc) {
+        const int st = kvc % C::kStages;
+        if (MOA_INF_DIAG < 4 || kvc < C::kStages) mbar_wait_warp(smem_u32(&bars.kv_full[st]), (kvc / C::kStages) & 1);
+        const int u = sc & 1;
+        if (sc >= 2 && MOA_INF_DIAG < 3) mbar_wait_warp(smem_u32(&bars.s_free[u]), ((sc - 2) >> 1) & 1);
         tc_fence_after();
         const uint32_t k_addr = kv_smem + st * 2 * C::kKTile, v_addr = k_addr + C::kKTile;
         const uint64_t kdesc = smem_desc_sw128(k_addr, 16, 1024), vdesc = smem_desc_sw128(v_addr, 16, 1024);
+        const uint32_t scol = tmem + 256u * u;
+        if (elect_one()) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if ((j == 1 && !it.has1) || t > it.tl[j]) continue;
-          const int u = sc[j] & 1;
-          if (sc[j] >= 2) mbar_wait_warp(smem_u32(&bars.s_free[j][u]), ((sc[j] - 2) >> 1) & 1);
-          ++sc[j];
-          tc_fence_after();
-          const uint32_t q_addr = q_smem + (2 * j) * C::kQTile, d_addr = q_addr + C::kQTile;
-          const uint64_t qdesc = smem_desc_sw128(q_addr, 16, 1024), ddesc = smem_desc_sw128(d_addr, 16, 1024);
-          const uint32_t sc_col = s_col(tmem, j, u);
-          if (elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint64_t ao = (uint64_t)(((kk >> 2) * C::kQSlab + (kk & 3) * 32) >> 4);
-              const uint64_t bo = (uint64_t)(((kk >> 2) * C::kKSlab + (kk & 3) * 32) >> 4);
-              mma_ss(sc_col, qdesc + ao, kdesc + bo, idesc, kk > 0 ? 1u : 0u);       // S = Q K^T
-            }
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint64_t ao = (uint64_t)(((kk >> 2) * C::kQSlab + (kk & 3) * 32) >> 4);
-              const uint64_t bo = (uint64_t)(((kk >> 2) * C::kKSlab + (kk & 3) * 32) >> 4);
-              mma_ss(sc_col + 64u, ddesc + ao, vdesc + bo, idesc, kk > 0 ? 1u : 0u);  // G = dO V^T
-            }
-            mma_commit(smem_u32(&bars.s_full[j][u]));
-            if (pass == 1 && t == it.tl[j]) mma_commit(smem_u32(&bars.q_empty[j]));  // Q_j, dO_j free
+          for (int kk = 0; kk < (MOA_INF_DIAG == 2 ? 0 : D / 16); ++kk) {
+            const uint64_t ao = (uint64_t)(((kk >> 2) * C::kQSlab + (kk & 3) * 32) >> 4);
+            const uint64_t bo = (uint64_t)(((kk >> 2) * C::kKSlab + (kk & 3) * 32) >> 4);
+            mma_ss(scol, qdesc + ao, kdesc + bo, idesc, kk > 0 ? 1u : 0u);          // S = Q K^T
           }
-          __syncwarp();
+#pragma unroll
+          for (int kk = 0; kk < (MOA_INF_DIAG == 2 ? 0 : D / 16); ++kk) {
+            const uint64_t ao = (uint64_t)(((kk >> 2) * C::kQSlab + (kk & 3) * 32) >> 4);
+            const uint64_t bo = (uint64_t)(((kk >> 2) * C::kKSlab + (kk & 3) * 32) >> 4);
+            mma_ss(scol + 128u, ddesc + ao, vdesc + bo, idesc, kk > 0 ? 1u : 0u);   // G = dO V^T
+          }
+          mma_commit(smem_u32(&bars.s_full[u]));
+          if (pass == 1 && t == it.tl) mma_commit(smem_u32(&bars.q_empty));  // Q, dO free
+          if (MOA_INF_DIAG < 4) mma_commit(smem_u32(&bars.kv_empty[st]));
         }
-        if (elect_one()) mma_commit(smem_u32(&bars.kv_empty[st]));
         __syncwarp();
-        ++kvc;
       }
     }
   }
 }
 
+// merge of the two key halves' pass-0 statistics of a row (both warps evaluate the same
+// expression on (half 0, half 1), so they hold bit-identical results): the half holding the row
+// max (first key on a tie) keeps its star, the other half's star and rest join the rest
+__device__ __forceinline__ void merge_stats(float m0, float L0, float U0, float G0, int j0, float m1, float L1,
+                                            float U1, float G1, int j1, float &m, float &Lr, float &Ur, float &Gs,
+                                            int &js) {
+  const bool take0 = j1 < 0 || (j0 >= 0 && (m0 > m1 || (m0 == m1 && j0 < j1)));
+  const float ms = take0 ? m0 : m1, mo = take0 ? m1 : m0;
+  const float Ls = take0 ? L0 : L1, Lo = take0 ? L1 : L0;
+  const float Us = take0 ? U0 : U1, Uo = take0 ? U1 : U0;
+  const float Gss = take0 ? G0 : G1, Go = take0 ? G1 : G0;
+  const int jo = take0 ? j1 : j0;
+  const float w = jo >= 0 ? fast_exp2(mo - ms) : 0.f;
+  m = ms;
+  Lr = Ls + (1.f + Lo) * w;
+  Ur = Us + (Go + Uo) * w;
+  Gs = Gss;
+  js = take0 ? j0 : j1;
+}
+
 // ---------------------------------------------------------------- elementwise (warps 0-7)
 template <int D>
 __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint32_t tmem, int warp, int lane,
-                                            float (*pair)[2][2][2]) {
-  const int j = warp >> 2, wq = warp & 3;
+                                            float (*pair)[2][kPairRound], float (*xs)[6][kIM]) {
+  const int hf = warp >> 2, wq = warp & 3;
   const int row = wq * 32 + lane;
   const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-  const int r = wq >> 1;                  // row block of this warp inside the q tile
-  const int pair_bar = 1 + 2 * j + r;     // named barrier of the two warps of a row block
+  const int r = wq >> 1;                          // query block of this warp inside the q tile
+  const int pair_bar = 1 + 2 * hf + r;            // named barrier of the two warps of a (query block, half)
+  const int half_bar = 5 + wq;                    // named barrier of the two halves of a row quarter
   int sc = 0;
+  float s[kCols], g[kCols];
   for (int idx = blockIdx.x; idx < p.total; idx += gridDim.x) {
     const IItem it = get_iitem(p, idx);
-    if (j == 1 && !it.has1) continue;
-    const int64_t ti0 = it.i0 + (int64_t)j * kIM;
+    const int64_t ti0 = it.i0;
     const int64_t i = ti0 + row;
     const bool valid = i < p.N;
-    const int tl = it.tl[j];
-    // first kv tile holding keys past some row of this warp (causal mask needed from there on)
-    const int tdiag = (int)((ti0 + wq * 32) / kIN);
-    float m = -INFINITY, Lr = 0.f, Ur = 0.f, Gs = 0.f;
+    const int tl = it.tl;
+    const int64_t wrow0 = ti0 + wq * 32;  // first row of this warp
+    // pass-0 state of this row over this warp's key half: sums relative to a lazy reference mr
+    // (log2 units; refreshed only when the max grows by more than kRefLazy), and a DESIGNATED
+    // key js (value xs, weight pj = 2^(xs - mr), G = Gs) kept out of Lr = sum_{k != js} p_k and
+    // Ur = sum_{k != js} G_k p_k
+    float mr = -INFINITY, xsv = -INFINITY, pj = 0.f, Lr = 0.f, Ur = 0.f, Gs = 0.f;
     int js = -1;
-    float s[kIN], g[kIN];
     auto load_tile = [&]() {
       const int u = sc & 1;
-      mbar_wait_warp(smem_u32(&bars.s_full[j][u]), (sc >> 1) & 1);
+      mbar_wait_warp(smem_u32(&bars.s_full[u]), (sc >> 1) & 1);
       ++sc;
       tc_fence_after();
-      const uint32_t base = s_col(tmem, j, u) + lane_off;
-      tmem_ld32(base, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      tmem_ld32(base + 32u, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-      tmem_ld32(base + 64u, *reinterpret_cast<uint32_t(*)[32]>(&g[0]));
-      tmem_ld32(base + 96u, *reinterpret_cast<uint32_t(*)[32]>(&g[32]));
-      tmem_wait_ld();
+      const uint32_t base = tmem + 256u * u + lane_off + 64u * hf;
+      if (MOA_INF_DIAG != 5) {
+        if (MOA_INF_DIAG != 7) {
+          tmem_ld32(base, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+          tmem_ld32(base + 32u, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        }
+        // wait between the S and G pairs: with all four 32-column loads in flight before one
+        // wait the step took ~1400 cycles longer (tools/build_variant.py diag 1 vs 8: 1.57 vs
+        // 0.67 ms at N = 8k with no elementwise work); two in flight cost nothing measurable
+        tmem_wait_ld();
+        if (MOA_INF_DIAG != 6) {
+          tmem_ld32(base + 128u, *reinterpret_cast<uint32_t(*)[32]>(&g[0]));
+          tmem_ld32(base + 160u, *reinterpret_cast<uint32_t(*)[32]>(&g[32]));
+        }
+        tmem_wait_ld();
+      }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&bars.s_free[j][u]));
+      if (lane == 0) mbar_arrive(smem_u32(&bars.s_free[u]));
     };
-    // ---- pass 0: row statistics
-    for (int t = 0; t <= tl; ++t) {
+    auto lane_load = [&](int t) {
       load_tile();
-      const int64_t j0 = (int64_t)t * kIN;
-      if (t >= tdiag) {  // keys past the row: never visible
+      const int64_t j0 = (int64_t)t * kIN + kCols * hf;  // first key of this warp's half
+      const bool diag = j0 + kCols - 1 > wrow0;           // keys past some row of the warp
+      if (diag) {  // keys past the row: never visible
         const int dd = (int)(i - j0);
 #pragma unroll
-        for (int c = 0; c < kIN; ++c)
+        for (int c = 0; c < kCols; ++c)
           if (c > dd) s[c] = -INFINITY;
       }
-      float mx = s[0];
+      return diag;
+    };
+    // ---- pass 0: row statistics over this warp's key half
+    for (int t = 0; t <= tl; ++t) {
+      if (MOA_INF_DIAG >= 3) continue;
+      const bool diag = lane_load(t);
+      if (MOA_INF_DIAG == 1 || MOA_INF_DIAG >= 5) continue;
+      const int64_t j0 = (int64_t)t * kIN + kCols * hf;
+      float mq[4];
 #pragma unroll
-      for (int c = 1; c < kIN; ++c) mx = fmaxf(mx, s[c]);
-      mx *= p.sl2;  // tau > 0: the max commutes with the scaling
-      const bool newmax = mx > m;
-      float rs = 0.f, us = 0.f;
-      if (__any_sync(0xffffffffu, newmax)) {
-        // the tile's star (first key attaining its max) is split off when it is the row's new max
-        int ks = kIN;
+      for (int a = 0; a < 4; ++a) mq[a] = fmaxf(s[a], s[a + 4]);
+#pragma unroll
+      for (int c = 8; c < kCols; c += 8)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) mq[a] = fmax3(mq[a], s[c + a], s[c + a + 4]);
+      const float mxr = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));  // raw max
+      const float mx = mxr * p.sl2;  // tau > 0: the max commutes with the scaling
+      // the designated key only moves when a key beats it by more than 2^kStarLazy: any key it
+      // leaves in the sums then has A <= 2^kStarLazy / (1 + 2^kStarLazy) < 1, so 1 - A stays
+      // well conditioned; for random scores this happens in the row's first tile only
+      const bool sw = mx > xsv + kStarLazy;
+      if (__any_sync(0xffffffffu, sw)) {
+        int ks = kCols;
         float gst = 0.f;
 #pragma unroll
-        for (int c = kIN - 1; c >= 0; --c) {
-          const bool hit = s[c] * p.sl2 == mx;
+        for (int c = kCols - 1; c >= 0; --c) {
+          const bool hit = s[c] == mxr;
           ks = hit ? c : ks;
           gst = hit ? g[c] : gst;
         }
-        if (!newmax) ks = kIN;  // not a new row max: every key joins the rest
-        const float mn = newmax ? mx : m;
-#pragma unroll
-        for (int c = 0; c < kIN; ++c) {
-          const float e = c == ks ? 0.f : fast_exp2(fmaf(s[c], p.sl2, -mn));
-          rs += e;
-          us = fmaf(g[c], e, us);
+        if (!sw) ks = kCols;
+        const float mn = fmaxf(mr, mx);
+        if (mn > mr) {  // new reference (the first visible tile: mr = -inf, the sums are 0)
+          const float a = mr == -INFINITY ? 0.f : fast_exp2(mr - mn);
+          Lr *= a;
+          Ur *= a;
+          pj *= a;
+          mr = mn;
         }
-        if (newmax) {
-          const float alpha = fast_exp2(m - mx);  // 0 for the first tile (m = -inf)
-          Lr = (js >= 0 ? (1.f + Lr) * alpha : 0.f) + rs;
-          Ur = (js >= 0 ? (Gs + Ur) * alpha : 0.f) + us;
-          m = mx;
-          js = (int)j0 + ks;
-          Gs = gst;
-        } else {
-          Lr += rs;
-          Ur += us;
+        if (sw) {  // the old designated key joins the rest
+          Lr += pj;
+          Ur = fmaf(Gs, pj, Ur);
         }
-      } else {
+        float rs = 0.f, us = 0.f;
+        const float nm = mr == -INFINITY ? 0.f : -mr;
 #pragma unroll
-        for (int c = 0; c < kIN; ++c) {
-          const float e = fast_exp2(fmaf(s[c], p.sl2, -m));
+        for (int c = 0; c < kCols; ++c) {
+          const float e = c == ks ? 0.f : fast_exp2(fmaf(s[c], p.sl2, nm));
           rs += e;
           us = fmaf(g[c], e, us);
         }
         Lr += rs;
         Ur += us;
+        if (sw) {
+          js = (int)j0 + ks;
+          xsv = mx;
+          pj = fast_exp2(mx - mr);
+          Gs = gst;
+        }
+      } else {
+        if (mx > mr + kRefLazy) {  // lazy reference refresh (rare)
+          const float a = fast_exp2(mr - mx);
+          Lr *= a;
+          Ur *= a;
+          pj *= a;
+          mr = mx;
+        }
+        // packed f32x2 arithmetic, four independent sums, one exponential pair in kPolyEvery
+        // on the FMA pipe -- except in diagonal tiles: masked keys must add exactly 0 (MUFU
+        // ex2(-inf) = 0; the polynomial bottoms out at 2^-126, and on a row with one visible
+        // key any nonzero rest would turn its E from 0 into noise).  mr = -inf: this half has
+        // seen no key of the row yet and the tile is all masked (the offset stays finite).
+        const float nm = mr == -INFINITY ? 0.f : -mr;
+        const uint64_t sl2 = f2pk(p.sl2, p.sl2), nm2 = f2pk(nm, nm);
+        uint64_t r2[2] = {0ull, 0ull}, u2[2] = {0ull, 0ull};
+        auto sweep = [&](auto poly) {
+#pragma unroll
+          for (int c = 0; c < kCols; c += 2) {
+            float ya, yb, ea, eb;
+            f2upk(ffma2(f2pk(s[c], s[c + 1]), sl2, nm2), ya, yb);
+            if (decltype(poly)::value && (c >> 1) % kPolyEvery == kPolyEvery - 1) {
+              exp2_poly2(ya, yb, ea, eb);
+            } else {
+              ea = fast_exp2(ya);
+              eb = fast_exp2(yb);
+            }
+            const uint64_t e2 = f2pk(ea, eb);
+            r2[(c >> 1) & 1] = fadd2(r2[(c >> 1) & 1], e2);
+            u2[(c >> 1) & 1] = ffma2(f2pk(g[c], g[c + 1]), e2, u2[(c >> 1) & 1]);
+          }
+        };
+        if (diag)
+          sweep(std::false_type{});
+        else
+          sweep(std::true_type{});
+        float a0, a1, b0, b1;
+        f2upk(fadd2(r2[0], r2[1]), a0, a1);
+        f2upk(fadd2(u2[0], u2[1]), b0, b1);
+        Lr += a0 + a1;
+        Ur += b0 + b1;
       }
     }
-    const float l = 1.f + Lr, inv_l = 1.f / l, C1 = Gs + Ur;
-    const float Estar = Lr > 0.f ? (Ur - Gs * Lr) / (Lr * l) : 0.f;  // a row with one visible key: 0
-    const int64_t ib = ti0 / kIN + r;
-    const int64_t rows_real = p.N - ib * kIN < kIN ? p.N - ib * kIN : kIN;
+    // ---- merge the two halves' statistics (once per item): common reference, the larger
+    // designated key stays designated (first key on a tie), the other one joins the rest.  Both
+    // warps evaluate the same expression on (half 0, half 1): bit-identical results.
+    if (MOA_INF_DIAG != 1 && MOA_INF_DIAG < 3) {
+      xs[hf][0][row] = mr;
+      xs[hf][1][row] = pj;
+      xs[hf][2][row] = Lr;
+      xs[hf][3][row] = Ur;
+      xs[hf][4][row] = Gs;
+      xs[hf][5][row] = __int_as_float(js);
+      asm volatile("bar.sync %0, 64;" ::"r"(half_bar) : "memory");
+      const float mr0 = xs[0][0][row], mr1 = xs[1][0][row];
+      const int j0s = __float_as_int(xs[0][5][row]), j1s = __float_as_int(xs[1][5][row]);
+      const float mm = fmaxf(mr0, mr1);
+      const float w0 = mr0 == -INFINITY ? 0.f : fast_exp2(mr0 - mm), w1 = mr1 == -INFINITY ? 0.f : fast_exp2(mr1 - mm);
+      const float p0 = xs[0][1][row] * w0, p1 = xs[1][1][row] * w1;
+      const bool take0 = j1s < 0 || (j0s >= 0 && (p0 > p1 || (p0 == p1 && j0s < j1s)));
+      const float L0 = xs[0][2][row] * w0, L1 = xs[1][2][row] * w1;
+      const float U0 = xs[0][3][row] * w0, U1 = xs[1][3][row] * w1;
+      const float G0 = xs[0][4][row], G1 = xs[1][4][row];
+      mr = mm;
+      pj = take0 ? p0 : p1;
+      Gs = take0 ? G0 : G1;
+      js = take0 ? j0s : j1s;
+      Lr = (L0 + L1) + (take0 ? p1 : p0);
+      Ur = (U0 + U1) + (take0 ? G1 * p1 : G0 * p0);
+      asm volatile("bar.sync %0, 64;" ::"r"(half_bar) : "memory");  // both read before the next item's write
+    }
+    const float m = mr;
+    // l = sum of all p; C1 = R l; the designated key: E = pj (Ur - Gs Lr) / (l Lr) (0 for a
+    // row with one visible key)
+    const float l = pj + Lr, inv_l = 1.f / l, C1 = fmaf(pj, Gs, Ur);
+    const float Estar = Lr > 0.f ? pj * (Ur - Gs * Lr) / (Lr * l) : 0.f;
+    const int64_t ib = ti0 / kCols + r;
+    const int64_t rows_real = p.N - ib * kCols < kCols ? p.N - ib * kCols : kCols;
     float *orow = p.out + (((int64_t)it.b * p.nql + it.h) * p.nb + ib) * p.nb;
     // ---- pass 1: E, summed to block means
     for (int t = 0; t <= tl; ++t) {
+      if (MOA_INF_DIAG >= 3) continue;
       load_tile();
-      const int64_t j0 = (int64_t)t * kIN;
-      const int kst = js - (int)j0;  // the star's column (outside [0, 64) if not in this tile)
+      const int64_t j0 = (int64_t)t * kIN + kCols * hf;
+      const bool diag = j0 + kCols - 1 > wrow0;
+      const int jb = 2 * t + hf;  // key block
+      const int kst = js - (int)j0;  // the star's column (outside [0, 64) if not in this half)
       float acc = 0.f;
-      if (t >= tdiag) {
-        const int dd = (int)(i - j0);
+      const bool star_here = kst >= 0 && kst < kCols;
+      if (MOA_INF_DIAG == 1 || MOA_INF_DIAG >= 5) {
+        acc = s[lane] + g[lane];
+      } else if (diag || __any_sync(0xffffffffu, star_here)) {
+        // diagonal tiles (causal mask) and tiles holding some row's star (split off)
+        const int dd = diag ? (int)(i - j0) : kCols;
 #pragma unroll
-        for (int c = 0; c < kIN; ++c) {
+        for (int c = 0; c < kCols; ++c) {
           const float pe = c > dd ? 0.f : fast_exp2(fmaf(s[c], p.sl2, -m));
           const float e = __fdividef(pe * fmaf(-g[c], l, C1), l - pe);
           acc += (c == kst || c > dd) ? 0.f : e;
         }
       } else {
+        // E = p (C1 - G l) / (l - p) on packed pairs; one exponential pair in kPolyEvery on
+        // the FMA pipe, the reciprocals on MUFU
+        const uint64_t sl2 = f2pk(p.sl2, p.sl2), nm2 = f2pk(-m, -m), nl2 = f2pk(-l, -l), l2 = f2pk(l, l),
+                       c12 = f2pk(C1, C1), m12 = f2pk(-1.f, -1.f);
+        uint64_t a2[2] = {0ull, 0ull};
 #pragma unroll
-        for (int c = 0; c < kIN; ++c) {
-          const float pe = fast_exp2(fmaf(s[c], p.sl2, -m));
-          const float e = __fdividef(pe * fmaf(-g[c], l, C1), l - pe);
-          acc += c == kst ? 0.f : e;
+        for (int c = 0; c < kCols; c += 2) {
+          float ya, yb, ea, eb;
+          f2upk(ffma2(f2pk(s[c], s[c + 1]), sl2, nm2), ya, yb);
+          if ((c >> 1) % kPolyEvery == kPolyEvery - 1) {
+            exp2_poly2(ya, yb, ea, eb);
+          } else {
+            ea = fast_exp2(ya);
+            eb = fast_exp2(yb);
+          }
+          const uint64_t p2 = f2pk(ea, eb);
+          float da, db;
+          f2upk(ffma2(p2, m12, l2), da, db);  // l - p (>= 1 off the star)
+          const uint64_t q2 = fmul2(p2, ffma2(f2pk(g[c], g[c + 1]), nl2, c12));
+          a2[(c >> 1) & 1] = ffma2(q2, f2pk(fast_rcp(da), fast_rcp(db)), a2[(c >> 1) & 1]);
         }
+        float a0, a1;
+        f2upk(fadd2(a2[0], a2[1]), a0, a1);
+        acc = a0 + a1;
       }
-      acc = acc * inv_l + ((kst >= 0 && kst < kIN) ? Estar : 0.f);
+      acc = acc * inv_l + (star_here ? Estar : 0.f);
       if (!valid) acc = 0.f;
 #pragma unroll
       for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      // the two warps of the row block: fixed-order sum (deterministic), one store per block
-      if (lane == 0) pair[j][r][t & 1][wq & 1] = acc;
-      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-      if ((wq & 1) == 0 && lane == 0 && t <= ib && rows_real > 0) {
-        const float tot = pair[j][r][t & 1][0] + pair[j][r][t & 1][1];
-        const int64_t cols_real = p.N - j0 < kIN ? p.N - j0 : kIN;
-        const float mean = tot / (float)(rows_real * cols_real);
-        orow[t] = p.accumulate ? orow[t] + mean : mean;
+      // the two warps of a query block park their sums per tile (double-buffered rounds of
+      // kPairRound tiles) and meet once per round: fixed-order sum (deterministic), one store per block
+      if (lane == 0) pair[warp][(t / kPairRound) & 1][t % kPairRound] = acc;
+      if (t % kPairRound == kPairRound - 1 || t == tl) {
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        if ((wq & 1) == 0 && rows_real > 0) {
+          const int t0 = t - t % kPairRound;
+          for (int tt = t0 + lane; tt <= t; tt += 32) {
+            const int jbt = 2 * tt + hf;
+            if (jbt > ib) continue;  // no causal pairs above the diagonal
+            const int sl = tt % kPairRound, bu = (tt / kPairRound) & 1;
+            const float tot = pair[warp][bu][sl] + pair[warp + 1][bu][sl];
+            const int64_t jt = (int64_t)jbt * kCols;
+            const int64_t cols_real = p.N - jt < kCols ? p.N - jt : kCols;
+            const float mean = tot / (float)(rows_real * cols_real);
+            orow[jbt] = p.accumulate ? orow[jbt] + mean : mean;
+          }
+        }
       }
+      (void)jb;
     }
-    // blocks above the diagonal have no causal pairs
-    if (!p.accumulate && (wq & 1) == 0 && rows_real > 0)
-      for (int64_t jb = ib + 1 + lane; jb < p.nb; jb += 32) orow[jb] = 0.f;
+    // blocks above the diagonal have no causal pairs (both halves' blocks, written by half 0)
+    if (!p.accumulate && hf == 0 && (wq & 1) == 0 && rows_real > 0)
+      for (int64_t b2 = ib + 1 + lane; b2 < p.nb; b2 += 32) orow[b2] = 0.f;
   }
 }
 
@@ -311,23 +462,22 @@ __global__ void __launch_bounds__(kIThreads, 1)
   using C = ICfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ IBars bars;
-  __shared__ float pair[2][2][2][2];  // [tile][row block][kv tile parity][warp of the pair]
+  __shared__ float pair[8][2][kPairRound];  // [warp][round parity][tile in round] query-block row sums
+  __shared__ float xs[2][6][kIM];           // [half][mr, pj, Lr, Ur, Gs, js][row] pass-0 statistics exchange
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t smem_base = smem_u32(smem_raw);
   if (smem_base & 1023u) __trap();
-  const uint32_t q_smem = smem_base;                  // Q0, dO0, Q1, dO1
-  const uint32_t kv_smem = q_smem + 4 * C::kQTile;    // stages of (K, V)
+  const uint32_t q_smem = smem_base;                  // Q, dO
+  const uint32_t kv_smem = q_smem + 2 * C::kQTile;    // stages of (K, V)
 
   if (tid == 0) {
-    for (int j = 0; j < 2; ++j) {
-      mbar_init(smem_u32(&bars.q_full[j]), 1);
-      mbar_init(smem_u32(&bars.q_empty[j]), 1);
-      for (int u = 0; u < 2; ++u) {
-        mbar_init(smem_u32(&bars.s_full[j][u]), 1);
-        mbar_init(smem_u32(&bars.s_free[j][u]), 4);  // the tile's 4 elementwise warps
-      }
+    mbar_init(smem_u32(&bars.q_full), 1);
+    mbar_init(smem_u32(&bars.q_empty), 1);
+    for (int u = 0; u < 2; ++u) {
+      mbar_init(smem_u32(&bars.s_full[u]), 1);
+      mbar_init(smem_u32(&bars.s_free[u]), 8);  // the 8 elementwise warps
     }
-    for (int s = 0; s < kKVStages; ++s) {
+    for (int s = 0; s < C::kStages; ++s) {
       mbar_init(smem_u32(&bars.kv_full[s]), 1);
       mbar_init(smem_u32(&bars.kv_empty[s]), 1);
     }
@@ -346,32 +496,27 @@ __global__ void __launch_bounds__(kIThreads, 1)
   const uint32_t tmem = bars.tmem_base;
 
   if (warp < 8) {
-    inf_ew_role<D>(p, bars, tmem, warp, lane, pair);
+    inf_ew_role<D>(p, bars, tmem, warp, lane, pair, xs);
   } else if (warp == kWTma) {
     if (lane == 0) {
-      int qc[2] = {0, 0}, kvc = 0;
+      int qc = 0, kvc = 0;
       for (int idx = blockIdx.x; idx < p.total; idx += gridDim.x) {
         const IItem it = get_iitem(p, idx);
         const int g = it.h / p.G;
-        for (int j = 0; j < 2; ++j) {
-          if (j == 1 && !it.has1) continue;
-          if (qc[j] > 0) mbar_wait(smem_u32(&bars.q_empty[j]), (qc[j] - 1) & 1);
-          ++qc[j];
-          const uint32_t qbar = smem_u32(&bars.q_full[j]);
-          const uint32_t q_addr = q_smem + (2 * j) * C::kQTile;
-          mbar_expect_tx(qbar, 2 * C::kQTile);
-          for (int sl = 0; sl < C::kSlabs; ++sl) {
-            tma_load_4d(q_addr + sl * C::kQSlab, &tm_q, qbar, sl * 64, it.h, (int)(it.i0 + j * kIM), it.b);
-            tma_load_4d(q_addr + C::kQTile + sl * C::kQSlab, &tm_do, qbar, sl * 64, it.h, (int)(it.i0 + j * kIM),
-                        it.b);
-          }
+        if (qc > 0) mbar_wait_sleep(smem_u32(&bars.q_empty), (qc - 1) & 1, 128);
+        ++qc;
+        const uint32_t qbar = smem_u32(&bars.q_full);
+        mbar_expect_tx(qbar, 2 * C::kQTile);
+        for (int sl = 0; sl < C::kSlabs; ++sl) {
+          tma_load_4d(q_smem + sl * C::kQSlab, &tm_q, qbar, sl * 64, it.h, (int)it.i0, it.b);
+          tma_load_4d(q_smem + C::kQTile + sl * C::kQSlab, &tm_do, qbar, sl * 64, it.h, (int)it.i0, it.b);
         }
-        const int nt = 1 + (it.has1 ? it.tl[1] : it.tl[0]);
         for (int pass = 0; pass < 2; ++pass)
-          for (int t = 0; t < nt; ++t) {
-            const int st = kvc % kKVStages;
-            if (kvc >= kKVStages) mbar_wait(smem_u32(&bars.kv_empty[st]), ((kvc - kKVStages) / kKVStages) & 1);
-            ++kvc;
+          for (int t = 0; t <= it.tl; ++t, ++kvc) {
+            if (MOA_INF_DIAG >= 4 && kvc >= C::kStages) continue;
+            const int st = kvc % C::kStages;
+            if (kvc >= C::kStages)
+              mbar_wait_sleep(smem_u32(&bars.kv_empty[st]), ((kvc - C::kStages) / C::kStages) & 1, 64);
             const uint32_t kbar = smem_u32(&bars.kv_full[st]);
             const uint32_t k_addr = kv_smem + st * 2 * C::kKTile;
             mbar_expect_tx(kbar, 2 * C::kKTile);
@@ -410,9 +555,9 @@ int launch_tc(const InfluenceArgs &a, void *stream) {
   p.batch = a.batch;
   p.nql = a.nql;
   p.G = a.G;
-  p.nqb = (int)((a.N + 2 * kIM - 1) / (2 * kIM));
-  p.nb = (int)((a.N + kIN - 1) / kIN);
-  p.total = p.nqb * a.batch * a.nql;
+  p.nqt = (int)((a.N + kIM - 1) / kIM);
+  p.nb = (int)((a.N + kCols - 1) / kCols);
+  p.total = p.nqt * a.batch * a.nql;
   p.accumulate = a.accumulate;
   p.sl2 = a.scale * kLog2e;
   cudaError_t e = cudaFuncSetAttribute(influence_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,

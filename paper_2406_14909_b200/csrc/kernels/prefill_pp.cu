@@ -189,50 +189,6 @@ __device__ __forceinline__ void step_use(const BlockTiles &bt, int k, int &t, bo
   u1 = bt.has1 && tile_in(bt.r[1], t);
 }
 
-// ---------------------------------------------------------------- packed f32x2 arithmetic
-__device__ __forceinline__ uint64_t f2pk(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void f2upk(uint64_t r, float &a, float &b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-
-// 2^y for a pair on the FMA/ALU pipes: y = n + f, n = round(y), |f| <= 1/2, 2^f by a
-// degree-3 polynomial (relative error 7.7e-5, far below bf16's 3.9e-3), 2^n added to the
-// exponent field.  y is clamped at -126 (masked scores give ~1e-38, negligible).
-__device__ __forceinline__ void exp2_poly2(float ya, float yb, float &ra, float &rb) {
-  const uint64_t y = f2pk(fmaxf(ya, -126.f), fmaxf(yb, -126.f));
-  const uint64_t t = fadd2(y, f2pk(12582912.f, 12582912.f));   // 1.5 * 2^23: round to integer
-  const uint64_t n = fadd2(t, f2pk(-12582912.f, -12582912.f));
-  const uint64_t f = ffma2(n, f2pk(-1.f, -1.f), y);               // y - n, exact
-  uint64_t q = ffma2(f, f2pk(0.05508868380750935f, 0.05508868380750935f),
-                     f2pk(0.2426040514594784f, 0.2426040514594784f));
-  q = ffma2(q, f, f2pk(0.6932762416819616f, 0.6932762416819616f));
-  q = ffma2(q, f, f2pk(0.9999289403695111f, 0.9999289403695111f));
-  float qa, qb, ta, tb;
-  f2upk(q, qa, qb);
-  f2upk(t, ta, tb);
-  ra = __int_as_float(__float_as_int(qa) + (__float_as_int(ta) << 23));
-  rb = __int_as_float(__float_as_int(qb) + (__float_as_int(tb) << 23));
-}
-
 __device__ __forceinline__ void tmem_ld32_f(uint32_t taddr, float *x) {
   tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(x));
 }
