@@ -136,31 +136,111 @@ def algorithmic_work(windows, B, N, T, s, d, G):
 
 
 # --------------------------------------------------------------------------------------------
-def cpu_oracle_decode_rate(seconds: float = 12.0):
-    """Oracle (fp64 numpy, single process) decode of layer 0, sequence 0, all 32 heads, for
-    consecutive positions p = N, N+1, ... until `seconds` elapse; returns tokens/s extrapolated to
-    the whole C2 decode workload (32 layers x 8 sequences) and a description."""
+# Oracle CPU baseline on all host cores (SURVEY §8(d) "Oracle timing"): one process per core,
+# each timing oracle.decode / oracle.prefill_rows on rows drawn uniformly at random over
+# (layer, q-head, position) of the C2 workload until a shared deadline; the rates are
+# extrapolated to the whole workload by the in-window work (decode: visible keys
+# min(p+1, s+W_h) per row; prefill: sum |V(h,i)|, oracle.visible_pairs).  The oracle's cost
+# does not depend on the values, so one seeded K/V history serves every sampled layer.
+_ORC = {}
+
+
+def _orc_init():
+    try:
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def _orc_work(args):
+    """One worker: rows (l, h, i) from its own seeded stream until the deadline."""
     import oracle
 
-    W = oracle_windows_all_layers()[0]
-    d, s, N = CFG.head_dim, CFG.n_sink, CFG.N
+    kind, wid, deadline = args
+    o = _ORC
+    rng = np.random.default_rng(1000 + wid)
+    L, Hq, N, T, s, tau = o["L"], o["Hq"], o["N"], o["T"], o["s"], o["tau"]
+    K, V, Qp, qd = o["K"], o["V"], o["Q"], o["q"]
+    rows = keys = 0
+    while time.perf_counter() < deadline:
+        l, h = int(rng.integers(L)), int(rng.integers(Hq))
+        W = o["W"][l][h]
+        if kind == "decode":
+            n = int(rng.integers(T))
+            p = N + n
+            oracle.decode(qd[n][:, h:h + 1], K[:, :p + 1, h:h + 1], V[:, :p + 1, h:h + 1], p, [W], s, tau)
+            keys += min(p + 1, s + W)
+        else:
+            i = int(rng.integers(N))
+            oracle.prefill_rows(Qp[:, :, h:h + 1], K[:, :N, h:h + 1], V[:, :N, h:h + 1], [W], s, tau, [(0, 0, i)])
+            keys += len(oracle.visible_keys(i, W, s))
+        rows += 1
+    return rows, keys
+
+
+def cpu_oracle_baseline(seconds: float = 8.0, cores=None, full=True):
+    """Decode and prefill tokens/s of the fp64 oracle on `cores` processes (default: all),
+    `seconds` of wall time per phase, plus C1 run in full (`full=False`: decode only, no C1).
+    Returns (decode tokens/s, block)."""
+    import multiprocessing as mp
+
+    import oracle
+
+    cores = cores or os.cpu_count() or 1
+    L, Hq, N, T, d, s = CFG.layers, CFG.hq, CFG.N, CFG.decode_steps, CFG.head_dim, CFG.n_sink
+    W = oracle_windows_all_layers()
     g = torch.Generator().manual_seed(7)
-    hist = N + 64
-    K = torch.randn(1, hist, CFG.hkv, d, generator=g).to(torch.bfloat16).double().numpy()
-    V = torch.randn(1, hist, CFG.hkv, d, generator=g).to(torch.bfloat16).double().numpy()
-    q = torch.randn(64, 1, CFG.hq, d, generator=g).to(torch.bfloat16).double().numpy()
+    f64 = lambda *shape: torch.randn(*shape, generator=g).to(torch.bfloat16).double().numpy()  # noqa: E731
+    _ORC.update(L=L, Hq=Hq, N=N, T=T, s=s, tau=1 / math.sqrt(d), W=W,
+                K=f64(1, N + T, CFG.hkv, d), V=f64(1, N + T, CFG.hkv, d), Q=f64(1, N, Hq, d), q=f64(T, 1, Hq, d))
+    out = {}
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_orc_init) as pool:
+        for kind in (("decode", "prefill") if full else ("decode",)):
+            t0 = time.perf_counter()
+            res = pool.map(_orc_work, [(kind, w, t0 + seconds) for w in range(cores)])
+            wall = time.perf_counter() - t0
+            rows, keys = sum(r for r, _ in res), sum(k for _, k in res)
+            out[kind] = (rows, keys, wall)
+    # workload totals: decode keys per token step (all layers, heads, T positions averaged), prefill pairs
+    dec_keys = sum(min(N + n + 1, s + W[l][h]) for l in range(L) for h in range(Hq) for n in range(T)) / T
+    pre_pairs = sum(oracle.visible_pairs(N, W[l][h], s) for l in range(L) for h in range(Hq))
+    rows, keys, wall = out["decode"]
+    dec_tps = (keys / wall) / dec_keys            # tokens/s: one token of one sequence = dec_keys keys
+    if not full:
+        return dec_tps, {"kind": "oracle", "cores": cores, "value": dec_tps, "unit": "tokens/s",
+                         "sample": f"fp64 oracle.decode on {cores} processes x {seconds:.1f} s, {rows} rows "
+                                   f"drawn uniformly over the C2 workload's (layer, q-head, position), "
+                                   f"{keys} visible keys, extrapolated by visible keys ({dec_keys:.0f} per token)"}
+    rows_p, keys_p, wall_p = out["prefill"]
+    pre_tps = N * (keys_p / wall_p) / pre_pairs    # N tokens of one sequence = pre_pairs pairs
+    # C1 (BASELINE configs[0]) in full, one process: prefill + 64 decode steps
+    from moa_workloads import prefill_qkv as pq
+    c1 = CONFIGS["C1"]
+    qh, kh, vh = (x.double().numpy() for x in pq(c1, 0))
+    qd1, kd1, vd1 = (x.double().numpy() for x in decode_tokens(c1, 0, c1.decode_steps))
     t0 = time.perf_counter()
-    n = 0
-    while time.perf_counter() - t0 < seconds and n < 64:
-        oracle.decode(q[n], K[:, : N + n + 1], V[:, : N + n + 1], N + n, W, s, 1 / math.sqrt(d))
-        n += 1
-    dt = (time.perf_counter() - t0) / n  # seconds per (layer, sequence, token)
-    per_token_all = dt * CFG.layers * CFG.batch
-    rate = CFG.batch / per_token_all
-    return rate, {"kind": "oracle", "cores": 1,
-                  "sample": f"oracle.decode (fp64 numpy, 1 process) of layer 0, sequence 0, all {CFG.hq} heads, "
-                            f"{n} positions from p=N={N}; {dt*1e3:.1f} ms per (layer, sequence, token), "
-                            f"extrapolated to {CFG.layers} layers x {CFG.batch} sequences"}
+    oracle.prefill(qh, kh, vh, list(c1.windows), c1.n_sink, 1 / math.sqrt(c1.head_dim))
+    t1 = time.perf_counter()
+    Kh = np.concatenate([kh, kd1.transpose(1, 0, 2, 3)], 1)
+    Vh = np.concatenate([vh, vd1.transpose(1, 0, 2, 3)], 1)
+    for n in range(c1.decode_steps):
+        oracle.decode(qd1[n], Kh, Vh, c1.N + n, list(c1.windows), c1.n_sink, 1 / math.sqrt(c1.head_dim))
+    t2 = time.perf_counter()
+    block = {
+        "kind": "oracle", "cores": cores, "value": dec_tps, "unit": "tokens/s",
+        "sample": (f"fp64 oracle (oracle.decode / oracle.prefill_rows) on {cores} processes x {seconds:.0f} s per "
+                   f"phase, rows drawn uniformly over the C2 workload's (layer, q-head, position): decode "
+                   f"{rows} rows / {keys} visible keys, prefill {rows_p} rows / {keys_p} visible pairs; "
+                   f"extrapolated by in-window work (decode {dec_keys:.0f} keys per token step of one sequence, "
+                   f"prefill {pre_pairs} pairs per sequence)"),
+        "decode_tokens_per_s": dec_tps, "prefill_tokens_per_s": pre_tps,
+        "prefill_extrapolation": "sum |V(h,i)| (oracle.visible_pairs)",
+        "C1_full": {"prefill_s": t1 - t0, "decode_s": t2 - t1, "prefill_tokens_per_s": c1.N / (t1 - t0),
+                    "decode_tokens_per_s": c1.decode_steps / (t2 - t1), "cores": 1,
+                    "note": "C1 (configs[0]) run in full: prefill N=256 + 64 decode steps, 1 process"}}
+    return dec_tps, block
 
 
 # --------------------------------------------------------------------------------------------
@@ -170,20 +250,22 @@ def run_reference(args, rank, world):
         return
     rates = []
     for _ in range(args.warmup):
-        cpu_oracle_decode_rate(seconds=2.0)
+        cpu_oracle_baseline(seconds=1.0, full=False)
     t0 = time.perf_counter()
-    desc = None
     for _ in range(args.steps):
-        r, desc = cpu_oracle_decode_rate(seconds=8.0)
+        r, _ = cpu_oracle_baseline(seconds=3.0, full=False)
         rates.append(r)
     wall = time.perf_counter() - t0
     value = float(statistics.median(rates))
+    _, desc = cpu_oracle_baseline(seconds=6.0)   # prefill + C1 context, once, after the timed steps
+    desc["value"] = value
+    desc["sample"] = f"timed steps: decode, {args.steps} x 3 s on {desc['cores']} processes; " + desc["sample"]
     line = {
         "impl": "reference", "metric": "decode tokens/s", "value": value, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(world),
-        "cpu_baseline": dict(desc, value=value, unit="tokens/s"),
+        "cpu_baseline": desc,
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -200,6 +282,11 @@ def config_block(world):
 # --------------------------------------------------------------------------------------------
 def run_ours(args, rank, world, local_rank):
     import paper_2406_14909_b200 as moa
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # before any CUDA work: the worker processes are forked from this one
+        _, cpu = cpu_oracle_baseline()
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -297,20 +384,20 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- e2e: host buffers through the public API, H2D/D2H inside the timed region
     e2e = run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev)
+    del Q, K, V, O
+    ctx = ws = None
+    torch.cuda.empty_cache()
     kv_shard = None
     if world > 1 or args.kv_shard:
-        del Q, K, V, O
-        ctx = None
-        torch.cuda.empty_cache()
         try:
             kv_shard = run_kv_shard(rank, world, dev, scale)
         except Exception as exc:  # reported, never fatal for the main line
             kv_shard = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        torch.cuda.empty_cache()
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, desc = cpu_oracle_decode_rate()
-        cpu = dict(desc, value=rate, unit="tokens/s")
+    configs = None
+    if world == 1 and not args.no_configs:
+        configs = run_configs(dev, peaks)
 
     if rank == 0:
         line = {
@@ -343,6 +430,8 @@ def run_ours(args, rank, world, local_rank):
         }
         if kv_shard is not None:
             line["kv_shard"] = kv_shard
+        if configs is not None:
+            line["configs"] = configs
         print(json.dumps(line), flush=True)
 
 
@@ -420,6 +509,130 @@ def run_kv_shard(rank, world, dev, scale, T=64):
             "tokens": T, "scaling": "strong",
             "note": "NCCL all_gather_into_tensor of each layer's head outputs (torch.distributed, own stream, "
                     "preallocated), serialised before the next layer; device-timed, max over ranks"}
+
+
+def _config_windows(moa, cfg, l):
+    t = rule_table(cfg.name)
+    return moa.resolve_spans(t["alpha"][l], t["beta"][l], cfg.N, cfg.n_sink)
+
+
+def _bench_decode_cfg(moa, cfg, layers, T, dev, peaks):
+    """Fused decode over `layers` (all resident) for T tokens; CUDA events around the phase."""
+    L_all, B, N, s, d, G = cfg.layers, cfg.batch, cfg.N, cfg.n_sink, cfg.head_dim, cfg.group
+    wins = {l: _config_windows(moa, cfg, l) for l in range(L_all)}
+    ctx = moa.MoAContext(len(layers), cfg.hq, cfg.hkv, d, B, dtype=torch.bfloat16, device=dev.index)
+    for i, l in enumerate(layers):
+        ctx.set_spans(i, wins[l], s, N)
+    ctx.alloc_cache(B)
+    ws = ctx.alloc_workspace(B)
+    g = torch.Generator(device=dev).manual_seed(cfg.seed_base + 7)
+    kp = torch.randn(B, N, cfg.hkv, d, device=dev, generator=g).to(torch.bfloat16)
+    vp = torch.randn(B, N, cfg.hkv, d, device=dev, generator=g).to(torch.bfloat16)
+    qd, kd, vd = decode_tokens(cfg, 0, T, device=dev)
+    od = torch.empty(B, cfg.hq, d, dtype=torch.bfloat16, device=dev)
+    scale = 1 / math.sqrt(d)
+
+    def layer_bytes(l, p):   # in-window bytes of one layer-token (SURVEY §8(a7)) + q/o + new token
+        wg = [max(wins[l][x * G:(x + 1) * G]) for x in range(cfg.hkv)]
+        return B * (sum(min(p + 1, s + w) for w in wg) * d * 4 + cfg.hq * d * 4 + cfg.hkv * d * 8)
+
+    def run():
+        for i in range(len(layers)):
+            ctx.cache_fill(i, kp, vp)  # positions restart at N
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for t in range(T):
+            for i in range(len(layers)):
+                ctx.decode_step_fused(i, qd[t], kd[t], vd[t], od, N + t, scale, ws)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 1e3
+
+    run()
+    with ClockSampler(dev.index) as clk:
+        sec = statistics.median(run() for _ in range(3))
+    by_timed = sum(layer_bytes(l, N + t) for t in range(T) for l in layers)
+    by_all = sum(layer_bytes(l, N + t) for t in range(T) for l in range(L_all))
+    gbs = by_timed / sec / 1e9
+    sec_model = by_all / (gbs * 1e9)          # all L layers at the measured in-window rate
+    out = {"tokens_per_s": B * T / sec_model, "unit": "tokens/s", "batch": B, "tokens": T,
+           "positions": [N, N + T - 1], "layers_timed": len(layers), "layers_model": L_all,
+           "us_per_layer_token": sec / (T * len(layers)) * 1e6,
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                        "bytes_per_launch": by_timed / (T * len(layers))},
+           "clocks": clk.summary()}
+    if len(layers) < L_all:
+        out["sampling"] = (f"{len(layers)} of {L_all} layers resident (every {layers[1] - layers[0]}th, "
+                           f"{layers[0]}..{layers[-1]}: the whole density profile, not its densest end); "
+                           f"tokens/s = B*T / (in-window bytes of all {L_all} layers / the measured GB/s)")
+    del ctx, ws, kp, vp
+    torch.cuda.empty_cache()
+    return out
+
+
+def _bench_prefill_cfg(moa, cfg, dev, peaks):
+    """moa_prefill_attn + moa_cache_fill over every layer; per-layer events on the attention."""
+    L, B, N, s, d = cfg.layers, cfg.batch, cfg.N, cfg.n_sink, cfg.head_dim
+    wins = [_config_windows(moa, cfg, l) for l in range(L)]
+    ctx = moa.MoAContext(L, cfg.hq, cfg.hkv, d, B, dtype=torch.bfloat16, device=dev.index)
+    for l in range(L):
+        ctx.set_spans(l, wins[l], s, N)
+    ctx.alloc_cache(B)
+    qkv = [prefill_qkv(cfg, l, device=dev) for l in range(L)]
+    o = torch.empty_like(qkv[0][0])
+    scale = 1 / math.sqrt(d)
+    flops, _ = algorithmic_work(wins, B, N, 0, s, d, cfg.group)
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+
+    def run():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for l in range(L):
+            ev[l][0].record(stream)
+            ctx.prefill_attn(l, *qkv[l], o, scale)
+            ev[l][1].record(stream)
+            ctx.cache_fill(l, qkv[l][1], qkv[l][2])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 1e3, sum(a.elapsed_time(b) for a, b in ev) / 1e3
+
+    run()
+    with ClockSampler(dev.index) as clk:
+        res = [run() for _ in range(3)]
+    tot = statistics.median(r[0] for r in res)
+    attn = statistics.median(r[1] for r in res)
+    tf = flops / attn / 1e12
+    pk = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    out = {"tokens_per_s": B * N / tot, "unit": "tokens/s", "batch": B, "N": N, "layers": L,
+           "ms_all_layers": tot * 1e3, "attn_ms_all_layers": attn * 1e3,
+           "roofline": {"bound": "tensor", "achieved": tf, "peak": pk, "unit": "TFLOP/s", "frac": tf / pk,
+                        "frac_of_burst": tf / peaks["bf16_tflops"], "traffic": None,
+                        "note": "in-window FLOPs 4*d*sum|V| over the event-timed attention launches; "
+                                "tokens/s includes the cache fill"},
+           "clocks": clk.summary()}
+    del ctx, qkv, o
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_configs(dev, peaks):
+    """BASELINE.json configs[2..4] on this GPU, as sub-blocks of the one JSON line:
+    C3 GQA decode (all 32 layers, 64 tokens), C4 prefill (all 40 layers), C5 decode (16 of 80
+    layers resident, strided over the density profile, 16 tokens; its 172 GB cache does not fit)."""
+    import paper_2406_14909_b200 as moa
+    out = {}
+    for name, fn in (("C3", lambda c: _bench_decode_cfg(moa, c, list(range(c.layers)), 64, dev, peaks)),
+                     ("C4", lambda c: _bench_prefill_cfg(moa, c, dev, peaks)),
+                     ("C5", lambda c: _bench_decode_cfg(moa, c, list(range(0, c.layers, 5)), 16, dev, peaks))):
+        try:
+            out[name] = dict(mode="prefill" if name == "C4" else "decode", **fn(CONFIGS[name]))
+        except Exception as exc:  # reported, never fatal for the main line
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
@@ -514,6 +727,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C3/C4/C5 sub-blocks")
     ap.add_argument("--kv-shard", action="store_true", help="also run the kv-group sharded decode at N = 1")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
