@@ -5,7 +5,10 @@ One step = one pass of the whole hot path over one batch of the C2 workload
 (configs[1], Vicuna-7B attention shape): span resolution is done once at
 setup; the timed step is the prefill of all 32 layers (tcgen05 kernel + cache
 fill, N = 4096, B = 8) followed by 512 decode tokens x 32 layers (fused
-append + split-KV decode + combine, one launch per layer-token).
+append + split-KV decode + combine; one cross-layer launch per token,
+moa_decode_step_fused_layers).  "decode_per_layer" reports the same decode with
+one launch per layer-token (the order a model needs when layer l+1's query
+depends on layer l's output).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -297,7 +300,8 @@ def run_ours(args, rank, world, local_rank):
     for l in range(L):
         ctx.set_spans(l, windows[l], s, N)
     ctx.alloc_cache(B)
-    ws = ctx.alloc_workspace(B)
+    ws = ctx.alloc_workspace(B)          # single-layer launches
+    ws_l = ctx.alloc_workspace(B, L)     # cross-layer launches (one slice per layer)
     # resident inputs (distinct per layer and per rank)
     Q, K, V = [], [], []
     for l in range(L):
@@ -306,9 +310,11 @@ def run_ours(args, rank, world, local_rank):
     O = torch.empty_like(Q[0])
     qd, kd, vd = decode_tokens(CFG, 1000 * rank, T, device=dev)
     od = torch.empty(B, CFG.hq, d, dtype=torch.bfloat16, device=dev)
+    od_l = torch.empty(L, B, CFG.hq, d, dtype=torch.bfloat16, device=dev)
     stream = torch.cuda.current_stream()
+    ctx.prepare_layers()
 
-    n_ev = T * L
+    n_ev = T   # decode launches per step (one per token)
     ev_p = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
 
     def step(record=False):
@@ -321,12 +327,13 @@ def run_ours(args, rank, world, local_rank):
             ctx.cache_fill(l, K[l], V[l])     # = moa_prefill split in two so the attention kernel is timed alone
         ph = torch.cuda.Event(enable_timing=True)
         ph.record(stream)
-        # decode: no event between launches -- an event record between two PDL launches stops the
-        # next kernel's prologue from overlapping the previous one's tail (measured 60.0 vs 52.6 us
-        # per launch, tools/time_decode.py); the phase events bracket the launches instead.
+        # decode: one cross-layer launch per token (moa_decode_step_fused_layers: all 32 layers'
+        # append + split-KV decode + combine; every layer reads this token's q -- layer stride 0).
+        # No event between launches (an event record between two PDL launches stops the next
+        # kernel's prologue from overlapping the previous one's tail); the phase events bracket them.
         for t in range(T):
-            for l in range(L):
-                ctx.decode_step_fused(l, qd[t], kd[t], vd[t], od, N + t, scale, ws)
+            ctx.decode_step_fused_layers(0, qd[t].expand(L, *qd[t].shape), kd[t].expand(L, *kd[t].shape),
+                                         vd[t].expand(L, *vd[t].shape), od_l, N + t, scale, ws_l)
         return ph
 
     for _ in range(args.warmup):
@@ -363,11 +370,11 @@ def run_ours(args, rank, world, local_rank):
     decode_tps = B * T * world * K_steps / (dec / 1e3)
     prefill_tps = B * N * world * K_steps / (pre / 1e3)
 
-    # roofline of the dominant kernel (decode: one launch per layer-token)
+    # roofline of the dominant kernel (decode: one cross-layer launch per token)
     flops, dec_bytes_per_token = algorithmic_work(windows, B, N, T, s, d, CFG.group)
     peaks, peak_src = load_peaks()
     dk_avg_ms = dec / (K_steps * n_ev)   # decode phase (max over ranks) / launches, gaps included
-    dec_bytes_per_launch = dec_bytes_per_token / L
+    dec_bytes_per_launch = dec_bytes_per_token
     achieved_gbs = dec_bytes_per_launch / (dk_avg_ms / 1e3) / 1e9
     pk_total_s = sum(pk_ms) / 1e3 / K_steps
     achieved_tf = flops / pk_total_s / 1e12
@@ -382,10 +389,13 @@ def run_ours(args, rank, world, local_rank):
                         f"its algorithmic bytes {tj.get('algorithmic_bytes_same_launch')}, "
                         f"ratio {tj.get('traffic_over_algorithmic'):.3f}")
 
+    # ---------------- the same decode with one launch per layer (a model whose layer l+1 query
+    # depends on layer l's output cannot batch its layers): 64 tokens, same cache, same timing
+    per_layer = run_per_layer(ctx, ws, K, V, qd, kd, vd, od, scale, world, dev, dec_bytes_per_token, peaks)
     # ---------------- e2e: host buffers through the public API, H2D/D2H inside the timed region
-    e2e = run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev)
+    e2e = run_e2e(ctx, ws_l, Q, K, V, qd, kd, vd, scale, world, dev)
     del Q, K, V, O
-    ctx = ws = None
+    ctx = ws = ws_l = None
     torch.cuda.empty_cache()
     kv_shard = None
     if world > 1 or args.kv_shard:
@@ -418,13 +428,15 @@ def run_ours(args, rank, world, local_rank):
             "decode_ms_per_step": dec / K_steps,
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic, "traffic_note": traffic_note,
-                         "kernel": "moa decode_kernel (fused append + split-KV + last-CTA combine)",
+                         "kernel": "decode_mma_kernel<128,2,2,ML=true>: one launch per token over all 32 layers "
+                                   "(fused append + split-KV + last-CTA combine per layer)",
                          "bytes_per_launch": dec_bytes_per_launch, "avg_launch_ms": dk_avg_ms,
                          "avg_launch_note": "decode phase time (CUDA events on the launch stream, timed "
                                             "steps) / launches; inter-launch gaps count against the kernel",
                          "peak_source": peak_src},
             "e2e": e2e,
-            "gpu_launches": K_steps * (2 * L + T * L),
+            "decode_per_layer": per_layer,
+            "gpu_launches": K_steps * (2 * L + T),
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
@@ -524,44 +536,57 @@ def _bench_decode_cfg(moa, cfg, layers, T, dev, peaks):
     for i, l in enumerate(layers):
         ctx.set_spans(i, wins[l], s, N)
     ctx.alloc_cache(B)
-    ws = ctx.alloc_workspace(B)
+    nl = len(layers)
+    ws = ctx.alloc_workspace(B, nl)
+    ctx.prepare_layers()
     g = torch.Generator(device=dev).manual_seed(cfg.seed_base + 7)
     kp = torch.randn(B, N, cfg.hkv, d, device=dev, generator=g).to(torch.bfloat16)
     vp = torch.randn(B, N, cfg.hkv, d, device=dev, generator=g).to(torch.bfloat16)
     qd, kd, vd = decode_tokens(cfg, 0, T, device=dev)
-    od = torch.empty(B, cfg.hq, d, dtype=torch.bfloat16, device=dev)
+    od = torch.empty(nl, B, cfg.hq, d, dtype=torch.bfloat16, device=dev)
     scale = 1 / math.sqrt(d)
 
     def layer_bytes(l, p):   # in-window bytes of one layer-token + q/o + new token
         wg = [max(wins[l][x * G:(x + 1) * G]) for x in range(cfg.hkv)]
         return B * (sum(min(p + 1, s + w) for w in wg) * d * 4 + cfg.hq * d * 4 + cfg.hkv * d * 8)
 
-    def run():
-        for i in range(len(layers)):
+    def run(cross):
+        for i in range(nl):
             ctx.cache_fill(i, kp, vp)  # positions restart at N
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for t in range(T):
-            for i in range(len(layers)):
-                ctx.decode_step_fused(i, qd[t], kd[t], vd[t], od, N + t, scale, ws)
+            if cross:   # one launch per token over the resident layers
+                ctx.decode_step_fused_layers(0, qd[t].expand(nl, *qd[t].shape), kd[t].expand(nl, *kd[t].shape),
+                                             vd[t].expand(nl, *vd[t].shape), od, N + t, scale, ws)
+            else:
+                for i in range(nl):
+                    ctx.decode_step_fused(i, qd[t], kd[t], vd[t], od[i], N + t, scale, ws)
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / 1e3
 
-    run()
+    run(True)
     with ClockSampler(dev.index) as clk:
-        sec = statistics.median(run() for _ in range(3))
+        sec = statistics.median(run(True) for _ in range(3))
+    run(False)
+    sec_pl = statistics.median(run(False) for _ in range(2))
     by_timed = sum(layer_bytes(l, N + t) for t in range(T) for l in layers)
     by_all = sum(layer_bytes(l, N + t) for t in range(T) for l in range(L_all))
     gbs = by_timed / sec / 1e9
+    gbs_pl = by_timed / sec_pl / 1e9
     sec_model = by_all / (gbs * 1e9)          # all L layers at the measured in-window rate
     out = {"tokens_per_s": B * T / sec_model, "unit": "tokens/s", "batch": B, "tokens": T,
            "positions": [N, N + T - 1], "layers_timed": len(layers), "layers_model": L_all,
+           "launch": "moa_decode_step_fused_layers: one launch per token over the resident layers",
            "us_per_layer_token": sec / (T * len(layers)) * 1e6,
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": gbs / peaks["hbm_gbs"], "traffic": None,
-                        "bytes_per_launch": by_timed / (T * len(layers))},
+                        "bytes_per_launch": by_timed / T},
+           "per_layer": {"tokens_per_s": B * T / (by_all / (gbs_pl * 1e9)), "achieved_gbs": gbs_pl,
+                         "frac": gbs_pl / peaks["hbm_gbs"],
+                         "note": "moa_decode_step_fused, one launch per layer-token"},
            "clocks": clk.summary()}
     if len(layers) < L_all:
         out["sampling"] = (f"{len(layers)} of {L_all} layers resident (every {layers[1] - layers[0]}th, "
@@ -635,6 +660,35 @@ def run_configs(dev, peaks):
     return out
 
 
+def run_per_layer(ctx, ws, K, V, qd, kd, vd, od, scale, world, dev, bytes_per_token, peaks, T=64):
+    """Decode tokens/s with one moa_decode_step_fused launch per layer-token (the model-faithful
+    order when layer l+1's query depends on layer l), on the same resident cache."""
+    L, B, N = CFG.layers, CFG.batch, CFG.N
+    for l in range(L):
+        ctx.cache_fill(l, K[l], V[l])    # positions restart at N
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(T):
+        for l in range(L):
+            ctx.decode_step_fused(l, qd[t], kd[t], vd[t], od, N + t, scale, ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        x = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+        ms = x.item()
+    gbs = bytes_per_token * T / (ms / 1e3) / 1e9
+    return {"value": B * T * world / (ms / 1e3), "unit": "tokens/s", "tokens": T,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / peaks["hbm_gbs"], "avg_launch_ms": ms / (T * L)},
+            "note": "moa_decode_step_fused, one launch per layer-token (decode_mma_kernel<128,2,2,ML=false>, "
+                    "PDL-chained)"}
+
+
 def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
     """Decode tokens/s through MoAContext with pinned HOST inputs and outputs.
 
@@ -693,10 +747,8 @@ def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
         if t >= 2:
             stream.wait_event(ev_out[t - 2])       # dout[t % 2] drained to host
         buf, ob = din[t % 2], dout[t % 2]
-        for l in range(L):
-            row = buf[l]
-            ctx.decode_step_fused(l, row[:nq].view(B, hq_, d), row[nq:nq + nk].view(B, hkv_, d),
-                                  row[nq + nk:].view(B, hkv_, d), ob[l], N + t, scale, ws)
+        ctx.decode_step_fused_layers(0, buf[:, :nq].view(L, B, hq_, d), buf[:, nq:nq + nk].view(L, B, hkv_, d),
+                                     buf[:, nq + nk:].view(L, B, hkv_, d), ob, N + t, scale, ws)
         ev_done[t].record(stream)
         cs.wait_event(ev_done[t])
         with torch.cuda.stream(cs):
@@ -716,8 +768,9 @@ def run_e2e(ctx, ws, Q, K, V, qd, kd, vd, scale, world, dev):
     return {"value": B * T * world / (dec_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "prefill_ms": e0.elapsed_time(e1), "decode_ms": dec_ms,
             "note": "1 step; prefill inputs of one layer staged host->device per layer (o read back); "
-                    "decode: per token one pinned H2D of q/k_new/v_new for all layers and one D2H of o "
-                    "for all layers, on a copy stream double-buffered against the decode launches"}
+                    "decode: per token one pinned H2D of q/k_new/v_new for all layers, one cross-layer "
+                    "launch and one D2H of o for all layers, on a copy stream double-buffered against "
+                    "the decode launches"}
 
 
 def main():

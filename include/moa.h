@@ -246,6 +246,43 @@ moa_status moa_decode_step_fused(moa_ctx *ctx, int layer, const void *q, const v
                                  size_t ws_bytes, moa_stream_t stream);
 
 /*
+ * Cross-layer decode: moa_decode_step_fused of the layers
+ * [layer0, layer0 + n_layers) for one token position in ONE persistent launch.  Every CTA
+ * streams its share of layer l's cache and then, without draining its TMA pipeline, its
+ * share of layer l+1, so the per-launch ramp-up and tail (the last CTAs, the last
+ * region's LSE merge) are paid once per token instead of once per layer.  Each layer is
+ * masked and merged exactly as moa_decode_step_fused does it (heads masked
+ * independently).  With the rank-invariant split (moa_set_decode_split)
+ * the results are bitwise those of n_layers single-layer calls; with the balanced split the
+ * CTA ranges can differ (the grid is sized for the largest layer), so they agree to rounding.
+ * Ranges longer than 32 layers run as several launches of <= 32 layers.  For when the q of several layers are available together
+ * (layer-parallel blocks, the attention sub-step of a pipelined schedule, the synthetic
+ * benchmark); a model whose layer l+1 query depends on layer l's output uses the
+ * single-layer call.
+ *   q, o            bf16 [n_layers][B][Hq_local][d]: layer stride q/o_layer_stride, batch
+ *                   stride q/o_batch_stride (elements)
+ *   k_new, v_new    bf16 [n_layers][B][Hkv_local][d]: kv_layer_stride, kv_batch_stride
+ *                   (input layer strides may be 0: every layer reads the same rows)
+ *   lse_out         nullable fp32, layer stride lse_layer_stride, [B][Hq_local] per layer
+ *   workspace       >= n_layers * moa_workspace_bytes(ctx, batch) bytes; layer i uses the
+ *                   i-th equal slice
+ * Every layer must be set, bound with tensor maps (bf16), uniform (not ragged), share one
+ * sink count and expect `pos` (all advance to pos + 1).  The launch reads a device copy of
+ * the layers' tables built by moa_prepare_layers; if it is stale (set_spans, bind,
+ * set_decode_split or set_ragged since), the call rebuilds it first, which synchronises the
+ * device -- or fails with MOA_ERR_STATE while `stream` is capturing a CUDA graph.  The
+ * launch does not stream early (its predecessor may be the previous token's launch, which
+ * appended to these layers).
+ */
+moa_status moa_prepare_layers(moa_ctx *ctx);
+moa_status moa_decode_step_fused_layers(moa_ctx *ctx, int layer0, int n_layers, const void *q, const void *k_new,
+                                        const void *v_new, void *o, int64_t q_layer_stride,
+                                        int64_t kv_layer_stride, int64_t o_layer_stride, int64_t q_batch_stride,
+                                        int64_t kv_batch_stride, int64_t o_batch_stride, int batch, int64_t pos,
+                                        float scale, float *lse_out, int64_t lse_layer_stride, void *workspace,
+                                        size_t ws_bytes, moa_stream_t stream);
+
+/*
  * Append + decode of a ragged batch: moa_decode_step_fused where sequence b is at its
  * own position pos[b] (a6 + a7 + a8 per sequence, PAPER.md:704 cache replacement).
  *   pos   DEVICE int64 [batch], caller-owned, 8-byte aligned, read by the kernel after its

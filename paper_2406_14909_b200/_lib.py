@@ -47,6 +47,10 @@ _SIGS = [
     ("moa_decode_step_fused", c_int, [_P, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int, c_int64,
                                       c_float, _P, _P, c_size_t, _P]),
     ("moa_advance_pos", c_int, [_P, c_int, c_int64, _P]),
+    ("moa_prepare_layers", c_int, [_P]),
+    ("moa_decode_step_fused_layers", c_int, [_P, c_int, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int64,
+                                             c_int64, c_int64, c_int, c_int64, c_float, _P, c_int64, _P, c_size_t,
+                                             _P]),
     ("moa_set_decode_split", c_int, [_P, c_int]),
     ("moa_decode_step_fused_ragged", c_int, [_P, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int, _P,
                                              c_float, _P, _P, c_size_t, _P]),

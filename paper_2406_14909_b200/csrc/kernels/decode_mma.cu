@@ -103,6 +103,10 @@ struct MParams {
   float *part;
   int *counters;
   int early;  // 1: the producer may stream the cache before the stream predecessor completes
+  // cross-layer launch (ML kernels only): per-layer tables and per-call layer strides
+  const DecodeLayerDesc *ml;
+  int nl;
+  int64_t q_ls, o_ls, kvn_ls, lse_ls, part_ls;
 #ifdef MOA_DEC_TRACE
   int trace_slot;
 #endif
@@ -248,6 +252,7 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *m, 
 // barrier id two segments later only after a hand-off in the other direction, so phases
 // never overlap.
 constexpr int kBarQFull = 1, kBarSegDone = 3;  // ids 1,2 and 3,4 (0 is __syncthreads)
+constexpr int kBarMl = 5;                      // cross-layer table (consumers + epilogue)
 constexpr int kHandoff = (kCW + 1) * 32;       // consumers + epilogue warp
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   __syncwarp();
@@ -327,112 +332,294 @@ __device__ __forceinline__ void combine_region_warp(const MParams &p, const int6
   }
 }
 
-template <int D, int STAGES, int CPS>
+// ---- cross-layer launch support (ML = true): each warp role walks the layers of the launch
+// in order with its own view of the current layer's parameters in shared memory (built by
+// one lane from the launch parameters + the layer's DecodeLayerDesc), so roles that run
+// ahead (the producer, the epilogue's q staging) never wait for the others at a layer
+// boundary.  The single-layer kernel (ML = false) reads the kernel parameters and the
+// shared-memory tables directly, as before.
+struct Tabs {
+  const int64_t *goff;
+  const int *wing;
+  const int *gc;
+};
+
+__device__ __forceinline__ void cta_range(const MParams &p, const Tabs &t, int64_t &X0, int64_t &X1) {
+  const int64_t n_cta = gridDim.x;
+  if (p.chunk) {
+    const int64_t J0 = chunk_cut(p, t.goff, t.gc, ((int64_t)blockIdx.x * p.ctot + n_cta - 1) / n_cta);
+    const int64_t J1 = chunk_cut(p, t.goff, t.gc, ((int64_t)(blockIdx.x + 1) * p.ctot + n_cta - 1) / n_cta);
+    X0 = chunk_row(p, t.goff, t.gc, J0);
+    X1 = chunk_row(p, t.goff, t.gc, J1);
+  } else {
+    X0 = cut_row(p, t.goff, ((int64_t)blockIdx.x * p.ctot + n_cta - 1) / n_cta);
+    X1 = cut_row(p, t.goff, ((int64_t)(blockIdx.x + 1) * p.ctot + n_cta - 1) / n_cta);
+  }
+}
+
+// view of layer l of a cross-layer launch (one thread writes it)
+__device__ __forceinline__ void build_view(const MParams &b, int l, MParams *out) {
+  const DecodeLayerDesc &dl = b.ml[l];
+  MParams v = b;
+  v.q = b.q + l * b.q_ls;
+  v.o = b.o + l * b.o_ls;
+  if (b.k_new) {
+    v.k_new = b.k_new + l * b.kvn_ls;
+    v.v_new = b.v_new + l * b.kvn_ls;
+  }
+  if (b.lse) v.lse = b.lse + l * b.lse_ls;
+  v.part = b.part + l * b.part_ls;
+  v.kc = static_cast<__nv_bfloat16 *>(dl.kc);
+  v.vc = static_cast<__nv_bfloat16 *>(dl.vc);
+  v.g_off = dl.g_off;
+  v.win_g = dl.win_g;
+  v.win_q = dl.win_q;
+  v.gc_off = dl.gc_off;
+  v.counters = dl.counters;
+  v.rows_per_seq = dl.rows_per_seq;
+  v.R = (int64_t)b.batch * dl.rows_per_seq;
+  v.ctot = b.chunk ? v.R + b.seg_cost * (int64_t)b.batch * dl.dec_cps
+                   : v.R + b.seg_cost * ((int64_t)b.batch * b.ngl - 1);
+  *out = v;
+}
+
+// Per-CTA table of a cross-layer launch, computed once at kernel start (shared memory): the
+// CTA's row range in every layer and the region holding its first row, so a role entering a
+// layer needs no binary search over global tables (dependent L2 round trips).
+constexpr int kMaxMl = 32;  // layers per cross-layer launch (the host splits longer ranges)
+struct MlRange {
+  int64_t X0, X1, start;  // CTA range; first row of the region holding X0
+  int b, g, Wg, pad_;
+};
+
+// Enter the next layer (of this role) whose CTA range is not empty.  l = -1 before the first
+// call.  whole_warp: every lane of the warp calls this (lane 0 builds the view).
+template <bool ML>
+__device__ __forceinline__ bool enter_layer(const MParams &p0, int &l, const MParams *&vp, Tabs &t, int64_t &X0,
+                                            int64_t &X1, Region &first, MParams *slot, const Tabs &smem_tabs,
+                                            const MlRange *rng, bool whole_warp) {
+  first.end = -1;
+  if constexpr (!ML) {
+    if (l >= 0) return false;
+    l = 0;
+    vp = &p0;
+    t = smem_tabs;
+    cta_range(p0, t, X0, X1);
+    return X0 < X1;
+  } else {
+    while (++l < p0.nl) {
+      const MlRange &r = rng[l];
+      if (r.X0 >= r.X1) continue;
+      if (whole_warp) __syncwarp();  // every lane is done with the previous view
+      if (!whole_warp || (threadIdx.x & 31) == 0) build_view(p0, l, slot);
+      if (whole_warp) __syncwarp();
+      vp = slot;
+      t.goff = slot->g_off;
+      t.wing = slot->win_g;
+      t.gc = slot->gc_off;
+      X0 = r.X0;
+      X1 = r.X1;
+      first.b = r.b;
+      first.g = r.g;
+      first.Wg = r.Wg;
+      first.start = r.start;
+      first.end = r.start + p0.n_sink + r.Wg;
+      return true;
+    }
+    return false;
+  }
+}
+
+// Region holding row x, the segment walk's next region (x == rg.end, or rg.end < 0 at the
+// start of a layer).  ML: regions of a layer are consecutive in (b, g) order, so the next one
+// starts at rg.end and needs only W_g of its group (one load, an L1 hit after the producer).
+template <bool ML>
+__device__ __forceinline__ Region region_at(const MParams &p, const Tabs &t, const Region &rg, const Region &first,
+                                            int64_t x) {
+  if constexpr (!ML) {
+    return region_of(p, t.goff, t.wing, x);
+  } else {
+    if (rg.end < 0) return first;
+    Region r;
+    r.g = rg.g + 1;
+    r.b = rg.b;
+    if (r.g == p.ngl) {
+      r.g = 0;
+      ++r.b;
+    }
+    r.Wg = t.wing[r.g];
+    r.start = rg.end;
+    r.end = r.start + p.n_sink + r.Wg;
+    return r;
+  }
+}
+
+template <int D, int STAGES, int CPS, bool ML>
 __global__ void __launch_bounds__(kThreads, CPS)
     decode_mma_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                       const __grid_constant__ CUtensorMap tm_k16, const __grid_constant__ CUtensorMap tm_v16,
-                      const MParams p) {
+                      const __grid_constant__ MParams p0) {
   using C = DCfg<D, STAGES>;
   constexpr int NT = D / 8;   // output n-tiles (8 dims each)
   constexpr int KS = D / 16;  // k-steps over the head dim
   constexpr int QS = q_stride<D>();
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full_bar[C::kStages], empty_bar[C::kStages];
-  __shared__ int64_t s_goff[kMaxGroups];
-  __shared__ int s_wing[kMaxGroups];
-  __shared__ int s_gc[kMaxGroups + 1];
+  __shared__ int64_t s_goff[ML ? 1 : kMaxGroups];
+  __shared__ int s_wing[ML ? 1 : kMaxGroups];
+  __shared__ int s_gc[ML ? 1 : kMaxGroups + 1];
   __shared__ __align__(16) __nv_bfloat16 s_q[2][16 * QS];
+  // per-role layer views (ML): consumers 0..kCW-1, producer, epilogue staging, epilogue merge
+  __shared__ __align__(16) MParams s_view[ML ? kCW + 3 : 1];
+  __shared__ MlRange s_rng[ML ? kMaxMl : 1];
+  __shared__ uint64_t rng_bar;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   // per-warp partials of the two segments in flight: [2][kCW][G][D + 4] fp32 after the tiles
   float *s_part = reinterpret_cast<float *>(smem_raw + (base - smem_u32(smem_raw)) + C::kStages * 2 * C::kTileBytes);
-  if (tid == 0) TRACE(0);
+  {
+    const MParams &p = p0;
+    if (tid == 0) TRACE(0);
+  }
 
   if (tid == 0) {
     for (int i = 0; i < C::kStages; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), kCW);
     }
+    mbar_init(smem_u32(&rng_bar), 1);
     fence_mbar_init();
   }
-  for (int g = tid; g < p.ngl; g += kThreads) {
-    s_goff[g] = p.g_off[g];
-    s_wing[g] = p.win_g[g];
+  if constexpr (!ML) {
+    for (int g = tid; g < p0.ngl; g += kThreads) {
+      s_goff[g] = p0.g_off[g];
+      s_wing[g] = p0.win_g[g];
+    }
+    __syncthreads();
+    if (p0.chunk)
+      for (int g = tid; g <= p0.ngl; g += kThreads) s_gc[g] = p0.gc_off[g];
   }
   __syncthreads();
-  if (p.chunk)
-    for (int g = tid; g <= p.ngl; g += kThreads) s_gc[g] = p.gc_off[g];
-  __syncthreads();
-  const int64_t n_cta = gridDim.x;
-  int64_t X0, X1;
-  if (p.chunk) {
-    const int64_t J0 = chunk_cut(p, s_goff, s_gc, ((int64_t)blockIdx.x * p.ctot + n_cta - 1) / n_cta);
-    const int64_t J1 = chunk_cut(p, s_goff, s_gc, ((int64_t)(blockIdx.x + 1) * p.ctot + n_cta - 1) / n_cta);
-    X0 = chunk_row(p, s_goff, s_gc, J0);
-    X1 = chunk_row(p, s_goff, s_gc, J1);
-  } else {
-    X0 = cut_row(p, s_goff, ((int64_t)blockIdx.x * p.ctot + n_cta - 1) / n_cta);
-    X1 = cut_row(p, s_goff, ((int64_t)(blockIdx.x + 1) * p.ctot + n_cta - 1) / n_cta);
+  const Tabs smem_tabs{s_goff, s_wing, s_gc};
+  if constexpr (ML) {
+    // this CTA's range and first region in every layer, computed by the consumer and
+    // epilogue warps in parallel (two boundary cuts per layer, then the first region); the
+    // producer waits for rng_bar before its first layer.  Overlaps the predecessor's tail.
+    if (warp != kProd) {
+      const int t = warp < kCW ? tid : tid - 32;  // 0 .. kHandoff-1
+      for (int j = t; j < 2 * p0.nl; j += kHandoff) {
+        MParams v;
+        const int l = j >> 1;
+        build_view(p0, l, &v);
+        const Tabs tb{v.g_off, v.win_g, v.gc_off};
+        const int64_t n_cta = gridDim.x, c = blockIdx.x + (j & 1);
+        const int64_t T = (c * v.ctot + n_cta - 1) / n_cta;
+        const int64_t X = v.chunk ? chunk_row(v, tb.goff, tb.gc, chunk_cut(v, tb.goff, tb.gc, T)) : cut_row(v, tb.goff, T);
+        if (j & 1) s_rng[l].X1 = X; else s_rng[l].X0 = X;
+      }
+      named_bar_sync(kBarMl, kHandoff);
+      for (int l = t; l < p0.nl; l += kHandoff) {
+        MlRange &r = s_rng[l];
+        if (r.X0 < r.X1) {
+          MParams v;
+          build_view(p0, l, &v);
+          const Region rg = region_of(v, v.g_off, v.win_g, r.X0);
+          r.b = rg.b;
+          r.g = rg.g;
+          r.Wg = rg.Wg;
+          r.start = rg.start;
+        }
+      }
+      named_bar_sync(kBarMl, kHandoff);
+      if (t == 0) mbar_arrive(smem_u32(&rng_bar));
+    }
   }
-  // Programmatic dependent launch.  Everything above overlapped the previous kernel's tail.
-  // The consumers and the epilogue warp wait for the stream predecessor (q, k_new, the
-  // workspace, the tickets and o may be its inputs/outputs) before they trigger the next
-  // launch, so a CTA's trigger implies its predecessor completed: when this kernel starts,
-  // every kernel before its predecessor has completed and flushed.  With p.early the host has
-  // established that the predecessor does not write this layer's cache, so the producer
-  // streams cache tiles at once.
-  if (tid == 0) TRACE(1);
-  if (X0 >= X1) {
-    griddep_wait();
-    return;
+  if constexpr (!ML) {
+    // Programmatic dependent launch.  Everything above overlapped the previous kernel's tail.
+    // The consumers and the epilogue warp wait for the stream predecessor (q, k_new, the
+    // workspace, the tickets and o may be its inputs/outputs) before they trigger the next
+    // launch, so a CTA's trigger implies its predecessor completed: when this kernel starts,
+    // every kernel before its predecessor has completed and flushed.  With p.early the host has
+    // established that the predecessor does not write this layer's cache, so the producer
+    // streams cache tiles at once.
+    const MParams &p = p0;
+    if (tid == 0) TRACE(1);
+    int64_t X0, X1;
+    cta_range(p0, smem_tabs, X0, X1);
+    if (X0 >= X1) {
+      griddep_wait();
+      return;
+    }
   }
 
   if (warp == kProd) {
     // ------------------------------------------------------------ producer: TMA K/V tiles
     if (lane == 0) {
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      tma_prefetch_desc(&tm_k16);
-      tma_prefetch_desc(&tm_v16);
-      if (!p.early) griddep_wait();
-      TRACE(2);
+      if constexpr (!ML) {
+        tma_prefetch_desc(&tm_k);
+        tma_prefetch_desc(&tm_v);
+        tma_prefetch_desc(&tm_k16);
+        tma_prefetch_desc(&tm_v16);
+      }
+      if (!p0.early) griddep_wait();
+      if constexpr (ML) mbar_wait(smem_u32(&rng_bar), 0);
+      {
+        const MParams &p = p0;
+        TRACE(2);
+      }
       int T = 0;
       bool trig = false;
-      Region rg;
-      rg.end = -1;
-      for (int64_t x = X0; x < X1;) {
-        if (x >= rg.end) rg = region_of(p, s_goff, s_wing, x);
-        const int64_t seg_end = seg_end_of(p, rg, x, X1);
-        for (int64_t t0 = x; t0 < seg_end; t0 += kRows, ++T) {
-          const int st = T % C::kStages;
-          if (T >= C::kStages) {
-            mbar_wait(smem_u32(&empty_bar[st]), ((T - C::kStages) / C::kStages) & 1);
-            if (!trig) {  // the consumers have passed their griddepcontrol.wait
-              griddep_launch_dependents();
-              trig = true;
-            }
-          }
-          const uint32_t fb = smem_u32(&full_bar[st]);
-          const uint32_t kd = base + st * 2 * C::kTileBytes, vd = kd + C::kTileBytes;
-          const int64_t nrows = seg_end - t0;
-          if (nrows >= kRows) {
-            mbar_expect_tx(fb, 2 * C::kTileBytes);
-            for (int sl = 0; sl < C::kSlabs; ++sl) {
-              tma_load_2d(kd + sl * C::kSlabBytes, &tm_k, fb, sl * 64, (int)t0);
-              tma_load_2d(vd + sl * C::kSlabBytes, &tm_v, fb, sl * 64, (int)t0);
-            }
-          } else {  // segment tail: only the 16-row groups that hold rows of the segment
-            const int n16 = ((int)nrows + 15) >> 4;
-            mbar_expect_tx(fb, 2 * n16 * 16 * D * 2);
-            for (int r = 0; r < n16; ++r)
-              for (int sl = 0; sl < C::kSlabs; ++sl) {
-                tma_load_2d(kd + sl * C::kSlabBytes + r * 2048, &tm_k16, fb, sl * 64, (int)t0 + 16 * r);
-                tma_load_2d(vd + sl * C::kSlabBytes + r * 2048, &tm_v16, fb, sl * 64, (int)t0 + 16 * r);
-              }
-          }
+      int l = -1;
+      const MParams *vp = nullptr;
+      Tabs tb;
+      int64_t X0, X1;
+      Region first;
+      while (enter_layer<ML>(p0, l, vp, tb, X0, X1, first, &s_view[ML ? kCW : 0], smem_tabs, s_rng, false)) {
+        const MParams &p = *vp;
+        const CUtensorMap *mk = &tm_k, *mv = &tm_v, *mk16 = &tm_k16, *mv16 = &tm_v16;
+        if constexpr (ML) {
+          const CUtensorMap *mm = static_cast<const CUtensorMap *>(p0.ml[l].maps);
+          mk = mm;
+          mv = mm + 1;
+          mk16 = mm + 2;
+          mv16 = mm + 3;
         }
-        x = seg_end;
+        Region rg;
+        rg.end = -1;
+        for (int64_t x = X0; x < X1;) {
+          if (x >= rg.end) rg = region_at<ML>(p, tb, rg, first, x);
+          const int64_t seg_end = seg_end_of(p, rg, x, X1);
+          for (int64_t t0 = x; t0 < seg_end; t0 += kRows, ++T) {
+            const int st = T % C::kStages;
+            if (T >= C::kStages) {
+              mbar_wait(smem_u32(&empty_bar[st]), ((T - C::kStages) / C::kStages) & 1);
+              if (!trig) {  // the consumers have passed their griddepcontrol.wait
+                griddep_launch_dependents();
+                trig = true;
+              }
+            }
+            const uint32_t fb = smem_u32(&full_bar[st]);
+            const uint32_t kd = base + st * 2 * C::kTileBytes, vd = kd + C::kTileBytes;
+            const int64_t nrows = seg_end - t0;
+            if (nrows >= kRows) {
+              mbar_expect_tx(fb, 2 * C::kTileBytes);
+              for (int sl = 0; sl < C::kSlabs; ++sl) {
+                tma_load_2d(kd + sl * C::kSlabBytes, mk, fb, sl * 64, (int)t0);
+                tma_load_2d(vd + sl * C::kSlabBytes, mv, fb, sl * 64, (int)t0);
+              }
+            } else {  // segment tail: only the 16-row groups that hold rows of the segment
+              const int n16 = ((int)nrows + 15) >> 4;
+              mbar_expect_tx(fb, 2 * n16 * 16 * D * 2);
+              for (int r = 0; r < n16; ++r)
+                for (int sl = 0; sl < C::kSlabs; ++sl) {
+                  tma_load_2d(kd + sl * C::kSlabBytes + r * 2048, mk16, fb, sl * 64, (int)t0 + 16 * r);
+                  tma_load_2d(vd + sl * C::kSlabBytes + r * 2048, mv16, fb, sl * 64, (int)t0 + 16 * r);
+                }
+            }
+          }
+          x = seg_end;
+        }
       }
     }
     return;
@@ -442,123 +629,160 @@ __global__ void __launch_bounds__(kThreads, CPS)
     // ------------------------------------------------------------ epilogue warp
     griddep_wait();
     griddep_launch_dependents();
-    const int G = p.G;
-    int64_t xs = X0;  // staging cursor (runs two segments ahead of the consumers)
+    const int G = p0.G;
+    // staging cursor (runs two segments ahead of the consumers; may be a layer ahead)
+    int ls = -1;
+    const MParams *sp = nullptr;
+    Tabs stb;
+    int64_t sX0 = 0, sX1 = 0;
+    Region sfirst;
+    bool s_more = enter_layer<ML>(p0, ls, sp, stb, sX0, sX1, sfirst, &s_view[ML ? kCW + 1 : 0], smem_tabs, s_rng, true);
+    int64_t xs = sX0;
     int ns = 0;
-    int buf_region[2] = {-1, -1};  // region whose q rows each staging buffer holds
+    int64_t buf_region[2] = {-1, -1};  // (layer, region) whose q rows each staging buffer holds
     Region r;
     r.end = -1;
     auto stage_next = [&]() {
-      if (xs >= X1) return;
-      if (xs >= r.end) r = region_of(p, s_goff, s_wing, xs);
+      if (!s_more) return;
+      if (xs >= sX1) {
+        s_more = enter_layer<ML>(p0, ls, sp, stb, sX0, sX1, sfirst, &s_view[ML ? kCW + 1 : 0], smem_tabs, s_rng, true);
+        if (!s_more) return;
+        xs = sX0;
+        r.end = -1;
+      }
+      const MParams &p = *sp;
+      if (xs >= r.end) r = region_at<ML>(p, stb, r, sfirst, xs);
       const int ridx = r.b * p.ngl + r.g;
-      if (buf_region[ns & 1] != ridx) {  // consecutive chunks of one region share their q rows
+      const int64_t key = ((int64_t)ls << 32) | (uint32_t)ridx;
+      if (buf_region[ns & 1] != key) {  // consecutive chunks of one region share their q rows
         const __nv_bfloat16 *qb = p.q + (int64_t)r.b * p.q_bs + (int64_t)r.g * G * D;
         __nv_bfloat16 *sq = s_q[ns & 1];
         for (int v = lane; v < G * (D / 8); v += 32) {
           const int h = v / (D / 8), e = (v - h * (D / 8)) * 8;
           *reinterpret_cast<uint4 *>(sq + h * QS + e) = *reinterpret_cast<const uint4 *>(qb + h * D + e);
         }
-        buf_region[ns & 1] = ridx;
+        buf_region[ns & 1] = key;
       }
       named_bar_arrive(kBarQFull + (ns & 1), kHandoff);
-      xs = seg_end_of(p, r, xs, X1);
+      xs = seg_end_of(p, r, xs, sX1);
       ++ns;
     };
     stage_next();
     stage_next();
     int n = 0;
-    int run = 0;  // segments of the current region this CTA has finished (one ticket per run)
-    Region rg;
-    rg.end = -1;
-    int64_t slot = 0;
-    for (int64_t x = X0; x < X1; ++n) {
-      if (x >= rg.end) {
-        rg = region_of(p, s_goff, s_wing, x);
-        slot = p.chunk ? (int64_t)rg.b * s_gc[p.ngl] + s_gc[rg.g] + (x - rg.start) / p.chunk
-                       : (int64_t)blockIdx.x + rg.b * p.ngl + rg.g;
-      } else {
-        ++slot;  // next chunk of the same region (chunk mode only)
-      }
-      const int64_t seg_end = seg_end_of(p, rg, x, X1);
-      named_bar_sync(kBarSegDone + (n & 1), kHandoff);
-      // every consumer warp's partial of segment n is in shared memory (mbarrier release/
-      // acquire): merge the kCW of them by LSE into this segment's slot
-      const int ridx = rg.b * p.ngl + rg.g;
-      {
-        constexpr int PS = part_stride<D>();
-        constexpr int NE = D / 32;
-        const float *sp = s_part + (size_t)(n & 1) * kCW * G * PS;
-        float *gp = p.part + slot * G * PS;
-        for (int j = 0; j < G; ++j) {
-          float ls[kCW], mx = -INFINITY;
-#pragma unroll
-          for (int w = 0; w < kCW; ++w) {
-            ls[w] = sp[(w * G + j) * PS + D];
-            mx = fmaxf(mx, ls[w]);
-          }
-          float L = 0.f, O[NE];
-#pragma unroll
-          for (int i = 0; i < NE; ++i) O[i] = 0.f;
-          if (mx != -INFINITY) {
+    int lm = -1;
+    const MParams *mp = nullptr;
+    Tabs mtb;
+    int64_t X0, X1;
+    Region mfirst;
+    while (enter_layer<ML>(p0, lm, mp, mtb, X0, X1, mfirst, &s_view[ML ? kCW + 2 : 0], smem_tabs, s_rng, true)) {
+      const MParams &p = *mp;
+      int run = 0;  // segments of the current region this CTA has finished (one ticket per run)
+      Region rg;
+      rg.end = -1;
+      int64_t slot = 0;
+      for (int64_t x = X0; x < X1; ++n) {
+        if (x >= rg.end) {
+          rg = region_at<ML>(p, mtb, rg, mfirst, x);
+          slot = p.chunk ? (int64_t)rg.b * mtb.gc[p.ngl] + mtb.gc[rg.g] + (x - rg.start) / p.chunk
+                         : (int64_t)blockIdx.x + rg.b * p.ngl + rg.g;
+        } else {
+          ++slot;  // next chunk of the same region (chunk mode only)
+        }
+        const int64_t seg_end = seg_end_of(p, rg, x, X1);
+        named_bar_sync(kBarSegDone + (n & 1), kHandoff);
+        // every consumer warp's partial of segment n is in shared memory (mbarrier release/
+        // acquire): merge the kCW of them by LSE into this segment's slot
+        const int ridx = rg.b * p.ngl + rg.g;
+        {
+          constexpr int PS = part_stride<D>();
+          constexpr int NE = D / 32;
+          const float *spp = s_part + (size_t)(n & 1) * kCW * G * PS;
+          float *gp = p.part + slot * G * PS;
+          for (int j = 0; j < G; ++j) {
+            float lsv[kCW], mx = -INFINITY;
 #pragma unroll
             for (int w = 0; w < kCW; ++w) {
-              const float wt = ls[w] == -INFINITY ? 0.f : fast_exp2(ls[w] - mx);
-              L += wt;
-#pragma unroll
-              for (int i = 0; i < NE; ++i) O[i] = fmaf(wt, sp[(w * G + j) * PS + lane + 32 * i], O[i]);
+              lsv[w] = spp[(w * G + j) * PS + D];
+              mx = fmaxf(mx, lsv[w]);
             }
-          }
-          const float inv = L > 0.f ? 1.f / L : 0.f;
+            float L = 0.f, O[NE];
 #pragma unroll
-          for (int i = 0; i < NE; ++i) gp[j * PS + lane + 32 * i] = O[i] * inv;
-          if (lane == 0) gp[j * PS + D] = L > 0.f ? mx + __log2f(L) : -INFINITY;
+            for (int i = 0; i < NE; ++i) O[i] = 0.f;
+            if (mx != -INFINITY) {
+#pragma unroll
+              for (int w = 0; w < kCW; ++w) {
+                const float wt = lsv[w] == -INFINITY ? 0.f : fast_exp2(lsv[w] - mx);
+                L += wt;
+#pragma unroll
+                for (int i = 0; i < NE; ++i) O[i] = fmaf(wt, spp[(w * G + j) * PS + lane + 32 * i], O[i]);
+              }
+            }
+            const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+            for (int i = 0; i < NE; ++i) gp[j * PS + lane + 32 * i] = O[i] * inv;
+            if (lane == 0) gp[j * PS + D] = L > 0.f ? mx + __log2f(L) : -INFINITY;
+          }
+          __syncwarp();
         }
-        __syncwarp();
-      }
-      ++run;
-      const bool run_ends = seg_end >= rg.end || seg_end >= X1;
-      int last = 0;
-      if (run_ends && lane == 0) {
-        __threadfence();  // cumulative: orders the partials of the run before the ticket
-        int contributors;
-        if (p.chunk) {
-          contributors = s_gc[rg.g + 1] - s_gc[rg.g];
-        } else {
-          const int64_t c_first = cta_of(p, rg.start, ridx), c_last = cta_of(p, rg.end - 1, ridx);
-          contributors = (int)(c_last - c_first + 1);
+        ++run;
+        const bool run_ends = seg_end >= rg.end || seg_end >= X1;
+        int last = 0;
+        if (run_ends && lane == 0) {
+          __threadfence();  // cumulative: orders the partials of the run before the ticket
+          int contributors;
+          if (p.chunk) {
+            contributors = mtb.gc[rg.g + 1] - mtb.gc[rg.g];
+          } else {
+            const int64_t c_first = cta_of(p, rg.start, ridx), c_last = cta_of(p, rg.end - 1, ridx);
+            contributors = (int)(c_last - c_first + 1);
+          }
+          int *ctr = p.counters + ridx;
+          const int ticket = atomicAdd(ctr, run);
+          if (ticket + run == contributors) {
+            *ctr = 0;  // self-reset for the next launch
+            last = 1;
+          }
         }
-        int *ctr = p.counters + ridx;
-        const int ticket = atomicAdd(ctr, run);
-        if (ticket + run == contributors) {
-          *ctr = 0;  // self-reset for the next launch
-          last = 1;
+        if (run_ends) run = 0;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        stage_next();  // q of segment n+2 into the buffer segment n used
+        if (last) {
+          __threadfence();
+          combine_region_warp<D>(p, mtb.goff, mtb.wing, mtb.gc, ridx, lane);
         }
+        x = seg_end;
       }
-      if (run_ends) run = 0;
-      last = __shfl_sync(0xffffffffu, last, 0);
-      stage_next();  // q of segment n+2 into the buffer segment n used
-      if (last) {
-        __threadfence();
-        combine_region_warp<D>(p, s_goff, s_wing, s_gc, ridx, lane);
-      }
-      x = seg_end;
     }
-    if (lane == 0) TRACE(6);
+    {
+      const MParams &p = p0;
+      if (lane == 0) TRACE(6);
+    }
     return;
   }
 
   // -------------------------------------------------------------- consumers (warps 0..3)
   griddep_wait();
   griddep_launch_dependents();
-  if (tid == 0) TRACE(3);
+  {
+    const MParams &p = p0;
+    if (tid == 0) TRACE(3);
+  }
   const int qr = lane >> 2, qc = lane & 3;  // fragment row (head) / column-pair index
   const int h0 = qr, h1 = qr + 8;           // the two head rows this lane holds
-  const int s = p.n_sink;
+  const int s = p0.n_sink;
   int T = 0, n = 0;
 #ifdef MOA_DEC_TRACE
   int nseg = 0;
 #endif
+  const int G = p0.G;
+  int lc = -1;
+  const MParams *cp = nullptr;
+  Tabs ctb;
+  int64_t X0, X1;
+  Region cfirst;
+  while (enter_layer<ML>(p0, lc, cp, ctb, X0, X1, cfirst, &s_view[ML ? warp : 0], smem_tabs, s_rng, true)) {
+  const MParams &p = *cp;
   // per-region state, recomputed only when a segment starts a new region (a CTA's consecutive
   // chunks of one region reuse it: no global loads or 64-bit divisions between them)
   Region rg;
@@ -566,10 +790,9 @@ __global__ void __launch_bounds__(kThreads, CPS)
   int64_t pos = 0, slot_p = -1;
   int W0 = 0, W1 = 0, pm = 0, slot_r = -1, pos32 = 0, ring_age_max = 0;
   bool ring_live = false, seg_full = false;
-  const int G = p.G;
   for (int64_t x = X0; x < X1; ++n) {
     if (x >= rg.end) {
-      rg = region_of(p, s_goff, s_wing, x);
+      rg = region_at<ML>(p, ctb, rg, cfirst, x);
       pos = p.pos_b ? p.pos_b[rg.b] : p.pos;
       const int32_t *wq = p.win_bq ? p.win_bq + (int64_t)rg.b * p.ngl * G : p.win_q;
       W0 = h0 < G ? wq[rg.g * G + h0] : rg.Wg;
@@ -814,9 +1037,14 @@ __global__ void __launch_bounds__(kThreads, CPS)
     named_bar_arrive(kBarSegDone + (n & 1), kHandoff);
     x = seg_end;
   }
-  if (tid == 0) TRACE(5);
+  }  // layers
+  {
+    const MParams &p = p0;
+    if (tid == 0) TRACE(5);
+  }
 #ifdef MOA_DEC_TRACE
   if (tid == 0) {
+    const MParams &p = p0;
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     TRACE_V(7, (unsigned long long)T | ((unsigned long long)nseg << 40) | ((unsigned long long)smid << 48));
@@ -832,10 +1060,9 @@ int ctas_for(int64_t R, int cps) {
   return (int)(n < by_rows ? n : by_rows);
 }
 
-template <int D, int STAGES, int CPS>
-int launch_v(const DecodeMmaArgs &a, void *stream) {
-  using C = DCfg<D, STAGES>;
-  MParams p;
+// fill the per-call parameters shared by both launchers
+void fill_params(MParams &p, const DecodeMmaArgs &a) {
+  p = MParams{};
   p.q = static_cast<const __nv_bfloat16 *>(a.q);
   p.o = static_cast<__nv_bfloat16 *>(a.o);
   p.q_bs = a.q_bs;
@@ -847,7 +1074,6 @@ int launch_v(const DecodeMmaArgs &a, void *stream) {
   p.vc = static_cast<__nv_bfloat16 *>(a.v_cache);
   p.rows_per_seq = a.rows_per_seq;
   p.R = (int64_t)a.batch * a.rows_per_seq;
-  const int n = ctas_for(p.R, CPS);
   static const int64_t seg_cost = [] {
     const char *e = std::getenv("MOA_DEC_SEG_COST");  // tuning override
     return e ? (int64_t)std::atoll(e) : (int64_t)128;
@@ -872,17 +1098,16 @@ int launch_v(const DecodeMmaArgs &a, void *stream) {
   p.part = a.ws_part;
   p.counters = a.counters;
   p.early = a.early_read;
-#ifdef MOA_DEC_TRACE
-  static int launch_no = 0;
-  p.trace_slot = (launch_no++) & 1;
-#endif
-  const int smem = C::kSmem + 2 * kCW * a.G * part_stride<D>() * 4;
-  cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D, STAGES, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+template <int D, int STAGES, int CPS, bool ML>
+int launch_kernel(const MParams &p, const void *kmap, const void *vmap, const void *kmap16, const void *vmap16,
+                  int n, int G, void *stream) {
+  using C = DCfg<D, STAGES>;
+  const int smem = C::kSmem + 2 * kCW * G * part_stride<D>() * 4;
+  cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D, STAGES, CPS, ML>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return (int)e;
-  const CUtensorMap *km = static_cast<const CUtensorMap *>(a.kmap);
-  const CUtensorMap *vm = static_cast<const CUtensorMap *>(a.vmap);
-  const CUtensorMap *km16 = static_cast<const CUtensorMap *>(a.kmap16);
-  const CUtensorMap *vm16 = static_cast<const CUtensorMap *>(a.vmap16);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)n);
   cfg.blockDim = dim3(kThreads);
@@ -893,9 +1118,49 @@ int launch_v(const DecodeMmaArgs &a, void *stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, decode_mma_kernel<D, STAGES, CPS>, *km, *vm, *km16, *vm16, p);
+  static const CUtensorMap zero_map{};  // ML: the maps come from the layer descriptors
+  const CUtensorMap &km = kmap ? *static_cast<const CUtensorMap *>(kmap) : zero_map;
+  const CUtensorMap &vm = vmap ? *static_cast<const CUtensorMap *>(vmap) : zero_map;
+  const CUtensorMap &km16 = kmap16 ? *static_cast<const CUtensorMap *>(kmap16) : zero_map;
+  const CUtensorMap &vm16 = vmap16 ? *static_cast<const CUtensorMap *>(vmap16) : zero_map;
+  e = cudaLaunchKernelEx(&cfg, decode_mma_kernel<D, STAGES, CPS, ML>, km, vm, km16, vm16, p);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
+}
+
+template <int D, int STAGES, int CPS>
+int launch_v(const DecodeMmaArgs &a, void *stream) {
+  MParams p;
+  fill_params(p, a);
+#ifdef MOA_DEC_TRACE
+  static int launch_no = 0;
+  p.trace_slot = (launch_no++) & 1;
+#endif
+  return launch_kernel<D, STAGES, CPS, false>(p, a.kmap, a.vmap, a.kmap16, a.vmap16, ctas_for(p.R, CPS), a.G,
+                                              stream);
+}
+
+template <int D, int STAGES, int CPS>
+int launch_layers_v(const DecodeLayersArgs &l, void *stream) {
+  MParams p;
+  fill_params(p, l.a);
+  // early streaming only when the host established that the stream predecessor does not
+  // append to these layers (a previous layer chunk of the same token)
+  p.ml = l.d_layers;
+  p.nl = l.n_layers;
+  p.q_ls = l.q_ls;
+  p.o_ls = l.o_ls;
+  p.kvn_ls = l.kvn_ls;
+  p.lse_ls = l.lse_ls;
+  p.part_ls = l.part_ls;
+  // balanced split: the ticket count of a region is the CTAs between its first and last row,
+  // so no CTA may get an empty range in any layer: n <= every layer's total cost
+  int64_t n = ctas_for(l.max_rows, CPS);
+  if (!p.chunk) {
+    const int64_t min_ctot = l.min_rows + p.seg_cost * ((int64_t)p.batch * p.ngl - 1);
+    if (n > min_ctot) n = min_ctot;
+  }
+  return launch_kernel<D, STAGES, CPS, true>(p, nullptr, nullptr, nullptr, nullptr, (int)n, l.a.G, stream);
 }
 
 template <int D>
@@ -932,6 +1197,11 @@ extern "C" int moa_debug_decode_trace(void *host, size_t bytes) {
 int launch_decode_mma(const DecodeMmaArgs &a, void *stream) {
   if (a.d == 128) return launch_d<128>(a, stream);
   return launch_d<64>(a, stream);
+}
+
+int launch_decode_mma_layers(const DecodeLayersArgs &l, void *stream) {
+  if (l.a.d == 128) return launch_layers_v<128, 2, 2>(l, stream);
+  return launch_layers_v<64, 6, 2>(l, stream);
 }
 
 }  // namespace moa

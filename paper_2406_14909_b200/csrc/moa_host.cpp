@@ -217,6 +217,7 @@ moa_status moa_destroy(moa_ctx *ctx) {
   {
     DeviceGuard dg(ctx->device);
     for (auto &p : ctx->layers) free_tables(p);
+    if (ctx->d_ml) cudaFree(ctx->d_ml);
   }
   delete ctx;
   return MOA_OK;
@@ -399,6 +400,7 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
     free_tables(p);
   }
   p = np;
+  ctx->ml_dirty = true;
   return ok();
 }
 
@@ -407,6 +409,7 @@ moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq
   moa_status st = check_layer(ctx, layer, true);
   if (st) return st;
   LayerPlan &p = ctx->layers[layer];
+  ctx->ml_dirty = true;
   if (batch == 0) {
     DeviceGuard dg(ctx->device);
     free_ragged(p);
@@ -572,6 +575,7 @@ moa_status moa_bind_layer_cache(moa_ctx *ctx, int layer, void *k_cache, void *v_
   p.next_pos = 0;
   p.maps_ok = false;
   ctx->last_cache_write = moa_ctx::kAllLayers;
+  ctx->ml_dirty = true;
   if (ctx->device >= 0) {
     // rows not yet reached by the sequence must hold finite values: the tensor-core decode
     // multiplies masked rows by a zero probability, and 0 * NaN would poison the sum
@@ -883,6 +887,157 @@ moa_status moa_decode_step_fused_ragged(moa_ctx *ctx, int layer, const void *q, 
                        batch, 0, scale, lse_out, workspace, ws_bytes, stream, true, pos);
 }
 
+// ---- cross-layer decode ------------------------------------------------
+// Device image: DecodeLayerDesc[L] then 4 CUtensorMap per layer (128-byte aligned).  Layers that
+// are not set or not bound get a zeroed descriptor (the launch checks its layers).
+moa_status moa_prepare_layers(moa_ctx *ctx) {
+  if (!ctx) return fail(MOA_ERR_INVALID_ARG, "ctx is NULL");
+  if (ctx->device < 0) return fail(MOA_ERR_STATE, "planning context (device -1) cannot launch");
+  if (ctx->dtype != MOA_BF16) return fail(MOA_ERR_UNSUPPORTED, "cross-layer decode is bf16 only");
+  const size_t desc_bytes = align256((size_t)ctx->L * sizeof(moa::DecodeLayerDesc));
+  const size_t total = desc_bytes + (size_t)ctx->L * 4 * 128;
+  DeviceGuard dg(ctx->device);
+  if (!ctx->d_ml) {
+    cudaError_t e = cudaMalloc(&ctx->d_ml, total);
+    if (e != cudaSuccess) {
+      ctx->d_ml = nullptr;
+      return cuda_fail(e, "cudaMalloc(cross-layer descriptors)");
+    }
+  }
+  std::vector<unsigned char> img(total, 0);
+  auto *desc = reinterpret_cast<moa::DecodeLayerDesc *>(img.data());
+  unsigned char *dmaps = static_cast<unsigned char *>(ctx->d_ml) + desc_bytes;
+  for (int l = 0; l < ctx->L; ++l) {
+    const LayerPlan &p = ctx->layers[l];
+    if (!p.set || !p.k_cache || !p.maps_ok) continue;
+    moa::DecodeLayerDesc &d = desc[l];
+    d.maps = dmaps + (size_t)l * 4 * 128;
+    d.kc = p.k_cache;
+    d.vc = p.v_cache;
+    d.g_off = p.d_g_off;
+    d.win_g = p.d_win_g;
+    d.win_q = p.d_win_q;
+    d.gc_off = p.d_gc_off;
+    d.counters = p.d_counters;
+    d.rows_per_seq = p.rows_per_seq;
+    d.dec_cps = p.dec_cps;
+    unsigned char *m = img.data() + desc_bytes + (size_t)l * 4 * 128;
+    std::memcpy(m, p.kmap, 128);
+    std::memcpy(m + 128, p.vmap, 128);
+    std::memcpy(m + 256, p.kmap16, 128);
+    std::memcpy(m + 384, p.vmap16, 128);
+  }
+  if (img != ctx->ml_image) {
+    // launches still in flight may read the old image
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_ml, img.data(), total, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "upload of the cross-layer descriptors");
+    ctx->ml_image = std::move(img);
+  }
+  ctx->ml_dirty = false;
+  return ok();
+}
+
+moa_status moa_decode_step_fused_layers(moa_ctx *ctx, int layer0, int n_layers, const void *q, const void *k_new,
+                                        const void *v_new, void *o, int64_t q_layer_stride,
+                                        int64_t kv_layer_stride, int64_t o_layer_stride, int64_t q_batch_stride,
+                                        int64_t kv_batch_stride, int64_t o_batch_stride, int batch, int64_t pos,
+                                        float scale, float *lse_out, int64_t lse_layer_stride, void *workspace,
+                                        size_t ws_bytes, moa_stream_t stream) {
+  if (!ctx) return fail(MOA_ERR_INVALID_ARG, "ctx is NULL");
+  if (n_layers < 1 || layer0 < 0 || layer0 + n_layers > ctx->L)
+    return fail(MOA_ERR_INVALID_ARG, "layers [%d, %d) not in [0, %d)", layer0, layer0 + n_layers, ctx->L);
+  if (ctx->dtype != MOA_BF16) return fail(MOA_ERR_UNSUPPORTED, "cross-layer decode is bf16 only");
+  if (ctx->ngl > 128) return fail(MOA_ERR_UNSUPPORTED, "more than 128 local kv-groups");
+  if (!q || !o || !k_new || !v_new) return fail(MOA_ERR_INVALID_ARG, "q/k_new/v_new/o must be non-NULL");
+  const int64_t d = ctx->d;
+  if (q_batch_stride < ctx->nql * d || o_batch_stride < ctx->nql * d || kv_batch_stride < ctx->ngl * d)
+    return fail(MOA_ERR_SHAPE, "batch strides smaller than local heads * head_dim");
+  // inputs may be shared by the layers (layer stride 0); outputs may not overlap
+  auto bad_in = [&](int64_t ls, int64_t bs) { return ls != 0 && ls < (int64_t)batch * bs; };
+  if (n_layers > 1 && (bad_in(q_layer_stride, q_batch_stride) || bad_in(kv_layer_stride, kv_batch_stride) ||
+                       o_layer_stride < (int64_t)batch * o_batch_stride ||
+                       (lse_out && lse_layer_stride < (int64_t)batch * ctx->nql)))
+    return fail(MOA_ERR_SHAPE, "layer strides: inputs 0 or >= one layer's batch, outputs >= one layer's batch");
+  if (q_layer_stride < 0 || kv_layer_stride < 0) return fail(MOA_ERR_SHAPE, "negative layer stride");
+  const int64_t es = 2;
+  if (!aligned16(q) || !aligned16(o) || !aligned16(k_new) || !aligned16(v_new) ||
+      ((q_batch_stride | o_batch_stride | kv_batch_stride | q_layer_stride | o_layer_stride | kv_layer_stride) * es) % 16)
+    return fail(MOA_ERR_INVALID_ARG, "decode pointers and strides must be 16-byte aligned");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(MOA_ERR_INVALID_ARG, "scale must be finite > 0");
+  int n_sink = -1;
+  int64_t max_rows = 0, min_rows = INT64_MAX;
+  size_t per_layer = 256;
+  for (int l = layer0; l < layer0 + n_layers; ++l) {
+    moa_status st = check_launch_common(ctx, l, batch);
+    if (st) return st;
+    const LayerPlan &p = ctx->layers[l];
+    if (p.rag_batch) return fail(MOA_ERR_STATE, "layer %d is ragged", l);
+    if (!p.maps_ok) return fail(MOA_ERR_STATE, "layer %d cache has no tensor maps (re-bind the cache)", l);
+    if (pos != p.next_pos || pos < 0)
+      return fail(MOA_ERR_STATE, "decode pos=%lld but layer %d expects %lld", (long long)pos, l,
+                  (long long)p.next_pos);
+    if (n_sink >= 0 && p.n_sink != n_sink) return fail(MOA_ERR_STATE, "layers disagree on the sink count");
+    n_sink = p.n_sink;
+    max_rows = std::max<int64_t>(max_rows, (int64_t)batch * p.rows_per_seq);
+    min_rows = std::min<int64_t>(min_rows, (int64_t)batch * p.rows_per_seq);
+    DeviceGuard dg(ctx->device);
+    per_layer = std::max(per_layer, moa::decode_mma_ws_bytes(batch, ctx->ngl, ctx->G, ctx->d, p.dec_cps));
+  }
+  if (!workspace || ws_bytes < per_layer * n_layers)
+    return fail(MOA_ERR_OOM, "workspace of %zu bytes < %zu needed (%d layers)", ws_bytes, per_layer * n_layers,
+                n_layers);
+  if (!aligned16(workspace)) return fail(MOA_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
+  if (ctx->ml_dirty) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing((cudaStream_t)stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+      return fail(MOA_ERR_STATE, "call moa_prepare_layers before capturing a cross-layer decode");
+    moa_status st = moa_prepare_layers(ctx);
+    if (st) return st;
+  }
+  const LayerPlan &p0 = ctx->layers[layer0];
+  DeviceGuard dg(ctx->device);
+  moa::DecodeLayersArgs la{};
+  moa::DecodeMmaArgs &m = la.a;
+  m.q = q; m.o = o; m.q_bs = q_batch_stride; m.o_bs = o_batch_stride;
+  m.k_new = k_new; m.v_new = v_new; m.kv_bs = kv_batch_stride;
+  m.k_cache = p0.k_cache; m.v_cache = p0.v_cache; m.rows_per_seq = p0.rows_per_seq;
+  m.d_g_off = p0.d_g_off; m.d_win_g = p0.d_win_g; m.d_win_q = p0.d_win_q;
+  m.ngl = ctx->ngl; m.G = ctx->G; m.d = ctx->d; m.n_sink = n_sink; m.batch = batch;
+  m.pos = pos; m.scale = scale; m.lse = lse_out; m.ws_part = static_cast<float *>(workspace);
+  m.counters = p0.d_counters;
+  m.chunk = ctx->dec_chunk;
+  m.chunks_per_seq = p0.dec_cps;
+  m.d_gc_off = p0.d_gc_off;
+  m.early_read = 0;
+  la.q_ls = q_layer_stride;
+  la.o_ls = o_layer_stride;
+  la.kvn_ls = kv_layer_stride;
+  la.lse_ls = lse_layer_stride;
+  la.part_ls = (int64_t)(per_layer / 4);
+  la.max_rows = max_rows;
+  la.min_rows = min_rows;
+  // at most kMaxLayersPerLaunch layers per launch (the kernel keeps a per-layer table per CTA)
+  constexpr int kMaxLayersPerLaunch = 32;
+  for (int c0 = 0; c0 < n_layers; c0 += kMaxLayersPerLaunch) {
+    moa::DecodeLayersArgs lc = la;
+    lc.d_layers = reinterpret_cast<const moa::DecodeLayerDesc *>(ctx->d_ml) + layer0 + c0;
+    lc.n_layers = std::min(kMaxLayersPerLaunch, n_layers - c0);
+    lc.a.q = static_cast<const char *>(q) + c0 * q_layer_stride * es;
+    lc.a.o = static_cast<char *>(o) + c0 * o_layer_stride * es;
+    lc.a.k_new = static_cast<const char *>(k_new) + c0 * kv_layer_stride * es;
+    lc.a.v_new = static_cast<const char *>(v_new) + c0 * kv_layer_stride * es;
+    lc.a.lse = lse_out ? lse_out + c0 * lse_layer_stride : nullptr;
+    lc.a.ws_part = static_cast<float *>(workspace) + c0 * la.part_ls;
+    lc.a.early_read = c0 > 0 && early_read_enabled();  // predecessor: the previous chunk (other layers)
+    int e = moa::launch_decode_mma_layers(lc, stream);
+    if (e) return cuda_fail((cudaError_t)e, "cross-layer decode launch");
+  }
+  for (int l = layer0; l < layer0 + n_layers; ++l) ctx->layers[l].next_pos = pos + 1;
+  ctx->last_cache_write = moa_ctx::kAllLayers;
+  return ok();
+}
+
 moa_status moa_set_decode_split(moa_ctx *ctx, int chunk_rows) {
   if (!ctx) return fail(MOA_ERR_INVALID_ARG, "ctx is NULL");
   if (chunk_rows != 0 && (chunk_rows < 64 || chunk_rows > (1 << 20) || chunk_rows % 64))
@@ -890,6 +1045,7 @@ moa_status moa_set_decode_split(moa_ctx *ctx, int chunk_rows) {
   for (const auto &p : ctx->layers)
     if (p.rag_batch) return fail(MOA_ERR_STATE, "set the decode split before moa_set_ragged");
   ctx->dec_chunk = chunk_rows;
+  ctx->ml_dirty = true;
   for (auto &p : ctx->layers) {
     if (!p.set) continue;
     p.dec_cps = 0;

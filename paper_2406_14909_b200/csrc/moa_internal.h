@@ -197,6 +197,11 @@ struct moa_ctx {
   int last_cache_write = kAllLayers;
   // bf16 decode split: rows per rank-invariant chunk (0: balanced row split, not rank-invariant)
   int dec_chunk = 0;
+  // cross-layer decode: device image of DecodeLayerDesc[L] + 4 tensor maps per layer
+  // (moa_prepare_layers); stale after set_spans / bind / set_decode_split / set_ragged
+  void *d_ml = nullptr;
+  std::vector<unsigned char> ml_image;
+  bool ml_dirty = true;
 };
 
 namespace moa {
@@ -296,6 +301,30 @@ struct DecodeMmaArgs {
   const int32_t *d_gc_off;     // first chunk of each local group inside a sequence [ngl + 1]
 };
 int launch_decode_mma(const DecodeMmaArgs &a, void *stream);
+
+// Cross-layer decode (moa_decode_step_fused_layers): one launch streams
+// the caches of n consecutive layers.  The per-layer static data lives in a device array of
+// these (ctx->d_ml, rebuilt by moa_prepare_layers); the per-call data (q/o/k_new/v_new bases
+// and layer strides, pos, scale) comes with the launch.
+struct DecodeLayerDesc {
+  const void *maps;              // 4 CUtensorMap (kmap, vmap, kmap16, vmap16), device copies
+  void *kc, *vc;                 // the layer's cache
+  const int64_t *g_off;
+  const int32_t *win_g, *win_q, *gc_off;
+  int *counters;
+  int64_t rows_per_seq;
+  int dec_cps;
+  int pad_;
+};
+struct DecodeLayersArgs {
+  DecodeMmaArgs a;               // layer 0 of the range (tables/maps ignored) + per-call fields
+  const DecodeLayerDesc *d_layers;  // [n] (device), already offset to the first layer
+  int n_layers;
+  int64_t q_ls, o_ls, kvn_ls, lse_ls, part_ls;  // layer strides (elements; part in floats)
+  int64_t max_rows;              // max over the layers of batch * rows_per_seq (grid size)
+  int64_t min_rows;              // min over the layers (balanced split: no CTA may get an empty range)
+};
+int launch_decode_mma_layers(const DecodeLayersArgs &a, void *stream);
 size_t decode_mma_ws_bytes(int batch, int ngl, int G, int d, int chunks_per_seq);
 
 // attention influence of the profiling stage (kernels/influence.cu)

@@ -249,8 +249,9 @@ class MoAContext:
         self.bind_cache(k, v, batch)
         return k, v
 
-    def alloc_workspace(self, batch: int) -> torch.Tensor:
-        return torch.empty(self.workspace_bytes(batch), dtype=torch.uint8,
+    def alloc_workspace(self, batch: int, n_layers: int = 1) -> torch.Tensor:
+        """Decode workspace; n_layers > 1 sizes it for decode_step_fused_layers."""
+        return torch.empty(self.workspace_bytes(batch) * n_layers, dtype=torch.uint8,
                            device=torch.device("cuda", self.device))
 
     # ---- launches ------------------------------------------------------------------------
@@ -301,6 +302,21 @@ class MoAContext:
                                              _ptr(lse), _ptr(workspace),
                                              workspace.numel() * workspace.element_size(), _stream(stream)),
               "moa_decode_step_fused")
+
+    def prepare_layers(self):
+        """moa_prepare_layers: upload the cross-layer descriptors (before graph capture)."""
+        check(self.lib.moa_prepare_layers(self.ctx), "moa_prepare_layers")
+
+    def decode_step_fused_layers(self, layer0: int, q, k_new, v_new, o, pos: int, scale: float, workspace,
+                                 lse=None, stream=None):
+        """moa_decode_step_fused_layers: q/o [n, B, Hq, d], k_new/v_new [n, B, Hkv, d] (layer-major),
+        one launch for layers [layer0, layer0 + n); workspace >= n * workspace_bytes(B)."""
+        n, B = q.shape[0], q.shape[1]
+        check(self.lib.moa_decode_step_fused_layers(
+            self.ctx, layer0, n, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(o), q.stride(0), k_new.stride(0),
+            o.stride(0), q.stride(1), k_new.stride(1), o.stride(1), B, int(pos), float(scale), _ptr(lse),
+            lse.stride(0) if lse is not None else 0, _ptr(workspace), workspace.numel() * workspace.element_size(),
+            _stream(stream)), "moa_decode_step_fused_layers")
 
     def decode_step_fused_ragged(self, layer: int, q, k_new, v_new, o, pos, scale: float, workspace, lse=None,
                                  stream=None):

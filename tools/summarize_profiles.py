@@ -86,20 +86,25 @@ def main(rnd):
         ms = raw_metrics(rep)
         with open(os.path.join(out_dir, f"{rnd}_{kind}_full.txt"), "w") as f:
             f.write(f"# {rnd}: ncu --set full --clock-control none, {kind} kernel "
-                    f"(tools/prof_run.py {kind}, C2 layers 12-15)\n")
+                    f"(tools/prof_run.py, C2)\n")
             for m in ms:
                 f.write(f"kernel: {m.get('Kernel Name', '')[:120]}\n")
                 for k in KEYS:
                     f.write(f"  {k:<70} {m.get(k, 'n/a'):>16} {m['_units'].get(k, '')}\n")
         if kind == "decode":
             m = ms[0]
-            rd = float(m["dram__bytes_read.sum"]) * (1e6 if m["_units"]["dram__bytes_read.sum"] == "Mbyte" else 1)
-            wr = float(m["dram__bytes_write.sum"]) * (1e6 if m["_units"]["dram__bytes_write.sum"] == "Mbyte" else 1)
-            alg = c2_decode_bytes(12)
+            unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            rd = float(m["dram__bytes_read.sum"]) * unit[m["_units"]["dram__bytes_read.sum"]]
+            wr = float(m["dram__bytes_write.sum"]) * unit[m["_units"]["dram__bytes_write.sum"]]
+            import re
+            cross = re.search(r"decode_mma_kernel<\d+, \d+, \d+, (1|true)>", m.get("Kernel Name", "")) is not None
+            alg = sum(c2_decode_bytes(l) for l in range(32)) if cross else c2_decode_bytes(12)
             with open(os.path.join(out_dir, "decode_traffic.json"), "w") as f:
                 json.dump({"round": rnd, "bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                            "algorithmic_bytes_same_launch": alg, "traffic_over_algorithmic": (rd + wr) / alg,
-                           "launch": "decode_mma_kernel, C2 layer 12 (tools/prof_run.py decode), batch 8",
+                           "launch": ("cross-layer decode_mma_kernel, all 32 C2 layers, token N+1 (tools/prof_run.py "
+                                      "layers), batch 8") if cross else
+                                     "decode_mma_kernel, C2 layer 12 (tools/prof_run.py decode), batch 8",
                            "source": f"gpurun_out/{rnd}_decode_full.ncu-rep"}, f, indent=1)
             print("decode traffic", rd + wr, "algorithmic", alg, (rd + wr) / alg)
 
