@@ -510,6 +510,38 @@ def run_kv_shard(rank, world, dev, scale, T=64):
     phase(True)
     with_ag = phase(True)
     compute = phase(False)
+    fused, fused_err = None, None
+    if world > 1:
+        # fused head gather: the decode epilogue stores into every rank's symmetric-memory
+        # buffer over NVLink; layer l+1 waits on this rank's counter of layer l
+        try:
+            pg = mdist.PeerGather.from_symmetric_memory(ctx, shard, G, CFG.hkv, L, B, CFG.hq, d, dev)
+
+            def fused_phase():
+                for l in range(L):
+                    ctx.cache_fill(l, kl, vl)
+                torch.cuda.synchronize()
+                torch.distributed.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for t in range(T):
+                    ql = mdist.local_slice_q(qd[t], shard, G)
+                    kt, vt = mdist.local_slice_kv(kd[t], shard), mdist.local_slice_kv(vd[t], shard)
+                    for l in range(L):
+                        ctx.decode_step_fused(l, ql, kt, vt, od, N + t, scale, ws)
+                        pg.wait(l)                  # layer l+1 consumes every rank's heads
+                    pg.next_token()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                x = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+                torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+                return x.item()
+
+            fused_phase()
+            fused = fused_phase()
+            ctx.set_peer_outputs([], [], 0, 0, 0)
+        except Exception as exc:  # reported; the NCCL numbers above stand
+            fused_err = f"{type(exc).__name__}: {exc}"[:300]
     loads = [mdist.shard_cost(sh, cost) for sh in shards]
     return {"mode": f"kv-groups over {world} rank(s), cost-balanced contiguous ranges "
                     f"{[(sh.g0, sh.g1) for sh in shards]}, same batch of {B}",
@@ -518,6 +550,11 @@ def run_kv_shard(rank, world, dev, scale, T=64):
             "decode_tokens_per_s": B * T / (with_ag / 1e3),
             "decode_tokens_per_s_no_allgather": B * T / (compute / 1e3),
             "allgather_us_per_layer": (with_ag - compute) * 1e3 / (T * L),
+            "fused_gather": ({"decode_tokens_per_s": B * T / (fused / 1e3),
+                              "gather_us_per_layer": (fused - compute) * 1e3 / (T * L),
+                              "note": "moa_set_peer_outputs: decode epilogue P2P-stores every head row into "
+                                      "every rank's symmetric-memory buffer, per-layer counters + moa_wait_flag"}
+                             if fused is not None else {"error": fused_err} if fused_err else None),
             "tokens": T, "scaling": "strong",
             "note": "NCCL all_gather_into_tensor of each layer's head outputs (torch.distributed, own stream, "
                     "preallocated), serialised before the next layer; device-timed, max over ranks"}

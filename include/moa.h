@@ -283,6 +283,35 @@ moa_status moa_decode_step_fused_layers(moa_ctx *ctx, int layer0, int n_layers, 
                                         size_t ws_bytes, moa_stream_t stream);
 
 /*
+ * Fused head-output all-gather for kv-group sharded decode.
+ * Heads are masked independently, so a rank serving kv-groups [g0, g1)
+ * owns complete head outputs; the next layer needs every head on every rank.  With peer
+ * outputs installed, every bf16 decode launch of this context (single-layer, ragged and
+ * cross-layer) writes each finished head row, from the combine epilogue that produced it,
+ * into all n_peers destination buffers as well as into o, then releases it with one
+ * system-scope atomic increment of the destination's counter of that layer -- the
+ * all-gather becomes P2P stores over NVLink overlapped with the rest of the decode instead
+ * of a separate collective after it.
+ *   peer_o[k]      device address (as mapped on THIS device: a peer-mapped or symmetric-memory
+ *                  buffer) of destination k: bf16 [L][B][Hq_total][d]; layer l, sequence b,
+ *                  global q-head h at  l * peer_layer_stride + b * peer_batch_stride + h * d
+ *   peer_flags[k]  device address of destination k's uint32 counters [L]; every region
+ *                  (sequence, local kv-group) of layer l adds 1 when its G heads are written,
+ *                  so one token step of every rank adds B * Hkv_total to each counter
+ *   head0          global index of this context's first local q-head (g0 * G)
+ * n_peers = 0 switches it off.  The arrays are copied (at most 16 destinations); the call
+ * synchronises the device.  Unsupported for fp32 contexts.
+ */
+moa_status moa_set_peer_outputs(moa_ctx *ctx, int n_peers, void *const *peer_o, unsigned int *const *peer_flags,
+                                int64_t peer_batch_stride, int64_t peer_layer_stride, int head0);
+
+/* Stream-ordered wait: the next work on `stream` starts once the uint32 at `flag` (device
+ * memory, any peer's writes visible at system scope) has reached `expected` (counters only
+ * grow; compared modulo 2^32).  One tiny kernel; CUDA-graph capturable.  A wait still
+ * unsatisfied after 10 s traps (the next call reports MOA_ERR_CUDA) rather than hang. */
+moa_status moa_wait_flag(const unsigned int *flag, unsigned int expected, moa_stream_t stream);
+
+/*
  * Append + decode of a ragged batch: moa_decode_step_fused where sequence b is at its
  * own position pos[b] (a6 + a7 + a8 per sequence, PAPER.md:704 cache replacement).
  *   pos   DEVICE int64 [batch], caller-owned, 8-byte aligned, read by the kernel after its

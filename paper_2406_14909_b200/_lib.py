@@ -48,6 +48,8 @@ _SIGS = [
                                       c_float, _P, _P, c_size_t, _P]),
     ("moa_advance_pos", c_int, [_P, c_int, c_int64, _P]),
     ("moa_prepare_layers", c_int, [_P]),
+    ("moa_set_peer_outputs", c_int, [_P, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int64, c_int64, c_int]),
+    ("moa_wait_flag", c_int, [_P, ctypes.c_uint, _P]),
     ("moa_decode_step_fused_layers", c_int, [_P, c_int, c_int, _P, _P, _P, _P, c_int64, c_int64, c_int64, c_int64,
                                              c_int64, c_int64, c_int, c_int64, c_float, _P, c_int64, _P, c_size_t,
                                              _P]),

@@ -103,6 +103,10 @@ struct MParams {
   float *part;
   int *counters;
   int early;  // 1: the producer may stream the cache before the stream predecessor completes
+  // fused head-output all-gather (moa_set_peer_outputs; n_peers = 0: off)
+  const PeerOut *peers;
+  int n_peers, peer_head0, layer;
+  int64_t peer_bs, peer_ls;
   // cross-layer launch (ML kernels only): per-layer tables and per-call layer strides
   const DecodeLayerDesc *ml;
   int nl;
@@ -325,10 +329,31 @@ __device__ __forceinline__ void combine_region_warp(const MParams &p, const int6
       mx = nm;
     }
     const float inv = L > 0.f ? 1.f / L : 0.f;
+    __nv_bfloat16 ov[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) ov[i] = __float2bfloat16_rn(O[i] * inv);
     __nv_bfloat16 *ob = p.o + (int64_t)b * p.o_bs + (int64_t)(g * G + j) * D;
 #pragma unroll
-    for (int i = 0; i < NE; ++i) ob[lane + 32 * i] = __float2bfloat16_rn(O[i] * inv);
+    for (int i = 0; i < NE; ++i) ob[lane + 32 * i] = ov[i];
+    // fused head-output all-gather (moa_set_peer_outputs): the same bits into every
+    // destination's [B, Hq, d] buffer of this layer, at this context's global head offset
+    for (int k = 0; k < p.n_peers; ++k) {
+      __nv_bfloat16 *pb = static_cast<__nv_bfloat16 *>(p.peers[k].o) + (int64_t)p.layer * p.peer_ls +
+                          (int64_t)b * p.peer_bs + (int64_t)(p.peer_head0 + g * G + j) * D;
+#pragma unroll
+      for (int i = 0; i < NE; ++i) pb[lane + 32 * i] = ov[i];
+    }
     if (p.lse && lane == 0) p.lse[(int64_t)b * p.ngl * G + g * G + j] = L > 0.f ? (mx + __log2f(L)) * kLn2 : -INFINITY;
+  }
+  if (p.n_peers) {
+    // release: every lane's stores of this region, then one arrival on each destination's
+    // counter of this layer (a consumer waits with moa_wait_flag)
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_system();
+      for (int k = 0; k < p.n_peers; ++k) atomicAdd_system(p.peers[k].flag + p.layer, 1u);
+    }
   }
 }
 
@@ -369,6 +394,7 @@ __device__ __forceinline__ void build_view(const MParams &b, int l, MParams *out
   }
   if (b.lse) v.lse = b.lse + l * b.lse_ls;
   v.part = b.part + l * b.part_ls;
+  v.layer = b.layer + l;
   v.kc = static_cast<__nv_bfloat16 *>(dl.kc);
   v.vc = static_cast<__nv_bfloat16 *>(dl.vc);
   v.g_off = dl.g_off;
@@ -1098,6 +1124,12 @@ void fill_params(MParams &p, const DecodeMmaArgs &a) {
   p.part = a.ws_part;
   p.counters = a.counters;
   p.early = a.early_read;
+  p.peers = static_cast<const PeerOut *>(a.peers);
+  p.n_peers = a.n_peers;
+  p.peer_head0 = a.peer_head0;
+  p.peer_bs = a.peer_bs;
+  p.peer_ls = a.peer_ls;
+  p.layer = a.layer;
 }
 
 template <int D, int STAGES, int CPS, bool ML>
@@ -1197,6 +1229,30 @@ extern "C" int moa_debug_decode_trace(void *host, size_t bytes) {
 int launch_decode_mma(const DecodeMmaArgs &a, void *stream) {
   if (a.d == 128) return launch_d<128>(a, stream);
   return launch_d<64>(a, stream);
+}
+
+namespace {
+__global__ void wait_flag_kernel(const unsigned *flag, unsigned expected) {
+  // counters only grow (modulo 2^32): wait until flag - expected >= 0 in wrapped arithmetic.
+  // A wait that outlives 10 s traps (a sticky error the next library call reports) instead of
+  // hanging the device when a peer never arrives.
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - expected) >= 0) break;
+    __nanosleep(64);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10000000000ull) __trap();
+  }
+}
+}  // namespace
+
+int launch_wait_flag(const unsigned *flag, unsigned expected, void *stream) {
+  wait_flag_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag, expected);
+  return (int)cudaGetLastError();
 }
 
 int launch_decode_mma_layers(const DecodeLayersArgs &l, void *stream) {

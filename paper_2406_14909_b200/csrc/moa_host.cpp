@@ -218,6 +218,7 @@ moa_status moa_destroy(moa_ctx *ctx) {
     DeviceGuard dg(ctx->device);
     for (auto &p : ctx->layers) free_tables(p);
     if (ctx->d_ml) cudaFree(ctx->d_ml);
+    if (ctx->d_peers) cudaFree(ctx->d_peers);
   }
   delete ctx;
   return MOA_OK;
@@ -835,12 +836,15 @@ static moa_status decode_common(moa_ctx *ctx, int layer, const void *q, const vo
     m.d_gc_off = p.d_gc_off;
     m.early_read = early_read_enabled() && ctx->last_cache_write != layer &&
                    ctx->last_cache_write != moa_ctx::kAllLayers;
+    m.peers = ctx->d_peers; m.n_peers = ctx->n_peers; m.peer_head0 = ctx->peer_head0;
+    m.peer_bs = ctx->peer_bs; m.peer_ls = ctx->peer_ls; m.layer = layer;
     int e = moa::launch_decode_mma(m, stream);
     if (e) return cuda_fail((cudaError_t)e, "decode launch");
     if (fused && !d_pos) p.next_pos = pos + 1;
     ctx->last_cache_write = fused ? layer : -1;
     return ok();
   }
+  if (ctx->n_peers) return fail(MOA_ERR_UNSUPPORTED, "peer outputs need the bf16 decode");
   moa::DecodeArgs a{};
   a.q = q; a.o = o; a.q_batch_stride = q_batch_stride; a.o_batch_stride = o_batch_stride;
   a.k_new = fused ? k_new : nullptr; a.v_new = fused ? v_new : nullptr; a.kv_batch_stride = kv_batch_stride;
@@ -1010,6 +1014,8 @@ moa_status moa_decode_step_fused_layers(moa_ctx *ctx, int layer0, int n_layers, 
   m.chunks_per_seq = p0.dec_cps;
   m.d_gc_off = p0.d_gc_off;
   m.early_read = 0;
+  m.peers = ctx->d_peers; m.n_peers = ctx->n_peers; m.peer_head0 = ctx->peer_head0;
+  m.peer_bs = ctx->peer_bs; m.peer_ls = ctx->peer_ls; m.layer = layer0;
   la.q_ls = q_layer_stride;
   la.o_ls = o_layer_stride;
   la.kvn_ls = kv_layer_stride;
@@ -1030,11 +1036,53 @@ moa_status moa_decode_step_fused_layers(moa_ctx *ctx, int layer0, int n_layers, 
     lc.a.lse = lse_out ? lse_out + c0 * lse_layer_stride : nullptr;
     lc.a.ws_part = static_cast<float *>(workspace) + c0 * la.part_ls;
     lc.a.early_read = c0 > 0 && early_read_enabled();  // predecessor: the previous chunk (other layers)
+    lc.a.layer = layer0 + c0;
     int e = moa::launch_decode_mma_layers(lc, stream);
     if (e) return cuda_fail((cudaError_t)e, "cross-layer decode launch");
   }
   for (int l = layer0; l < layer0 + n_layers; ++l) ctx->layers[l].next_pos = pos + 1;
   ctx->last_cache_write = moa_ctx::kAllLayers;
+  return ok();
+}
+
+// ---- fused head-output all-gather ----------------------------------
+moa_status moa_set_peer_outputs(moa_ctx *ctx, int n_peers, void *const *peer_o, unsigned int *const *peer_flags,
+                                int64_t peer_batch_stride, int64_t peer_layer_stride, int head0) {
+  if (!ctx) return fail(MOA_ERR_INVALID_ARG, "ctx is NULL");
+  if (ctx->device < 0) return fail(MOA_ERR_STATE, "planning context (device -1) cannot launch");
+  if (n_peers < 0 || n_peers > 16) return fail(MOA_ERR_INVALID_ARG, "n_peers %d not in [0, 16]", n_peers);
+  DeviceGuard dg(ctx->device);
+  if (n_peers == 0) {
+    ctx->n_peers = 0;
+    return ok();
+  }
+  if (ctx->dtype != MOA_BF16) return fail(MOA_ERR_UNSUPPORTED, "peer outputs need the bf16 decode");
+  if (!peer_o || !peer_flags) return fail(MOA_ERR_INVALID_ARG, "peer pointer arrays are NULL");
+  if (head0 < 0 || peer_batch_stride < (int64_t)(head0 + ctx->nql) * ctx->d || peer_layer_stride < 0)
+    return fail(MOA_ERR_SHAPE, "peer layout: head0 %d + %d local heads do not fit the batch stride %lld", head0,
+                ctx->nql, (long long)peer_batch_stride);
+  std::vector<moa::PeerOut> host(n_peers);
+  for (int k = 0; k < n_peers; ++k) {
+    if (!peer_o[k] || !peer_flags[k] || ((uintptr_t)peer_flags[k] & 3))
+      return fail(MOA_ERR_INVALID_ARG, "peer %d: NULL or misaligned pointer", k);
+    host[k].o = peer_o[k];
+    host[k].flag = peer_flags[k];
+  }
+  cudaError_t e = cudaDeviceSynchronize();  // launches in flight may read the old table
+  if (e == cudaSuccess && !ctx->d_peers) e = cudaMalloc(&ctx->d_peers, 16 * sizeof(moa::PeerOut));
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_peers, host.data(), n_peers * sizeof(moa::PeerOut), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "peer output table");
+  ctx->n_peers = n_peers;
+  ctx->peer_head0 = head0;
+  ctx->peer_bs = peer_batch_stride;
+  ctx->peer_ls = peer_layer_stride;
+  return ok();
+}
+
+moa_status moa_wait_flag(const unsigned int *flag, unsigned int expected, moa_stream_t stream) {
+  if (!flag || ((uintptr_t)flag & 3)) return fail(MOA_ERR_INVALID_ARG, "flag must be a 4-byte aligned device pointer");
+  int e = moa::launch_wait_flag(flag, expected, stream);
+  if (e) return cuda_fail((cudaError_t)e, "wait_flag launch");
   return ok();
 }
 

@@ -202,6 +202,10 @@ struct moa_ctx {
   void *d_ml = nullptr;
   std::vector<unsigned char> ml_image;
   bool ml_dirty = true;
+  // fused head-output all-gather (moa_set_peer_outputs)
+  void *d_peers = nullptr;
+  int n_peers = 0, peer_head0 = 0;
+  int64_t peer_bs = 0, peer_ls = 0;
 };
 
 namespace moa {
@@ -299,8 +303,17 @@ struct DecodeMmaArgs {
   int chunk;                   // rank-invariant split: rows per chunk (0: balanced row split)
   int chunks_per_seq;          // sum_g ceil((s + W_g) / chunk)
   const int32_t *d_gc_off;     // first chunk of each local group inside a sequence [ngl + 1]
+  // fused head-output all-gather (moa_set_peer_outputs): n_peers destinations (device array)
+  const void *peers;
+  int n_peers, peer_head0, layer;
+  int64_t peer_bs, peer_ls;
+};
+struct PeerOut {
+  void *o;             // destination [L?][B][Hq_total][d] bf16 (peer-mapped device address)
+  unsigned *flag;      // destination's per-layer arrival counters [L]
 };
 int launch_decode_mma(const DecodeMmaArgs &a, void *stream);
+int launch_wait_flag(const unsigned *flag, unsigned expected, void *stream);
 
 // Cross-layer decode (moa_decode_step_fused_layers): one launch streams
 // the caches of n consecutive layers.  The per-layer static data lives in a device array of

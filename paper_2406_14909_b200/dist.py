@@ -206,6 +206,59 @@ class HeadGather:
         return out, done
 
 
+class PeerGather:
+    """Fused head-output all-gather for kv-group shards: the decode
+    epilogue of every rank writes its finished head rows straight into every rank's gathered
+    ``[L, B, Hq, d]`` buffer over NVLink (peer-mapped symmetric memory) and bumps that rank's
+    per-layer counter; a rank waits on its own counter (``wait``) before it consumes layer l's
+    heads.  No collective launch, no copy and no permute: each rank's heads land at their
+    global offset directly.
+
+    ``buffers``/``flags``: per-rank device addresses of the gathered buffers and counters as
+    mapped on THIS device; built from torch symmetric memory by ``from_symmetric_memory``
+    (multi-GPU), or from plain local tensors when several shard contexts share one GPU
+    (tests)."""
+
+    def __init__(self, ctx, shard: Shard, group_size: int, num_kv_heads: int, batch: int,
+                 out: torch.Tensor, flags: torch.Tensor, buffers: Sequence[int], flag_ptrs: Sequence[int]):
+        L, B, Hq, d = out.shape
+        self.out, self.flags = out, flags
+        self.per_layer_step = batch * num_kv_heads
+        self.tokens = 0
+        ctx.set_peer_outputs(list(buffers), list(flag_ptrs), batch_stride=Hq * d, layer_stride=B * Hq * d,
+                             head0=shard.g0 * group_size)
+
+    @classmethod
+    def from_symmetric_memory(cls, ctx, shard: Shard, group_size: int, num_kv_heads: int, num_layers: int,
+                              batch: int, num_q_heads: int, head_dim: int, device, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        o_bytes = num_layers * batch * num_q_heads * head_dim * 2
+        f_off = (o_bytes + 255) // 256 * 256
+        buf = symm.empty(f_off + 4 * num_layers, dtype=torch.uint8, device=device)
+        buf.zero_()
+        grp = group if group is not None else dist.group.WORLD
+        hdl = symm.rendezvous(buf, grp)
+        torch.cuda.synchronize(device)
+        dist.barrier(group=grp)   # every counter is zero before any rank writes
+        ptrs = [int(p) for p in hdl.buffer_ptrs]
+        out = buf[:o_bytes].view(torch.bfloat16).view(num_layers, batch, num_q_heads, head_dim)
+        flags = buf[f_off:f_off + 4 * num_layers].view(torch.int32)
+        pg = cls(ctx, shard, group_size, num_kv_heads, batch, out, flags, ptrs, [p + f_off for p in ptrs])
+        pg._keep = (buf, hdl)
+        return pg
+
+    def wait(self, layer: int, stream=None):
+        """Stream-ordered: later work waits until every rank's heads of `layer` of the
+        current token have landed in this rank's buffer."""
+        from .moa import wait_flag
+        wait_flag(self.flags[layer:layer + 1], (self.tokens + 1) * self.per_layer_step, stream)
+
+    def next_token(self):
+        self.tokens += 1
+
+
 class _null:
     def __enter__(self):
         return self

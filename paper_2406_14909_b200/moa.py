@@ -303,6 +303,16 @@ class MoAContext:
                                              workspace.numel() * workspace.element_size(), _stream(stream)),
               "moa_decode_step_fused")
 
+    def set_peer_outputs(self, peer_o: Sequence[int], peer_flags: Sequence[int], batch_stride: int,
+                         layer_stride: int, head0: int):
+        """moa_set_peer_outputs: destination buffers (device addresses as ints, e.g.
+        ``t.data_ptr()`` of peer-mapped / symmetric-memory tensors) and their uint32 counters."""
+        n = len(peer_o)
+        arr_o = (ctypes.c_void_p * max(n, 1))(*[int(x) for x in peer_o])
+        arr_f = (ctypes.c_void_p * max(n, 1))(*[int(x) for x in peer_flags])
+        check(self.lib.moa_set_peer_outputs(self.ctx, n, arr_o, arr_f, int(batch_stride), int(layer_stride),
+                                            int(head0)), "moa_set_peer_outputs")
+
     def prepare_layers(self):
         """moa_prepare_layers: upload the cross-layer descriptors (before graph capture)."""
         check(self.lib.moa_prepare_layers(self.ctx), "moa_prepare_layers")
@@ -341,3 +351,9 @@ class MoAContext:
         off, rows = self.cache_region(layer, b, g)
         start = self.layer_offset(layer, self._bound_batch) + off * self.d * es
         return buf[start: start + rows * self.d * es].view(self.dtype).view(rows, self.d)
+
+
+def wait_flag(flag: torch.Tensor, expected: int, stream=None):
+    """moa_wait_flag: the next work on `stream` waits until the uint32 counter `flag`
+    (a 1-element int32/uint32 device tensor view) reaches `expected` (mod 2^32)."""
+    check(_lib.lib().moa_wait_flag(_ptr(flag), int(expected) & 0xffffffff, _stream(stream)), "moa_wait_flag")
