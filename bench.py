@@ -3,8 +3,8 @@
 
 One step = one pass of the whole hot path over one batch of the C2 workload
 (configs[1], Vicuna-7B attention shape): span resolution is done once at
-setup; the timed step is the prefill of all 32 layers (tcgen05 kernel + cache
-fill, N = 4096, B = 8) followed by 512 decode tokens x 32 layers (fused
+setup; the timed step is the prefill of all 32 layers (tcgen05 kernel with the
+cache fill fused into it, N = 4096, B = 8) followed by 512 decode tokens x 32 layers (fused
 append + split-KV decode + combine; one cross-layer launch per token,
 moa_decode_step_fused_layers).  "decode_per_layer" reports the same decode with
 one launch per layer-token (the order a model needs when layer l+1's query
@@ -321,10 +321,9 @@ def run_ours(args, rank, world, local_rank):
         for l in range(L):
             if record:
                 ev_p[l][0].record(stream)
-            ctx.prefill_attn(l, Q[l], K[l], V[l], O, scale)
+            ctx.prefill(l, Q[l], K[l], V[l], O, scale)   # attention + fused cache fill, one kernel
             if record:
                 ev_p[l][1].record(stream)
-            ctx.cache_fill(l, K[l], V[l])     # = moa_prefill split in two so the attention kernel is timed alone
         ph = torch.cuda.Event(enable_timing=True)
         ph.record(stream)
         # decode: one cross-layer launch per token (moa_decode_step_fused_layers: all 32 layers'
@@ -421,9 +420,9 @@ def run_ours(args, rank, world, local_rank):
                                      "unit": "TFLOP/s",
                                      "frac": achieved_tf / peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]),
                                      "peak_source": peak_src + ", sustained bf16",
-                                     "note": "in-window FLOPs 4*d*sum|V| over the tcgen05 attention kernel's "
-                                             "event-timed launches (moa_prefill_attn); the step also runs "
-                                             "moa_cache_fill per layer",
+                                     "note": "in-window FLOPs 4*d*sum|V| over the event-timed launches of the "
+                                             "tcgen05 prefill kernel (moa_prefill: attention + the cache fill "
+                                             "fused into it)",
                                      "avg_launch_ms": pk_total_s * 1e3 / L}},
             "decode_ms_per_step": dec / K_steps,
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -436,7 +435,7 @@ def run_ours(args, rank, world, local_rank):
                          "peak_source": peak_src},
             "e2e": e2e,
             "decode_per_layer": per_layer,
-            "gpu_launches": K_steps * (2 * L + T),
+            "gpu_launches": K_steps * (L + T),
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
@@ -654,9 +653,8 @@ def _bench_prefill_cfg(moa, cfg, dev, peaks):
         e0.record(stream)
         for l in range(L):
             ev[l][0].record(stream)
-            ctx.prefill_attn(l, *qkv[l], o, scale)
+            ctx.prefill(l, *qkv[l], o, scale)   # attention + fused cache fill
             ev[l][1].record(stream)
-            ctx.cache_fill(l, qkv[l][1], qkv[l][2])
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / 1e3, sum(a.elapsed_time(b) for a, b in ev) / 1e3
@@ -672,8 +670,8 @@ def _bench_prefill_cfg(moa, cfg, dev, peaks):
            "ms_all_layers": tot * 1e3, "attn_ms_all_layers": attn * 1e3,
            "roofline": {"bound": "tensor", "achieved": tf, "peak": pk, "unit": "TFLOP/s", "frac": tf / pk,
                         "frac_of_burst": tf / peaks["bf16_tflops"], "traffic": None,
-                        "note": "in-window FLOPs 4*d*sum|V| over the event-timed attention launches; "
-                                "tokens/s includes the cache fill"},
+                        "note": "in-window FLOPs 4*d*sum|V| over the event-timed moa_prefill launches "
+                                "(attention + fused cache fill)"},
            "clocks": clk.summary()}
     del ctx, qkv, o
     torch.cuda.empty_cache()

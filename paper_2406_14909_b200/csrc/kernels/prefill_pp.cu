@@ -98,6 +98,14 @@ struct PpParams {
   int o_v8;              // output rows 32-byte aligned: 256-bit stores in the epilogue
   const int64_t *seq_n;  // ragged: per-sequence N_b (null: N)
   const int32_t *win_bq; // ragged: per-sequence windows [batch, nql] (null: win_q)
+  // fused cache fill (a5): the last q block of each group's filler head writes the cache rows
+  // of the K/V tiles it streams anyway, from shared memory (warp 10)
+  int fill;
+  __nv_bfloat16 *kc, *vc;
+  int64_t rows_per_seq;
+  const int64_t *g_off;
+  const int32_t *win_g;
+  const int32_t *fill_h;  // [ngl] local q-head whose last q block fills the group (-1: none)
 };
 
 struct PBars {
@@ -106,6 +114,8 @@ struct PBars {
   uint64_t v_full[4], v_empty[4];
   uint64_t s_full[2], p_full[2];
   uint64_t o_full[2], o_empty[2];
+  uint64_t k_copied[6], v_copied[4];  // fused cache fill: warp 10's stores have read a filler tile
+  int k_gen[6], v_gen[4];             // fused cache fill: ring step whose load the producer issued last
   uint32_t tmem_base;
 };
 
@@ -180,6 +190,85 @@ __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
   if (!RAG) it.W = p.win_q[it.h];
   it.bt = kv_block_tiles(it.i0, it.N, it.W, p.n_sink, bshift_of<BS>(p));
   return it;
+}
+
+
+// Fused cache fill: the cache keeps positions [0, min(s, N)) and
+// [max(s, N - W_g), N) of every (b, g) (reading c13).  Kv tile t is stored by
+// the item of the group's filler head (the head with the largest window, W_h = W_g) whose q
+// block holds rows [128 t, 128 t + 128): tile t is on that item's diagonal, so every item
+// streams it anyway (causal; sink tiles are q block 0's diagonal), and the fill work spreads
+// over the head's last q blocks instead of one item.  Warp 10 TMA-stores the kept rows from
+// the tile in shared memory while the tensor core uses it.  Token mask, uniform batch only.
+__device__ __forceinline__ bool fill_item(const PpParams &p, const PItem &it) {
+  return p.fill && p.fill_h[it.h / p.G] == it.h;
+}
+// rows [r0, r1) of kv tile t that the cache keeps (r1 <= r0: none)
+__device__ __forceinline__ void fill_rows(const PpParams &p, int64_t N, int Wg, int t, int &r0, int &r1, int &q0,
+                                          int &q1) {
+  const int64_t j0 = (int64_t)t * kN;
+  const int64_t s = p.n_sink;
+  const int64_t sink_end = s < N ? s : N;
+  const int64_t ring_lo = (N - Wg) > s ? (N - Wg) : s;
+  // two ranges: sinks [0, sink_end) and ring [ring_lo, N), clipped to the tile
+  int64_t a0 = j0, a1 = j0 + kN < sink_end ? j0 + kN : sink_end;
+  int64_t b0 = j0 > ring_lo ? j0 : ring_lo, b1 = j0 + kN < N ? j0 + kN : N;
+  r0 = (int)(a0 - j0);
+  r1 = (int)(a1 - j0);
+  q0 = (int)(b0 - j0);
+  q1 = (int)(b1 - j0);
+}
+// tile t of a filler item is stored by it iff it is one of the item's diagonal tiles
+// (t >= i0 / 128) and holds kept rows
+__device__ __forceinline__ bool fill_tile(const PpParams &p, int64_t i0, int64_t N, int Wg, int t) {
+  if ((int64_t)t * kN < i0) return false;
+  int r0, r1, q0, q1;
+  fill_rows(p, N, Wg, t, r0, r1, q0, q1);
+  return r1 > r0 || q1 > q0;
+}
+#ifndef MOA_PP_FILL_STORES
+#define MOA_PP_FILL_STORES 1  // diagnostics: 0 keeps the fill protocol but issues no stores
+#endif
+// TMA stores of the kept rows of one K or V tile (two 64-column 128B-swizzled slabs in shared
+// memory) into the layer cache: the rows of a tile map to runs of consecutive ring slots (a run
+// ends where the ring wraps), each run goes out as 16-row boxes where the tile row is 16-aligned
+// and 1-row boxes at its ends; the TMA engine un-swizzles (one thread issues, no registers).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *m, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+template <int D>
+__device__ __forceinline__ void fill_store(const PpParams &p, uint32_t tile, const CUtensorMap *m16,
+                                           const CUtensorMap *m1, int64_t region, int64_t N, int Wg, int t) {
+  constexpr int kSlabs = D / 64;
+  constexpr int kSlabBytes = kM * 128;
+  int r0, r1, q0, q1;
+  fill_rows(p, N, Wg, t, r0, r1, q0, q1);
+  const int64_t j0 = (int64_t)t * kN;
+  const int s = p.n_sink;
+  for (int rr = 0; rr < 2; ++rr) {
+    int r = rr ? q0 : r0;
+    const int hi = rr ? q1 : r1;
+    while (r < hi) {
+      const int64_t pos = j0 + r;
+      const int64_t slot = pos < s ? pos : s + (pos - s) % Wg;
+      int n = hi - r;
+      if (pos >= s && s + Wg - slot < n) n = (int)(s + Wg - slot);
+      int cr = (int)(region + slot);
+      while (MOA_PP_FILL_STORES && n > 0) {
+        const bool box16 = (r & 15) == 0 && n >= 16;
+        for (int sl = 0; sl < kSlabs; ++sl)
+          tma_store_2d(box16 ? m16 : m1, tile + sl * kSlabBytes + r * 128, sl * 64, cr);
+        const int st = box16 ? 16 : 1;
+        r += st;
+        cr += st;
+        n -= st;
+      }
+    }
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
 // which q tiles use union step k (tile t); false/false = skipped by every role
@@ -657,7 +746,9 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
 template <int D, int BS, bool RAG>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_pp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const PpParams p) {
+                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc16,
+                      const __grid_constant__ CUtensorMap tm_vc16, const __grid_constant__ CUtensorMap tm_kc1,
+                      const __grid_constant__ CUtensorMap tm_vc1, const PpParams p) {
   using C = PCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];  // SW128 TMA / UMMA tiles need 1024-B alignment
   __shared__ PBars bars;
@@ -682,10 +773,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::kNK; ++s) {
       mbar_init(smem_u32(&bars.k_full[s]), 1);
       mbar_init(smem_u32(&bars.k_empty[s]), 2);  // one commit per MMA warp
+      mbar_init(smem_u32(&bars.k_copied[s]), 1);
+      bars.k_gen[s] = -1;
     }
     for (int s = 0; s < C::kNV; ++s) {
       mbar_init(smem_u32(&bars.v_full[s]), 1);
       mbar_init(smem_u32(&bars.v_empty[s]), 2);
+      mbar_init(smem_u32(&bars.v_copied[s]), 1);
+      bars.v_gen[s] = -1;
     }
     fence_mbar_init();
   }
@@ -711,28 +806,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarpKV) {
     if (lane == 0) {
       int T = 0;
+      uint32_t kfill = 0, vfill = 0, kcph = 0, vcph = 0;  // per slot: holds a filler tile / copied parity
+      volatile int *kgen = bars.k_gen, *vgen = bars.v_gen;
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
         const PItem it = get_pitem<BS, RAG>(p, idx);
-            const int g = it.h / p.G;
+        const int g = it.h / p.G;
+        const bool fi = fill_item(p, it);
+        const int Wg = fi ? p.win_g[g] : 0;
         const int ns = it.bt.steps();
         for (int k = 0; k < ns; ++k) {
           int t;
           bool u0, u1;
           step_use(it.bt, k, t, u0, u1);
           if (!u0 && !u1) continue;
+          const bool ft = fi && fill_tile(p, it.i0, it.N, Wg, t);
           const int j0 = t * kN;
           const int ks = T % C::kNK;
           if (T >= C::kNK) mbar_wait(smem_u32(&bars.k_empty[ks]), ((T - C::kNK) / C::kNK) & 1);
+          if (kfill >> ks & 1) {  // warp 10's stores still read the previous (filler) tile of this slot
+            mbar_wait(smem_u32(&bars.k_copied[ks]), kcph >> ks & 1);
+            kcph ^= 1u << ks;
+          }
+          kfill = (kfill & ~(1u << ks)) | ((uint32_t)ft << ks);
           const uint32_t kbar = smem_u32(&bars.k_full[ks]);
           mbar_expect_tx(kbar, C::kTileBytes);
           for (int sl = 0; sl < C::kSlabs; ++sl)
             tma_load_4d(k_smem + ks * C::kTileBytes + sl * C::kSlabBytes, &tm_k, kbar, sl * 64, g, j0, it.b);
+          if (ft) kgen[ks] = T;  // warp 10 may now wait for this fill's k_full phase
           const int vs = T % C::kNV;
           if (T >= C::kNV) mbar_wait(smem_u32(&bars.v_empty[vs]), ((T - C::kNV) / C::kNV) & 1);
+          if (vfill >> vs & 1) {
+            mbar_wait(smem_u32(&bars.v_copied[vs]), vcph >> vs & 1);
+            vcph ^= 1u << vs;
+          }
+          vfill = (vfill & ~(1u << vs)) | ((uint32_t)ft << vs);
           const uint32_t vbar = smem_u32(&bars.v_full[vs]);
           mbar_expect_tx(vbar, C::kTileBytes);
           for (int sl = 0; sl < C::kSlabs; ++sl)
             tma_load_4d(v_smem + vs * C::kTileBytes + sl * C::kSlabBytes, &tm_v, vbar, sl * 64, g, j0, it.b);
+          if (ft) vgen[vs] = T;
           ++T;
         }
       }
@@ -740,9 +852,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kWarpQ) {
     if (lane == 0) {
       int qc[2] = {0, 0};
+      int T = 0;  // K/V ring step (the producer's count)
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
         const PItem it = get_pitem<BS, RAG>(p, idx);
-            for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < 2; ++j) {
           if (j == 1 && !it.bt.has1) continue;
           if (qc[j] > 0) mbar_wait(smem_u32(&bars.q_empty[j]), (qc[j] - 1) & 1);
           ++qc[j];
@@ -759,7 +872,53 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int sl = 0; sl < C::kSlabs; ++sl)
               tma_prefetch_4d(&tm_q, sl * 64, nx.h, (int)(nx.i0 + j * kM), nx.b);
         }
+        // fused cache fill: TMA-store the kept rows of this item's filler tiles.  The producer
+        // publishes the ring step it loaded into a slot (k_gen / v_gen) and does not refill a
+        // slot holding a filler tile before warp 10 releases it (k_copied / v_copied), so the
+        // full-barrier phase warp 10 waits for is unambiguous; the slots are released at the
+        // item's end, once the stores have read them
+        if (!p.fill) continue;
+        const bool fi = fill_item(p, it);
+        const int ns = it.bt.steps();
+        if (!fi) {
+          for (int k = 0; k < ns; ++k) {
+            int t;
+            bool u0, u1;
+            step_use(it.bt, k, t, u0, u1);
+            T += (u0 || u1);
+          }
+          continue;
+        }
+        const int g = it.h / p.G;
+        const int Wg = p.win_g[g];
+        const int64_t region = (int64_t)it.b * p.rows_per_seq + p.g_off[g];
+        volatile int *kgen = bars.k_gen, *vgen = bars.v_gen;
+        uint32_t pend[4];  // copied-barriers of this item's stored tiles (<= 2 diagonal tiles)
+        int np_ = 0;
+        for (int k = 0; k < ns; ++k) {
+          int t;
+          bool u0, u1;
+          step_use(it.bt, k, t, u0, u1);
+          if (!u0 && !u1) continue;
+          if (fill_tile(p, it.i0, it.N, Wg, t)) {
+            const int ks = T % C::kNK, vs = T % C::kNV;
+            while (kgen[ks] != T) __nanosleep(32);
+            mbar_wait(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
+            fill_store<D>(p, k_smem + ks * C::kTileBytes, &tm_kc16, &tm_kc1, region, it.N, Wg, t);
+            while (vgen[vs] != T) __nanosleep(32);
+            mbar_wait(smem_u32(&bars.v_full[vs]), (T / C::kNV) & 1);
+            fill_store<D>(p, v_smem + vs * C::kTileBytes, &tm_vc16, &tm_vc1, region, it.N, Wg, t);
+            pend[np_++] = smem_u32(&bars.k_copied[ks]);
+            pend[np_++] = smem_u32(&bars.v_copied[vs]);
+          }
+          ++T;
+        }
+        if (np_) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          for (int i = 0; i < np_; ++i) mbar_arrive(pend[i]);
+        }
       }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // cache writes complete
     }
   } else if (warp == kWarpMMA || warp == kWarpMMA1) {
     mma_role<D, BS, RAG>(p, bars, tmem, q_smem, k_smem, v_smem, total, warp == kWarpMMA ? 0 : 1);
@@ -785,6 +944,11 @@ int launch_pp(const PrefillArgs &a, void *stream) {
       !make_tile_map(&mk, a.k, D, ngl, a.N, a.batch, a.kv_row_stride, kN) ||
       !make_tile_map(&mv, a.v, D, ngl, a.N, a.batch, a.kv_row_stride, kN))
     return (int)cudaErrorInvalidValue;
+  static const CUtensorMap zero_map{};
+  const CUtensorMap *mk16 = a.fill ? static_cast<const CUtensorMap *>(a.kmap16) : &zero_map;
+  const CUtensorMap *mv16 = a.fill ? static_cast<const CUtensorMap *>(a.vmap16) : &zero_map;
+  const CUtensorMap *mk1 = a.fill ? static_cast<const CUtensorMap *>(a.kmap1) : &zero_map;
+  const CUtensorMap *mv1 = a.fill ? static_cast<const CUtensorMap *>(a.vmap1) : &zero_map;
   PpParams p;
   p.o = a.o;
   p.lse = a.lse;
@@ -802,6 +966,13 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   p.o_v8 = (((uintptr_t)a.o | (uintptr_t)(a.o_row_stride * 2)) & 31) == 0;
   p.win_bq = a.d_win_bq;
   p.items = a.d_seq_n ? a.d_items_rag : a.d_items2;
+  p.fill = a.fill;
+  p.kc = static_cast<__nv_bfloat16 *>(a.k_cache);
+  p.vc = static_cast<__nv_bfloat16 *>(a.v_cache);
+  p.rows_per_seq = a.rows_per_seq;
+  p.g_off = a.d_g_off;
+  p.win_g = a.d_win_g;
+  p.fill_h = a.d_fill_h;
   // the token mask (bshift < 0) and the block mask are separate instantiations, so the
   // token path carries no block-mode arithmetic
   const bool rag = p.seq_n != nullptr;
@@ -813,7 +984,7 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   if (e != cudaSuccess) return (int)e;
   const int total = rag ? p.n_items : p.n_items * p.batch;
   const int grid = total < num_sms_pp() ? total : num_sms_pp();
-  kern<<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, p);
+  kern<<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, *mk16, *mv16, *mk1, *mv1, p);
   return (int)cudaGetLastError();
 }
 

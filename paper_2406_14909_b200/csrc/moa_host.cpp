@@ -97,7 +97,7 @@ void free_tables(LayerPlan &p) {
   p.d_tables = nullptr;
   p.d_win_q = p.d_win_g = nullptr;
   p.d_g_off = nullptr;
-  p.d_items = p.d_items2 = p.d_chunks = p.d_g_chunk = p.d_gc_off = nullptr;
+  p.d_items = p.d_items2 = p.d_chunks = p.d_g_chunk = p.d_gc_off = p.d_fill_h = nullptr;
   p.d_counters = nullptr;
 }
 
@@ -113,7 +113,8 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   size_t o_chunks = align16(o_items2 + p.items2.size() * 4);
   size_t o_gch = align16(o_chunks + p.chunks.size() * 4);
   size_t o_gco = align16(o_gch + p.g_chunk.size() * 4);
-  size_t o_cnt = align16(o_gco + p.gc_off.size() * 4);
+  size_t o_fh = align16(o_gco + p.gc_off.size() * 4);
+  size_t o_cnt = align16(o_fh + p.fill_h.size() * 4);
   size_t total = align16(o_cnt + (size_t)ctx->max_batch * ctx->ngl * 4);
   std::vector<unsigned char> host(total, 0);
   std::memcpy(host.data() + o_winq, p.win_q.data(), p.win_q.size() * 4);
@@ -124,6 +125,7 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   std::memcpy(host.data() + o_chunks, p.chunks.data(), p.chunks.size() * 4);
   std::memcpy(host.data() + o_gch, p.g_chunk.data(), p.g_chunk.size() * 4);
   std::memcpy(host.data() + o_gco, p.gc_off.data(), p.gc_off.size() * 4);
+  std::memcpy(host.data() + o_fh, p.fill_h.data(), p.fill_h.size() * 4);
   DeviceGuard dg(ctx->device);
   free_tables(p);
   void *d = nullptr;
@@ -145,6 +147,7 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   p.d_g_chunk = reinterpret_cast<const int32_t *>(b + o_gch);
   p.d_gc_off = reinterpret_cast<const int32_t *>(b + o_gco);
   p.d_counters = reinterpret_cast<int *>(b + o_cnt);
+  p.d_fill_h = reinterpret_cast<const int32_t *>(b + o_fh);
   return MOA_OK;
 }
 
@@ -291,6 +294,13 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
     off += (int64_t)n_sink + wg;
   }
   np.rows_per_seq = off;
+  np.fill_h.assign(ctx->ngl, -1);
+  for (int g = 0; g < ctx->ngl; ++g)
+    for (int j = 0; j < G; ++j)
+      if (np.win_q[g * G + j] == np.win_g[g]) {
+        np.fill_h[g] = g * G + j;
+        break;
+      }
 
   // prefill work items (h_local, q_tile).  Order: heads by total kv-tile count, heaviest
   // first (so the kernel tail holds light work), and the q tiles of one head consecutively,
@@ -392,6 +402,8 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
     std::memcpy(np.vmap, p.vmap, sizeof(np.vmap));
     std::memcpy(np.kmap16, p.kmap16, sizeof(np.kmap16));
     std::memcpy(np.vmap16, p.vmap16, sizeof(np.vmap16));
+    std::memcpy(np.kmap1, p.kmap1, sizeof(np.kmap1));
+    std::memcpy(np.vmap1, p.vmap1, sizeof(np.vmap1));
     np.maps_ok = p.maps_ok;
   }
   st = upload_tables(ctx, np);
@@ -592,7 +604,9 @@ moa_status moa_bind_layer_cache(moa_ctx *ctx, int layer, void *k_cache, void *v_
     if (!moa::encode_cache_map(p.kmap, k_cache, ctx->d, rows, 64) ||
         !moa::encode_cache_map(p.vmap, v_cache, ctx->d, rows, 64) ||
         !moa::encode_cache_map(p.kmap16, k_cache, ctx->d, rows, 16) ||
-        !moa::encode_cache_map(p.vmap16, v_cache, ctx->d, rows, 16))
+        !moa::encode_cache_map(p.vmap16, v_cache, ctx->d, rows, 16) ||
+        !moa::encode_cache_map(p.kmap1, k_cache, ctx->d, rows, 1) ||
+        !moa::encode_cache_map(p.vmap1, v_cache, ctx->d, rows, 1))
       return fail(MOA_ERR_CUDA, "cuTensorMapEncodeTiled failed for the layer %d cache", layer);
     p.maps_ok = true;
   }
@@ -630,6 +644,15 @@ static moa_status check_launch_common(const moa_ctx *ctx, int layer, int batch) 
 }
 
 static bool aligned16(const void *ptr) { return ((uintptr_t)ptr & 15) == 0; }
+
+// MOA_PP_FUSED_FILL=0: moa_prefill runs the separate cache-fill kernel (A/B diagnostics)
+static bool fused_fill_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("MOA_PP_FUSED_FILL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const void *k, const void *v, void *o,
                                  int64_t q_row_stride, int64_t kv_row_stride, int64_t o_row_stride, int batch,
@@ -672,10 +695,24 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
     a.d_items_rag = p.d_rag_items2;
     a.n_items_rag = (int)(p.rag_items2.size() / 2);
   }
+  // fused cache fill (a5 inside the prefill kernel): bf16, token mask, uniform batch
+  const bool fused = fill && ctx->dtype == MOA_BF16 && p.bshift < 0 && !p.rag_batch && p.maps_ok &&
+                     fused_fill_enabled();
+  if (fused) {
+    a.fill = 1;
+    a.kmap16 = p.kmap16; a.vmap16 = p.vmap16; a.kmap1 = p.kmap1; a.vmap1 = p.vmap1;
+    a.k_cache = p.k_cache; a.v_cache = p.v_cache; a.rows_per_seq = p.rows_per_seq;
+    a.d_g_off = p.d_g_off; a.d_win_g = p.d_win_g; a.d_fill_h = p.d_fill_h;
+  }
   int e = ctx->dtype == MOA_FP32 ? moa::launch_prefill_f32(a, stream) : moa::launch_prefill_bf16_pp(a, stream);
   if (e) return cuda_fail((cudaError_t)e, "prefill launch");
   if (!fill) {
     ctx->last_cache_write = -1;
+    return ok();
+  }
+  if (fused) {
+    p.next_pos = N;
+    ctx->last_cache_write = layer;
     return ok();
   }
   moa::CacheArgs c{};

@@ -149,6 +149,7 @@ struct LayerPlan {
   int max_chunks_per_group = 0;
   int dec_cps = 0;               // bf16 decode: rank-invariant chunks per sequence (ctx->dec_chunk rows each)
   std::vector<int32_t> gc_off;   // first rank-invariant chunk of each group in a sequence, size ngl + 1
+  std::vector<int32_t> fill_h;   // [ngl] first local q-head with W_h = W_g (fused cache fill)
   const int32_t *d_gc_off = nullptr;
   // device copies of the tables (one allocation)
   void *d_tables = nullptr;
@@ -159,6 +160,7 @@ struct LayerPlan {
   const int32_t *d_items2 = nullptr;
   const int32_t *d_chunks = nullptr;
   const int32_t *d_g_chunk = nullptr;
+  const int32_t *d_fill_h = nullptr;  // [ngl] local q-head of the group whose last q block fills the cache
   int *d_counters = nullptr;     // [max_batch, ngl] decode combine tickets (zeroed at upload)
   // ragged batch (moa_set_ragged): per-sequence prompt length N_b and windows W_{b,h}
   int rag_batch = 0;             // 0 = uniform batch
@@ -175,6 +177,8 @@ struct LayerPlan {
   alignas(64) unsigned char vmap[128] = {};
   alignas(64) unsigned char kmap16[128] = {};  // 16-row boxes (tile tails)
   alignas(64) unsigned char vmap16[128] = {};
+  alignas(64) unsigned char kmap1[128] = {};   // 1-row boxes (prefill's fused cache fill)
+  alignas(64) unsigned char vmap1[128] = {};
   bool maps_ok = false;
   // bound cache
   void *k_cache = nullptr;
@@ -231,6 +235,13 @@ struct PrefillArgs {
   const int32_t *d_win_bq;  // ragged: per-sequence windows [batch, nql] (null: d_win_q)
   const int32_t *d_items_rag;  // ragged two-tile items (h | b << 16, q_block), real items only, LPT
   int n_items_rag;
+  // fused cache fill (bf16 token-mask uniform prefill): write the kept rows from the K/V tiles
+  int fill;
+  void *k_cache, *v_cache;
+  int64_t rows_per_seq;
+  const int64_t *d_g_off;
+  const int32_t *d_win_g, *d_fill_h;
+  const void *kmap16, *vmap16, *kmap1, *vmap1;  // cache tensor maps (16-row / 1-row boxes)
 };
 int launch_prefill_f32(const PrefillArgs &a, void *stream);
 int launch_prefill_bf16_pp(const PrefillArgs &a, void *stream);

@@ -393,3 +393,36 @@ def test_set_spans_twice_keeps_cache_maps_for_decode(moa):
     Kh, Vh = torch.cat([k, kd[:, None]], 1), torch.cat([v, vd[:, None]], 1)
     Od, _ = oracle.decode(f64(qd), f64(Kh), f64(Vh), N, W2, s, tau)
     assert np.abs(f64(od) - Od).max() < 2e-2
+
+
+@pytest.mark.parametrize("N,s,W,Hkv", [
+    (300, 4, [3, 140, 0, 290, 17, 17, 1, 0], 2),      # G=4: filler heads 3 (W=290) and 4 (first of the 17s)
+    (1000, 64, [0, 0, 512, 2000], 4),                 # sink-only groups, W > N
+    (40, 64, [5, 100], 2),                            # N < s: every position is a sink
+    (129, 8, [128, 1, 64, 129], 4),                   # ragged last tile, W = N
+    (777, 16, [600, 77, 300, 5, 700, 760, 2, 40], 4), # G=2, filler head second in its group
+])
+def test_fused_cache_fill_equals_separate_fill(moa, N, s, W, Hkv):
+    """moa_prefill's fused cache fill (warp 10 copies the kept rows of the filler item's K/V
+    tiles from shared memory) writes the same cache bytes as moa_prefill_attn + the separate
+    moa_cache_fill kernel, and both match the oracle image (reading c13)."""
+    B, d = 3, 128
+    Hq = len(W)
+    dtype = torch.bfloat16
+    q, k, v = (normal((B, N, h, d), 900 + i, dtype).cuda() for i, h in enumerate((Hq, Hkv, Hkv)))
+    scale = 1 / math.sqrt(d)
+    c1 = moa.MoAContext(1, Hq, Hkv, d, B, dtype=dtype)
+    c2 = moa.MoAContext(1, Hq, Hkv, d, B, dtype=dtype)
+    for c in (c1, c2):
+        c.set_spans(0, W, s, N)
+        c.alloc_cache(B)
+    o1, o2 = torch.empty_like(q), torch.empty_like(q)
+    c1.prefill(0, q, k, v, o1, scale)
+    c2.prefill_attn(0, q, k, v, o2, scale)
+    c2.cache_fill(0, k, v)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o1), bits(o2))
+    for which in (0, 1):
+        assert torch.equal(c1._cache[which], c2._cache[which]), which
+    assert c1.next_pos(0) == N
+    check_cache_image(c1, 0, k.cpu(), v.cpu(), N - 1, W, s, B, Hq // Hkv)

@@ -10,8 +10,8 @@ OUT=gpurun_out
 mkdir -p $OUT
 K='regex:prefill_pp_kernel|prefill_f32_kernel|decode_mma_kernel|decode_kernel|cache_fill_kernel|kv_append_kernel'
 L=32; T=512
-# warm-up launches of bench.py (--warmup 3): 3 steps x (L prefill + L cache fill + T cross-layer decode)
-SKIP=$((3 * (2 * L + T)))
+# warm-up launches of bench.py (--warmup 3): 3 steps x (L prefill with fused fill + T cross-layer decode)
+SKIP=$((3 * (L + T)))
 
 # 1) launch list of the same command bench.py runs (per-launch device time, serialised)
 timeout -k 10 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -s $SKIP -c 600 \
