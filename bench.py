@@ -701,6 +701,11 @@ def run_per_layer(ctx, ws, K, V, qd, kd, vd, od, scale, world, dev, bytes_per_to
     L, B, N = CFG.layers, CFG.batch, CFG.N
     for l in range(L):
         ctx.cache_fill(l, K[l], V[l])    # positions restart at N
+    for t in range(4):                   # warm-up tokens (not timed)
+        for l in range(L):
+            ctx.decode_step_fused(l, qd[t], kd[t], vd[t], od, N + t, scale, ws)
+    for l in range(L):
+        ctx.cache_fill(l, K[l], V[l])
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
