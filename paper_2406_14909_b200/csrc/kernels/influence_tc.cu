@@ -399,10 +399,11 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
         }
       } else {
         // E = p (C1 - G l) / (l - p) on packed pairs; one exponential pair in kPolyEvery on
-        // the FMA pipe, the reciprocals on MUFU
+        // the FMA pipe.  A pair's two quotients share one MUFU reciprocal:
+        // qa / da + qb / db = (qa db + qb da) / (da db)  (da, db in [1, l]: no overflow)
         const uint64_t sl2 = f2pk(p.sl2, p.sl2), nm2 = f2pk(-m, -m), nl2 = f2pk(-l, -l), l2 = f2pk(l, l),
                        c12 = f2pk(C1, C1), m12 = f2pk(-1.f, -1.f);
-        uint64_t a2[2] = {0ull, 0ull};
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < kCols; c += 2) {
           float ya, yb, ea, eb;
@@ -417,11 +418,11 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
           float da, db;
           f2upk(ffma2(p2, m12, l2), da, db);  // l - p (>= 1 off the star)
           const uint64_t q2 = fmul2(p2, ffma2(f2pk(g[c], g[c + 1]), nl2, c12));
-          a2[(c >> 1) & 1] = ffma2(q2, f2pk(fast_rcp(da), fast_rcp(db)), a2[(c >> 1) & 1]);
+          float qa, qb;
+          f2upk(fmul2(q2, f2pk(db, da)), qa, qb);
+          a[(c >> 1) & 3] = fmaf(qa + qb, fast_rcp(da * db), a[(c >> 1) & 3]);
         }
-        float a0, a1;
-        f2upk(fadd2(a2[0], a2[1]), a0, a1);
-        acc = a0 + a1;
+        acc = (a[0] + a[1]) + (a[2] + a[3]);
       }
       acc = acc * inv_l + (star_here ? Estar : 0.f);
       if (!valid) acc = 0.f;
