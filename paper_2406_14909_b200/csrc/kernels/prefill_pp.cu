@@ -115,7 +115,7 @@ struct PBars {
   uint64_t s_full[2], p_full[2];
   uint64_t o_full[2], o_empty[2];
   uint64_t k_copied[6], v_copied[4];  // fused cache fill: warp 10's stores have read a filler tile
-  int k_gen[6], v_gen[4];             // fused cache fill: ring step whose load the producer issued last
+  uint64_t k_issued[6], v_issued[4];  // fused cache fill: the producer issued a filler tile's load
   uint32_t tmem_base;
 };
 
@@ -774,13 +774,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&bars.k_full[s]), 1);
       mbar_init(smem_u32(&bars.k_empty[s]), 2);  // one commit per MMA warp
       mbar_init(smem_u32(&bars.k_copied[s]), 1);
-      bars.k_gen[s] = -1;
+      mbar_init(smem_u32(&bars.k_issued[s]), 1);
     }
     for (int s = 0; s < C::kNV; ++s) {
       mbar_init(smem_u32(&bars.v_full[s]), 1);
       mbar_init(smem_u32(&bars.v_empty[s]), 2);
       mbar_init(smem_u32(&bars.v_copied[s]), 1);
-      bars.v_gen[s] = -1;
+      mbar_init(smem_u32(&bars.v_issued[s]), 1);
     }
     fence_mbar_init();
   }
@@ -807,7 +807,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int T = 0;
       uint32_t kfill = 0, vfill = 0, kcph = 0, vcph = 0;  // per slot: holds a filler tile / copied parity
-      volatile int *kgen = bars.k_gen, *vgen = bars.v_gen;
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
         const PItem it = get_pitem<BS, RAG>(p, idx);
         const int g = it.h / p.G;
@@ -832,7 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(kbar, C::kTileBytes);
           for (int sl = 0; sl < C::kSlabs; ++sl)
             tma_load_4d(k_smem + ks * C::kTileBytes + sl * C::kSlabBytes, &tm_k, kbar, sl * 64, g, j0, it.b);
-          if (ft) kgen[ks] = T;  // warp 10 may now wait for this fill's k_full phase
+          if (ft) mbar_arrive(smem_u32(&bars.k_issued[ks]));  // warp 10 may wait for this fill's k_full phase
           const int vs = T % C::kNV;
           if (T >= C::kNV) mbar_wait(smem_u32(&bars.v_empty[vs]), ((T - C::kNV) / C::kNV) & 1);
           if (vfill >> vs & 1) {
@@ -844,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(vbar, C::kTileBytes);
           for (int sl = 0; sl < C::kSlabs; ++sl)
             tma_load_4d(v_smem + vs * C::kTileBytes + sl * C::kSlabBytes, &tm_v, vbar, sl * 64, g, j0, it.b);
-          if (ft) vgen[vs] = T;
+          if (ft) mbar_arrive(smem_u32(&bars.v_issued[vs]));
           ++T;
         }
       }
@@ -853,6 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int qc[2] = {0, 0};
       int T = 0;  // K/V ring step (the producer's count)
+      uint32_t kiph = 0, viph = 0;  // per slot: parity of the next issued-barrier phase
       for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
         const PItem it = get_pitem<BS, RAG>(p, idx);
         for (int j = 0; j < 2; ++j) {
@@ -873,10 +873,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_prefetch_4d(&tm_q, sl * 64, nx.h, (int)(nx.i0 + j * kM), nx.b);
         }
         // fused cache fill: TMA-store the kept rows of this item's filler tiles.  The producer
-        // publishes the ring step it loaded into a slot (k_gen / v_gen) and does not refill a
-        // slot holding a filler tile before warp 10 releases it (k_copied / v_copied), so the
-        // full-barrier phase warp 10 waits for is unambiguous; the slots are released at the
-        // item's end, once the stores have read them
+        // signals each filler load it issues (k_issued / v_issued) and does not refill a slot
+        // holding a filler tile before warp 10 releases it (k_copied / v_copied), so the
+        // full-barrier phase warp 10 then waits for is unambiguous; the slots are released at
+        // the item's end, once the stores have read them
         if (!p.fill) continue;
         const bool fi = fill_item(p, it);
         const int ns = it.bt.steps();
@@ -892,7 +892,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int g = it.h / p.G;
         const int Wg = p.win_g[g];
         const int64_t region = (int64_t)it.b * p.rows_per_seq + p.g_off[g];
-        volatile int *kgen = bars.k_gen, *vgen = bars.v_gen;
         uint32_t pend[4];  // copied-barriers of this item's stored tiles (<= 2 diagonal tiles)
         int np_ = 0;
         for (int k = 0; k < ns; ++k) {
@@ -902,10 +901,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!u0 && !u1) continue;
           if (fill_tile(p, it.i0, it.N, Wg, t)) {
             const int ks = T % C::kNK, vs = T % C::kNV;
-            while (kgen[ks] != T) __nanosleep(32);
+            mbar_wait(smem_u32(&bars.k_issued[ks]), kiph >> ks & 1);
+            kiph ^= 1u << ks;
             mbar_wait(smem_u32(&bars.k_full[ks]), (T / C::kNK) & 1);
             fill_store<D>(p, k_smem + ks * C::kTileBytes, &tm_kc16, &tm_kc1, region, it.N, Wg, t);
-            while (vgen[vs] != T) __nanosleep(32);
+            mbar_wait(smem_u32(&bars.v_issued[vs]), viph >> vs & 1);
+            viph ^= 1u << vs;
             mbar_wait(smem_u32(&bars.v_full[vs]), (T / C::kNV) & 1);
             fill_store<D>(p, v_smem + vs * C::kTileBytes, &tm_vc16, &tm_vc1, region, it.N, Wg, t);
             pend[np_++] = smem_u32(&bars.k_copied[ks]);
