@@ -271,6 +271,21 @@ __device__ __forceinline__ void fill_store(const PpParams &p, uint32_t tile, con
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// bits e of a 32-column word with e <= k (k < 0: none, k >= 31: all)
+__device__ __forceinline__ uint32_t bits_le(int k) {
+  return k >= 31 ? 0xffffffffu : (k < 0 ? 0u : (2u << k) - 1u);
+}
+#ifndef MOA_PP_MASK_BITS
+#define MOA_PP_MASK_BITS 1
+#endif
+#ifndef MOA_PP_LATE_SUM
+#define MOA_PP_LATE_SUM 0  // 1: row sum of the bf16 P after the p_full hand-over
+#endif
+#ifndef MOA_PP_ROLL
+#define MOA_PP_ROLL 1  // 1: rescale and epilogue loops not unrolled (code size study)
+#endif
+constexpr int kUnrollRescale = MOA_PP_ROLL ? 1 : 4, kUnrollEpi = MOA_PP_ROLL ? 1 : 2;
+
 // which q tiles use union step k (tile t); false/false = skipped by every role
 __device__ __forceinline__ void step_use(const BlockTiles &bt, int k, int &t, bool &u0, bool &u1) {
   t = bt.at(k);
@@ -468,15 +483,27 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
 #pragma unroll
       for (int c = 0; c < kN / 32; ++c) tmem_ld32_f(scol + c * 32, &x[c * 32]);
       tmem_wait_ld();
+      if ((warp & 3) == 0) PPTR(1 + j, 42)
       if (!full) {
         // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  j0+c >= lo_i)
         const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0);
         const int lo = BS >= 0 ? (int)(lo_i - j0) - 1 : dd - it.W;  // token mask: the original form
+#if MOA_PP_MASK_BITS
+        // as 32-bit visibility words (a bit test + a select per element instead of three compares)
+#pragma unroll
+        for (int w = 0; w < kN / 32; ++w) {
+          const uint32_t vis = bits_le(dd - 32 * w) & (bits_le(sk - 1 - 32 * w) | ~bits_le(lo - 32 * w));
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(vis & (1u << e))) x[32 * w + e] = -INFINITY;
+        }
+#else
 #pragma unroll
         for (int c = 0; c < kN; ++c) {
           const bool vis = c <= dd && (c < sk || c > lo);
           if (!vis) x[c] = -INFINITY;
         }
+#endif
       }
       float mx[8];
 #pragma unroll
@@ -501,7 +528,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       }
       if (__any_sync(0xffffffffu, rescale)) {
         // PV_j(prev) is complete (S_j(t) completed after it); scale this row of O_j
-#pragma unroll
+#pragma unroll kUnrollRescale
         for (int c = 0; c < D / 32; ++c) {
           float r[32];
           tmem_ld32_f(ocol + c * 32, r);
@@ -515,9 +542,9 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
       const float nm = m_used == -INFINITY ? 0.f : -m_used;
       const uint64_t nm2 = f2pk(nm, nm);
       uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+      uint32_t pk[64];  // P_j row, bf16 pairs
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
-        uint32_t pk[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
           const int c = ch * 32 + e;  // pair index: columns 2c, 2c+1
@@ -530,19 +557,28 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
             ea = fast_exp2(ya);
             eb = fast_exp2(yb);
           }
-          acc[e & 3] = fadd2(acc[e & 3], f2pk(ea, eb));
-          pk[e] = pack_bf16x2(ea, eb);
+          if (!MOA_PP_LATE_SUM) acc[e & 3] = fadd2(acc[e & 3], f2pk(ea, eb));
+          pk[c] = pack_bf16x2(ea, eb);
         }
-        tmem_st32(scol + ch * 32, pk);
+        tmem_st32(scol + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[ch * 32]));
       }
-      float s0, s1;
-      f2upk(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), s0, s1);
-      l += s0 + s1;
+      if ((warp & 3) == 0) PPTR(1 + j, 43)
       tmem_wait_st();
+      if ((warp & 3) == 0) PPTR(1 + j, 44)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&bars.p_full[j]));
       if ((warp & 3) == 0) PPTR(1 + j, 41)
+      if (MOA_PP_LATE_SUM) {
+        // row sum of the bf16 P the tensor core multiplies, after P is handed over (off the
+        // critical path of the MMA chain): a bf16 is the top half of an f32
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          acc[c & 3] = fadd2(acc[c & 3], f2pk(__uint_as_float(pk[c] << 16), __uint_as_float(pk[c] & 0xffff0000u)));
+      }
+      float s0, s1;
+      f2upk(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), s0, s1);
+      l += s0 + s1;
     }
     // epilogue: O_j / l -> bf16 rows, lse
     mbar_wait_warp(smem_u32(&bars.o_full[j]), ic & 1);
@@ -552,7 +588,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
     const bool store = MOA_PP_OSTORE && i <= ti1 && (!RAG || i < p.seq_n[it.b]);  // ragged: rows past N_b are not outputs
     __nv_bfloat16 *orow =
         static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride + (int64_t)it.h * D;
-#pragma unroll
+#pragma unroll kUnrollEpi
     for (int c = 0; c < D / 32; c += 2) {  // two TMEM loads in flight per wait
       float r[32], r2[32];
       tmem_ld32_f(ocol + c * 32, r);

@@ -1,0 +1,188 @@
+// softmax_bench.cu -- diagnostic (not part of libmoa): cycles of the prefill kernel's per-tile
+// softmax in isolation (TMEM load of a 128x128 fp32 S tile, row max, exponentials, bf16 pack,
+// row sum, TMEM store of P), one CTA per SM, 4 warps (one per sub-partition, the kernel's
+// layout: one tile's softmax at a time) or 8 warps (two tiles' softmaxes at once).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2406_14909_b200/csrc/kernels \
+//        -o tools/bin/softmax_bench tools/softmax_bench.cu -lcuda
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "ptx_sm100.cuh"
+
+using namespace moa;
+using namespace moa::ptx;
+
+__device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t y) {
+  uint32_t r;
+  asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(r) : "r"(y));
+  return r;
+}
+__device__ __forceinline__ uint32_t ex2_f16x2(uint32_t y) {
+  uint32_t r;
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(y));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+constexpr int ITERS = 256;
+
+// FLAGS: 1 max, 2 pack+store P, 4 row sum, 8 TMEM load each iteration
+template <int POLY, int FLAGS>
+__global__ void __launch_bounds__(256, 1) bench(long long *cyc, float *sink) {
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) tmem_alloc<512>(__cvta_generic_to_shared(&tbase));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (warp >= 4 ? 256u : 0u);
+  {
+    uint32_t init[32];
+    for (int c = 0; c < 4; ++c) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) init[e] = __float_as_uint(0.01f * ((threadIdx.x * 7 + c * 32 + e) % 97) - 0.3f);
+      tmem_st32(tmem + c * 32, init);
+    }
+    tmem_wait_st();
+  }
+  const uint64_t sl2 = f2pk(0.1275f, 0.1275f);
+  float m_used = 0.5f, l = 0.f;
+  uint32_t xr = 0;
+  float x[128];
+#pragma unroll
+  for (int c = 0; c < 128; ++c) x[c] = 0.001f * c;
+  __syncwarp();
+  const long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+    if (FLAGS & 8) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tmem + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
+      tmem_wait_ld();
+    } else {
+      m_used += 1e-9f;  // keeps the exponentials in the loop
+    }
+    float mt = m_used;
+    if (FLAGS & 1) {
+      float mx[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) mx[a] = fmaxf(x[a], x[a + 8]);
+#pragma unroll
+      for (int c = 16; c < 128; c += 16)
+#pragma unroll
+        for (int a = 0; a < 8; a += 2) {
+          mx[a] = fmax3(mx[a], x[c + a], x[c + a + 8]);
+          mx[a + 1] = fmax3(mx[a + 1], x[c + a + 1], x[c + a + 9]);
+        }
+      mt = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * 0.1275f;
+      if (__any_sync(0xffffffffu, mt > m_used + 8.f)) m_used = mt;
+    }
+    const uint64_t nm2 = f2pk(-m_used, -m_used);
+    uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+    for (int ch = 0; ch < 2; ++ch) {
+      uint32_t pk[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int c = ch * 32 + e;
+        const uint64_t y = ffma2(f2pk(x[2 * c], x[2 * c + 1]), sl2, nm2);
+        float ya, yb, ea, eb;
+        f2upk(y, ya, yb);
+        if (POLY < 0) {  // packed MUFU: -1 bf16x2 in and out, -2 f16x2
+          uint32_t pp = POLY == -1 ? ex2_bf16x2(pack_bf16x2(ya, yb)) : ex2_f16x2(pack_f16x2(ya, yb));
+          if (POLY == -1) {
+            ea = __uint_as_float(pp << 16);
+            eb = __uint_as_float(pp & 0xffff0000u);
+          } else {
+            __half2 h = *reinterpret_cast<__half2 *>(&pp);
+            ea = __low2float(h);
+            eb = __high2float(h);
+          }
+          if (FLAGS & 4) acc[e & 3] = fadd2(acc[e & 3], f2pk(ea, eb));
+          if (FLAGS & 2) pk[e] = POLY == -1 ? pp : pack_bf16x2(ea, eb);
+          else xr ^= pp;
+          continue;
+        }
+        if (POLY > 0 && c % (POLY > 0 ? POLY : 1) == POLY - 1) {
+          exp2_poly2(ya, yb, ea, eb);
+        } else {
+          ea = fast_exp2(ya);
+          eb = fast_exp2(yb);
+        }
+        if (FLAGS & 4) acc[e & 3] = fadd2(acc[e & 3], f2pk(ea, eb));
+        if (FLAGS & 2) pk[e] = pack_bf16x2(ea, eb);
+        else xr ^= __float_as_uint(ea) ^ __float_as_uint(eb);
+      }
+      if (FLAGS & 2) tmem_st32(tmem + ch * 32, pk);
+    }
+    if (FLAGS & 4) {
+      float s0, s1;
+      f2upk(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), s0, s1);
+      l += s0 + s1;
+    }
+    if (FLAGS & 2) {
+      tmem_wait_st();
+      if (!(FLAGS & 8)) {  // the stored P must not be dead: fold one column back
+        uint32_t r[32];
+        tmem_ld32(tmem, r);
+        tmem_wait_ld();
+        xr ^= r[0] ^ r[17];
+      }
+    }
+  }
+  const long long t1 = clock64();
+  if ((threadIdx.x & 31) == 0) cyc[blockIdx.x * 8 + warp] = t1 - t0;
+  if (l == 12345.f || xr == 0x12345u) sink[threadIdx.x] = l + (float)xr;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tbase);
+}
+
+template <int POLY, int FLAGS>
+void run(const char *name, int warps, long long *d_cyc, float *d_sink, int nsm) {
+  bench<POLY, FLAGS><<<nsm, warps * 32>>>(d_cyc, d_sink);
+  cudaDeviceSynchronize();
+  bench<POLY, FLAGS><<<nsm, warps * 32>>>(d_cyc, d_sink);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    printf("%s: %s\n", name, cudaGetErrorString(e));
+    return;
+  }
+  static long long h[148 * 8];
+  cudaMemcpy(h, d_cyc, sizeof(long long) * nsm * 8, cudaMemcpyDeviceToHost);
+  double s = 0;
+  for (int b = 0; b < nsm; ++b)
+    for (int w = 0; w < warps; ++w) s += h[b * 8 + w];
+  printf("%-34s warps %d: %7.1f cycles per 128x128 tile step\n", name, warps, s / (nsm * warps) / ITERS);
+}
+
+int main() {
+  long long *d_cyc;
+  float *d_sink;
+  cudaMalloc(&d_cyc, sizeof(long long) * 148 * 8);
+  cudaMalloc(&d_sink, 4096);
+  int nsm = 148;
+  for (int w : {4, 8}) {
+    run<-1, 15>("full, MUFU bf16x2", w, d_cyc, d_sink, nsm);
+    run<-2, 15>("full, MUFU f16x2", w, d_cyc, d_sink, nsm);
+    run<-1, 8>("ld + exp only, MUFU bf16x2", w, d_cyc, d_sink, nsm);
+    run<4, 15>("full (ld+max+exp p1/4+pack/st+sum)", w, d_cyc, d_sink, nsm);
+    run<3, 15>("full, poly 1/3", w, d_cyc, d_sink, nsm);
+    run<2, 15>("full, poly 1/2", w, d_cyc, d_sink, nsm);
+    run<0, 15>("full, no poly", w, d_cyc, d_sink, nsm);
+    run<4, 14>("no max", w, d_cyc, d_sink, nsm);
+    run<4, 13>("no pack/st", w, d_cyc, d_sink, nsm);
+    run<4, 11>("no row sum", w, d_cyc, d_sink, nsm);
+    run<4, 7>("no TMEM load", w, d_cyc, d_sink, nsm);
+    run<4, 8>("ld + exp only", w, d_cyc, d_sink, nsm);
+    run<0, 8>("ld + exp only, no poly", w, d_cyc, d_sink, nsm);
+  }
+  return 0;
+}

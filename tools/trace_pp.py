@@ -18,7 +18,7 @@ from moa_workloads import CONFIGS, prefill_qkv, rule_table  # noqa: E402
 
 TAGS = {1: "waits done, wait for turn", 2: "turn taken", 3: "dispatch done, pass turn", 4: "-",
         5: "-", 10: "mma p_full0 ok", 11: "mma p_full1 ok", 20: "mma PV0 issued", 21: "mma PV1 issued",
-        30: "mma S0 issued", 31: "mma S1 issued", 40: "sm s_full seen", 41: "sm p_full arrive"}
+        30: "mma S0 issued", 31: "mma S1 issued", 40: "sm s_full seen", 41: "sm p_full arrive", 42: "sm S loaded", 43: "sm exps issued", 44: "sm P stored"}
 
 
 def main(name="C2", nev=120):
