@@ -33,6 +33,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../moa_internal.h"
 #include "common.cuh"
@@ -316,16 +317,19 @@ constexpr int kBarTurn0 = 2;  // named barriers: kBarTurn0 + j = "warp of tile j
 
 // diagnostic build (-DMOA_PP_DIAG_TRACE, tools/trace_pp.py): (tag, clock64) events of CTA 0
 #ifdef MOA_PP_DIAG_TRACE
+#define pp_tr_arg (trn_arg_)
 __device__ unsigned long long g_pp_trace[4][4096];
 __device__ int g_pp_trace_n[4];
-#define PPTR(role, tag)                                                                          \
-  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) {                                              \
-    if (trn_ < 4096) g_pp_trace[role][trn_] = ((unsigned long long)(tag) << 56) | (unsigned long long)clock64(); \
+#define PPTR(role, tag) PPTR_CTA(0, role, tag)
+#define PPTR_CTA(cta, role, tag)                                                                 \
+  if (blockIdx.x == (cta) && (threadIdx.x & 31) == 0) {                                          \
+    if (trn_ < 4096) g_pp_trace[role][trn_] = ((unsigned long long)(tag) << 56) | ((unsigned long long)(pp_tr_arg & 0xff) << 48) | ((unsigned long long)clock64() & 0xffffffffffffull); \
     ++trn_;                                                                                      \
     g_pp_trace_n[role] = trn_ < 4096 ? trn_ : 4096;                                              \
   }
 #else
 #define PPTR(role, tag) {}
+#define PPTR_CTA(cta, role, tag) {}
 #endif
 
 template <int D, int BS, bool RAG>
@@ -343,8 +347,9 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
   uint32_t kph = 0, vph = 0, pph = 0, qph = 0, oph = 0;
   bool ostarted = false;
   bool wait_turn = j == 1;  // warp 9 (Q0) dispatches first
-  int trn_ = 0;
+  int trn_ = 0, trn_arg_ = 0;
   (void)trn_;
+  (void)trn_arg_;
   auto take_turn = [&]() {
     PPTR(j ? 3 : 0, 1)
     if (wait_turn) asm volatile("bar.sync %0, 64;" ::"r"(kBarTurn0 + j) : "memory");
@@ -454,8 +459,9 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
   const uint32_t scol = tmem + lane_off + (j ? 128u : 0u);
   const uint32_t ocol = tmem + lane_off + (j ? C::kColO1 : C::kColO0);
   const uint64_t sl2 = f2pk(p.scale_log2, p.scale_log2);
-  int trn_ = 0;
+  int trn_ = 0, trn_arg_ = 0;
   (void)trn_;
+  (void)trn_arg_;
   int sc = 0;  // S handshakes of this tile
   int ic = 0;  // items of this tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
@@ -627,8 +633,9 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
   const int bar_pair = kBarPair0 + (warp & 3);
   auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_pair) : "memory"); };
   const uint64_t sl2 = f2pk(p.scale_log2, p.scale_log2);
-  int trn_ = 0;
+  int trn_ = 0, trn_arg_ = 0;
   (void)trn_;
+  (void)trn_arg_;
   int sc[2] = {0, 0};  // S handshakes per tile
   int ic[2] = {0, 0};  // items per tile
   for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
@@ -970,7 +977,661 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ==========================================================================================
+// Clustered prefill (token mask, uniform batch; SURVEY §8(a) a4 + a5).  The two-tile kernel
+// above aliases P_j with the first columns of S_j, so S_j(t+1) cannot start before PV_j(t)
+// has read P_j(t): each tile's chain  softmax -> PV -> S -> softmax  is serial and two tiles
+// keep the tensor core ~60 % busy (profiles/).  Here a cluster of two CTAs (two SMs)
+// takes one 256-row item and each CTA owns ONE 128-row q tile, which frees TMEM for separate,
+// double-buffered S and P:
+//   TMEM (512 columns): S0 | S1 (fp32 128x128) | P0 | P1 (bf16 packed 128x128) | O (fp32 128xD)
+// so S(u+1) and PV(u-1) are computed while the softmax of S(u) runs -- the softmax warps
+// never wait for the tensor core in the steady state.  Each K/V tile
+// of the pair's union schedule is loaded ONCE for both SMs: CTA r TMA-loads rows
+// [64 r, 64 r + 64) of it multicast into both CTAs' shared memory (each full barrier expects
+// the whole tile), so L2 traffic stays that of the two-tile kernel; a slot is refilled only
+// after both CTAs' MMA warps released it (multicast tcgen05.commit, barrier count 2).
+//
+// Warps (384 threads; setmaxnreg gives the softmax warpgroups 208 registers, the rest 88):
+//   0-3  softmax of the even used steps (S0/P0) + epilogue    (thread = row = TMEM lane)
+//   4-7  softmax of the odd used steps (S1/P1)
+//   8    TMA producer: this CTA's halves of the K and V tiles (multicast)
+//   9    TMEM allocator + S = Q K^T issue
+//   10   Q tiles + fused cache fill (TMA stores from shared memory)
+//   11   O += P V issue
+// ==========================================================================================
+#ifndef MOA_CL_THREADS
+#define MOA_CL_THREADS 384
+#endif
+constexpr int kCThreads = MOA_CL_THREADS;  // warps 9-11 idle: warpgroup-aligned register reallocation
+#ifndef MOA_CL_REG_SOFTMAX
+#define MOA_CL_REG_SOFTMAX 208
+#endif
+#ifndef MOA_CL_REG_OTHER
+#define MOA_CL_REG_OTHER 88
+#endif
+// per sub-partition: two softmax warps + one other; an exact fit of the 512-register slot
+// hung setmaxnreg.inc on B200 (one softmax warp: 240 + 2 x 136), 504 works
+static_assert(2 * MOA_CL_REG_SOFTMAX + MOA_CL_REG_OTHER <= 504, "clustered prefill register split");
+constexpr int kCWarpKV = 8, kCWarpMMA = 9, kCWarpQ = 10, kCWarpPV = 11;
+constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
+
+// shared memory: kQ Q buffers (per item parity when 2), kNK K and kNV V slots of 32 KB (D=128);
+// the K ring is the deep one: a K slot is freed only when BOTH CTAs' S MMAs have read it
+#ifndef MOA_CL_Q
+#define MOA_CL_Q 1
+#endif
+#ifndef MOA_CL_NK
+#define MOA_CL_NK 4
+#endif
+template <int D>
+struct CCfg {
+  static constexpr int kQ = MOA_CL_Q;
+  static constexpr int kNK = D == 128 ? MOA_CL_NK : 4;
+  static constexpr int kNV = D == 128 ? 7 - MOA_CL_Q - MOA_CL_NK : 4;  // 224 KB + < 3 KB static
+  static_assert(kNK <= 6 && kNV <= 4 && kNV >= 2 && kQ >= 1 && kQ <= 2, "clustered prefill ring sizes");
+  static constexpr int kSmemBytes = (kQ + kNK + kNV) * PCfg<D>::kTileBytes;
+};
+
+struct CBars {
+  uint64_t q_full[2], q_empty[2];
+  uint64_t k_full[6], k_empty[6];
+  uint64_t v_full[4], v_empty[4];
+  uint64_t s_full[2], s_free[2], p_full[2], p_free[2];
+  uint64_t o_full, o_empty;
+  uint64_t ml_full[4], ml_empty[4];   // softmax group 1 -> group 0 epilogue hand-over, per warp pair
+  uint64_t k_copied[6], v_copied[4];  // fused fill: the filler CTA's stores have read a slot
+  uint64_t k_issued[6], v_issued[4];  // fused fill: this CTA's producer issued a filler tile
+  uint32_t tmem_base;
+};
+
+// CTA rank of the cluster whose q tile holds rows [128 t, 128 t + 128) of the item (the
+// fused fill of kv tile t is done by it: t is that q tile's diagonal tile)
+__device__ __forceinline__ int fill_rank(const PItem &it, int t) { return t - (int)(it.i0 / kN); }
+
+// MMA issue by two warps: warp 5 issues every S(u) = Q K(u)^T and warp 8 every PV(u) (O += P(u)
+// V(u)).  An MMA dispatch is nearly synchronous for the issuing thread and each MMA warp shares
+// its sub-partition with a busy softmax warp, so one warp doing both (waits, commits and loop
+// bookkeeping between dispatch groups) left the tensor core idle half the time; split, S(u+1)
+// waits only for its S buffer (free as soon as the softmax has S(u-1) in registers) and K(u+1),
+// and PV(u) only for P(u) and V(u).  The two streams touch disjoint TMEM (S buffers vs P
+// buffers + O), so their relative order in the tensor pipe does not matter.
+template <int D>
+__device__ __forceinline__ void cl_mma_s_role(const PpParams &p, CBars &bars, uint32_t tmem, uint32_t q_smem,
+                                              uint32_t k_smem, int total, int rank, int cid, int ncl) {
+  using C = PCfg<D>;
+  using CC = CCfg<D>;
+  constexpr uint32_t idesc_s = idesc_bf16_f32(kM, kN, false);
+  const uint64_t kdesc0 = smem_desc_sw128(k_smem, 16, 1024);
+  int T = 0, u = 0, ic = 0;  // union steps (K ring), used steps (S buffers), items of this CTA
+  int trn_ = 0, trn_arg_ = 0;
+  (void)trn_;
+  (void)trn_arg_;
+  for (int idx = cid; idx < total; idx += ncl) {
+    const PItem it = get_pitem<-1, false>(p, idx);
+    const bool mine = rank == 0 || it.bt.has1;
+    const TileRanges r = rank ? it.bt.r[1] : it.bt.r[0];
+    const int last_t = r.b1 > r.b0 ? r.b1 - 1 : r.a1 - 1;
+    const int qb = ic % CC::kQ;
+    const uint64_t adesc = smem_desc_sw128(q_smem + qb * C::kTileBytes, 16, 1024);
+    bool first_s = true;
+    const int ns = it.bt.steps();
+    for (int k = 0; k < ns; ++k) {
+      int t;
+      bool u0, u1;
+      step_use(it.bt, k, t, u0, u1);
+      if (!u0 && !u1) continue;
+      const bool use = mine && (rank ? u1 : u0);
+      const int ks = T % CC::kNK;
+      // every step's data must have landed before this CTA releases the slot (clean phases)
+      mbar_wait_warp(smem_u32(&bars.k_full[ks]), (T / CC::kNK) & 1);
+      if (use) {
+        const int b = u & 1;
+        if (u >= 2) mbar_wait_warp(smem_u32(&bars.s_free[b]), ((u >> 1) - 1) & 1);
+        if (first_s) mbar_wait_warp(smem_u32(&bars.q_full[qb]), (ic / CC::kQ) & 1);
+        first_s = false;
+        trn_arg_ = T;
+        PPTR_CTA(0, 0, 2)
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t bdesc = kdesc0 + (uint64_t)((ks * C::kTileBytes) >> 4);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * C::kSlabBytes + (kk & 3) * 32) >> 4;
+            mma_ss(tmem + kColS + 128 * b, adesc + off, bdesc + off, idesc_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(smem_u32(&bars.s_full[b]));
+          if (t == last_t) mma_commit(smem_u32(&bars.q_empty[qb]));
+          mma_commit_mc(smem_u32(&bars.k_empty[ks]), 3);
+        }
+        __syncwarp();
+        PPTR_CTA(0, 0, 30)
+        ++u;
+      } else {
+        if (elect_one()) mma_commit_mc(smem_u32(&bars.k_empty[ks]), 3);
+        __syncwarp();
+      }
+      ++T;
+    }
+    if (mine) ++ic;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void cl_mma_pv_role(const PpParams &p, CBars &bars, uint32_t tmem, uint32_t v_smem,
+                                               int total, int rank, int cid, int ncl) {
+  using C = PCfg<D>;
+  using CC = CCfg<D>;
+  constexpr uint32_t idesc_o = idesc_bf16_f32(kM, D, true);
+  const uint64_t vdesc0 = smem_desc_sw128(v_smem, C::kSlabBytes, 1024);
+  int T = 0, u = 0, ic = 0;  // union steps (V ring), used steps (P buffers), items of this CTA
+  int trn_ = 0, trn_arg_ = 0;
+  (void)trn_;
+  (void)trn_arg_;
+  for (int idx = cid; idx < total; idx += ncl) {
+    const PItem it = get_pitem<-1, false>(p, idx);
+    const bool mine = rank == 0 || it.bt.has1;
+    bool first_pv = true;
+    const int ns = it.bt.steps();
+    for (int k = 0; k < ns; ++k) {
+      int t;
+      bool u0, u1;
+      step_use(it.bt, k, t, u0, u1);
+      if (!u0 && !u1) continue;
+      const bool use = mine && (rank ? u1 : u0);
+      const int vs = T % CC::kNV;
+      mbar_wait_warp(smem_u32(&bars.v_full[vs]), (T / CC::kNV) & 1);
+      if (use) {
+        const int b = u & 1;
+        mbar_wait_warp(smem_u32(&bars.p_full[b]), (u >> 1) & 1);
+        if (first_pv && ic > 0) mbar_wait_warp(smem_u32(&bars.o_empty), (ic - 1) & 1);  // O drained
+        PPTR_CTA(0, 3, 10)
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t vdesc = vdesc0 + (uint64_t)((vs * C::kTileBytes) >> 4);
+#pragma unroll
+          for (int kk = 0; kk < kN / 16; ++kk)
+            mma_ts(tmem + kColO, tmem + kColP + 64 * b + kk * 8, vdesc + (uint64_t)((kk * 2048) >> 4), idesc_o,
+                   (first_pv && kk == 0) ? 0u : 1u);
+          mma_commit(smem_u32(&bars.p_free[b]));
+          mma_commit_mc(smem_u32(&bars.v_empty[vs]), 3);
+        }
+        __syncwarp();
+        PPTR_CTA(0, 3, 20)
+        first_pv = false;
+        ++u;
+      } else {
+        if (elect_one()) mma_commit_mc(smem_u32(&bars.v_empty[vs]), 3);
+        __syncwarp();
+      }
+      ++T;
+    }
+    if (mine) {
+      if (elect_one()) mma_commit(smem_u32(&bars.o_full));  // every PV of the item complete
+      __syncwarp();
+      ++ic;
+    }
+  }
+}
+
+// Softmax of this CTA's q tile by TWO warpgroups that take alternate used steps: group
+// g = warp >> 2 handles the steps u with u % 2 == g, i.e. always S buffer g and P buffer g
+// (thread = row = TMEM lane (warp & 3) * 32 + lane in both groups).  With S double-buffered
+// the two groups' steps overlap, so each sub-partition runs two softmax warps at once (one
+// warp alone is latency-bound).  The lazy row reference m (exponentials are taken against it;
+// it moves only when a row max exceeds it by 2^8) is passed from step u-1 to step u through
+// shared memory (m_x[u & 1][row]) and a named barrier per (warp pair, parity): the owner of
+// step u-1 publishes its reference right after its row max, so step u waits only for that,
+// not for the whole step.  Each group keeps its own partial row sum against the last
+// reference it used (rescaled when the reference moves); group 0 merges them in the epilogue.
+constexpr int kBarMx0 = 1;   // named barriers 1..8: m exchange, (warp pair, step parity)
+
+template <int D>
+__device__ __forceinline__ void cl_softmax_role(const PpParams &p, CBars &bars, uint32_t tmem, int total, int rank,
+                                                int cid, int ncl, int warp, int lane, float (*m_x)[kM],
+                                                float2 *ml_x) {
+  const int grp = warp >> 2, wq = warp & 3;
+  const int row = wq * 32 + lane;
+  const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+  const uint32_t ocol = tmem + lane_off + kColO;
+  const uint32_t scol = tmem + lane_off + kColS + 128 * grp;
+  const uint32_t pcol = tmem + lane_off + kColP + 64 * grp;
+  const uint64_t sl2 = f2pk(p.scale_log2, p.scale_log2);
+  int trn_ = 0, trn_arg_ = 0;
+  (void)trn_;
+  (void)trn_arg_;
+  int u = 0, ic = 0;  // used steps of this CTA (both groups count all of them), items
+  for (int idx = cid; idx < total; idx += ncl) {
+    const PItem it = get_pitem<-1, false>(p, idx);
+    if (rank == 1 && !it.bt.has1) continue;
+    const int64_t ti0 = it.i0 + rank * kM;
+    const int64_t ti1 = (ti0 + kM < it.N ? ti0 + kM : it.N) - 1;
+    const int64_t i = ti0 + row;
+    const TileRanges rj = rank ? it.bt.r[1] : it.bt.r[0];
+    const int nu = rj.count();  // used steps of this item
+    const int u_first = u;
+    float m_seen = -INFINITY, l = 0.f;  // this group's reference and partial row sum
+    const int ns = it.bt.steps();
+    for (int k = 0; k < ns; ++k) {
+      const int t = it.bt.at(k);
+      if (!tile_in(rj, t)) continue;
+      if ((u & 1) != grp) {
+        ++u;
+        continue;
+      }
+      const int64_t j0 = (int64_t)t * kN;
+      const bool full = kv_tile_full(ti0, ti1, t, it.W, p.n_sink);
+      mbar_wait_warp(smem_u32(&bars.s_full[grp]), (u >> 1) & 1);
+      if (wq == 0) PPTR(1 + grp, 40)
+      tc_fence_after();
+      float x[kN];
+#pragma unroll
+      for (int c = 0; c < kN / 32; ++c) tmem_ld32_f(scol + c * 32, &x[c * 32]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars.s_free[grp]));  // the tensor core may compute S(u+2)
+      if (!full) {
+        // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  c > i-j0-W)
+        const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0), lo = dd - it.W;
+#pragma unroll
+        for (int w = 0; w < kN / 32; ++w) {
+          const uint32_t vis = bits_le(dd - 32 * w) & (bits_le(sk - 1 - 32 * w) | ~bits_le(lo - 32 * w));
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (!(vis & (1u << e))) x[32 * w + e] = -INFINITY;
+        }
+      }
+      float mx[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) mx[a] = fmaxf(x[a], x[a + 8]);
+#pragma unroll
+      for (int c = 16; c < kN; c += 16)
+#pragma unroll
+        for (int a = 0; a < 8; a += 2) {
+          mx[a] = fmax3(mx[a], x[c + a], x[c + a + 8]);
+          mx[a + 1] = fmax3(mx[a + 1], x[c + a + 1], x[c + a + 9]);
+        }
+      const float rmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
+      const float mt = rmax * p.scale_log2;
+      if (wq == 0) PPTR(1 + grp, 42)
+      // the reference after step u-1 (the other group's step, or none at the item's start)
+      float m_prev = -INFINITY;
+      if (u > u_first) {
+        asm volatile("bar.sync %0, 64;" ::"r"(kBarMx0 + 2 * wq + ((u - 1) & 1)) : "memory");
+        m_prev = m_x[(u - 1) & 1][row];
+      }
+      if (wq == 0) PPTR(1 + grp, 43)
+      float m_u = m_prev;
+      bool rescale = false;
+      if (m_prev == -INFINITY) {
+        m_u = mt;  // no visible key so far: O is still exactly 0
+      } else if (mt > m_prev + kRescaleThreshold) {
+        m_u = mt;
+        rescale = true;
+      }
+      if (u + 1 < u_first + nu) {  // publish it for step u+1 (the other group)
+        m_x[u & 1][row] = m_u;
+        asm volatile("bar.arrive %0, 64;" ::"r"(kBarMx0 + 2 * wq + (u & 1)) : "memory");
+      }
+      if (__any_sync(0xffffffffu, rescale)) {
+        // O holds PV(u-1) once it completes; scale the rows whose reference moved
+        const float alpha = rescale ? fast_exp2(m_prev - m_u) : 1.f;
+        mbar_wait_warp(smem_u32(&bars.p_free[(u - 1) & 1]), ((u - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          float r[32];
+          tmem_ld32_f(ocol + c * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] *= alpha;
+          tmem_st32(ocol + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r));
+        }
+      }
+      if (m_u != m_seen) {  // this group's partial sum follows the reference
+        l = m_seen == -INFINITY ? 0.f : l * fast_exp2(m_seen - m_u);
+        m_seen = m_u;
+      }
+      const float nm = m_u == -INFINITY ? 0.f : -m_u;
+      const uint64_t nm2 = f2pk(nm, nm);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {  // pair index: columns 2c, 2c+1
+        const uint64_t y = ffma2(f2pk(x[2 * c], x[2 * c + 1]), sl2, nm2);
+        float ya, yb, ea, eb;
+        f2upk(y, ya, yb);
+        if (c % kPolyEvery == kPolyEvery - 1) {
+          exp2_poly2(ya, yb, ea, eb);
+        } else {
+          ea = fast_exp2(ya);
+          eb = fast_exp2(yb);
+        }
+        acc[c & 3] = fadd2(acc[c & 3], f2pk(ea, eb));
+        pk[c] = pack_bf16x2(ea, eb);
+      }
+      // P buffer grp is free once PV(u-2) has read it
+      if (wq == 0) PPTR(1 + grp, 44)
+      if (u >= 2) mbar_wait_warp(smem_u32(&bars.p_free[grp]), ((u >> 1) - 1) & 1);
+      if (wq == 0) PPTR(1 + grp, 45)
+      tc_fence_after();
+      tmem_st32(pcol, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      tmem_st32(pcol + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars.p_full[grp]));
+      if (wq == 0) PPTR(1 + grp, 41)
+      float s0, s1;
+      f2upk(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])), s0, s1);
+      l += s0 + s1;
+      ++u;
+    }
+    // epilogue (group 0): merge the two partial sums at the final reference, O / l -> bf16, lse
+    // hand-over slot (one per row): group 1 refills it only after group 0 has read it
+    if (grp == 1) {
+      if (ic > 0) mbar_wait_warp(smem_u32(&bars.ml_empty[wq]), (ic - 1) & 1);
+      ml_x[row] = make_float2(m_seen, l);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars.ml_full[wq]));
+      ++ic;
+      continue;
+    }
+    mbar_wait_warp(smem_u32(&bars.ml_full[wq]), ic & 1);
+    const float2 mlb = ml_x[row];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&bars.ml_empty[wq]));
+    const float mb = mlb.x, lb = mlb.y;
+    const float m_fin = fmaxf(m_seen, mb);
+    float lt = 0.f;
+    if (m_seen != -INFINITY) lt += l * fast_exp2(m_seen - m_fin);
+    if (mb != -INFINITY) lt += lb * fast_exp2(mb - m_fin);
+    mbar_wait_warp(smem_u32(&bars.o_full), ic & 1);
+    ++ic;
+    tc_fence_after();
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    const bool store = i <= ti1;
+    __nv_bfloat16 *orow =
+        static_cast<__nv_bfloat16 *>(p.o) + ((int64_t)it.b * p.N + i) * p.o_row_stride + (int64_t)it.h * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; c += 2) {
+      float r[32], r2[32];
+      tmem_ld32_f(ocol + c * 32, r);
+      tmem_ld32_f(ocol + (c + 1) * 32, r2);
+      tmem_wait_ld();
+      if (store) {
+        store_o_chunk32(orow + c * 32, r, inv, p.o_v8);
+        store_o_chunk32(orow + (c + 1) * 32, r2, inv, p.o_v8);
+      }
+    }
+    if (p.lse && store)
+      p.lse[((int64_t)it.b * p.nql + it.h) * p.N + i] = lt > 0.f ? (m_fin + __log2f(lt)) * kLn2 : -INFINITY;
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&bars.o_empty));
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kCThreads, 1)
+    prefill_cl_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kh,
+                      const __grid_constant__ CUtensorMap tm_vh, const __grid_constant__ CUtensorMap tm_kc16,
+                      const __grid_constant__ CUtensorMap tm_vc16, const __grid_constant__ CUtensorMap tm_kc1,
+                      const __grid_constant__ CUtensorMap tm_vc1, const PpParams p) {
+  using C = PCfg<D>;
+  using CC = CCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ CBars bars;
+  __shared__ float m_x[2][kM];  // softmax groups: reference exchange (step parity)
+  __shared__ float2 ml_x[kM];   // epilogue hand-over of group 1's (reference, partial sum)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t smem_base = smem_u32(smem_raw);
+  if (smem_base & 1023u) __trap();
+  const uint32_t q_smem = smem_base;                         // Q buffers (item parity)
+  const uint32_t k_smem = q_smem + CC::kQ * C::kTileBytes;   // kNK tiles
+  const uint32_t v_smem = k_smem + CC::kNK * C::kTileBytes;  // kNV tiles
+  const int total = p.n_items * p.batch;
+  const int rank = (int)cluster_ctarank(), cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t peer = (uint32_t)(rank ^ 1);
+
+  if (tid == 0) {
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(smem_u32(&bars.q_full[j]), 1);
+      mbar_init(smem_u32(&bars.q_empty[j]), 1);
+      mbar_init(smem_u32(&bars.s_full[j]), 1);
+      mbar_init(smem_u32(&bars.s_free[j]), 4);  // the 4 warps of the group owning buffer j
+      mbar_init(smem_u32(&bars.p_full[j]), 4);
+      mbar_init(smem_u32(&bars.p_free[j]), 1);
+    }
+    mbar_init(smem_u32(&bars.o_full), 1);
+    mbar_init(smem_u32(&bars.o_empty), 4);
+    for (int w = 0; w < 4; ++w) {
+      mbar_init(smem_u32(&bars.ml_full[w]), 1);
+      mbar_init(smem_u32(&bars.ml_empty[w]), 1);
+    }
+    for (int s = 0; s < CC::kNK; ++s) {
+      mbar_init(smem_u32(&bars.k_full[s]), 1);
+      mbar_init(smem_u32(&bars.k_empty[s]), 2);  // one commit from each CTA's MMA warp
+      mbar_init(smem_u32(&bars.k_copied[s]), 1);
+      mbar_init(smem_u32(&bars.k_issued[s]), 1);
+    }
+    for (int s = 0; s < CC::kNV; ++s) {
+      mbar_init(smem_u32(&bars.v_full[s]), 1);
+      mbar_init(smem_u32(&bars.v_empty[s]), 2);
+      mbar_init(smem_u32(&bars.v_copied[s]), 1);
+      mbar_init(smem_u32(&bars.v_issued[s]), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == kCWarpMMA) tmem_alloc<kTmemCols>(smem_u32(&bars.tmem_base));
+  if (warp == kCWarpKV && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_kh);
+    tma_prefetch_desc(&tm_vh);
+  }
+  tc_fence_before();
+  cluster_sync();  // both CTAs' barriers exist before any multicast or remote arrive
+  tc_fence_after();
+  const uint32_t tmem = bars.tmem_base;
+
+  if (warp < 8) {
+#ifndef MOA_CL_NOREG
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(MOA_CL_REG_SOFTMAX) : "memory");
+#endif
+    cl_softmax_role<D>(p, bars, tmem, total, rank, cid, ncl, warp, lane, m_x, ml_x);
+  } else {
+#ifndef MOA_CL_NOREG
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(MOA_CL_REG_OTHER) : "memory");
+#endif
+  if (warp == kCWarpKV) {
+    // K and V producer (one thread, two independent cursors over the union steps): this CTA's
+    // halves of each step's K and V tiles.  A V slot is freed only by PV(T - kNV), i.e. after the
+    // softmax of that step, while K runs kNK steps ahead of S; one blocking loop would hold the
+    // next K tile behind the V slot, so each cursor issues as soon as its own slot is free.
+    if (lane == 0) {
+      struct Cur {
+        int idx, k, ns, T;
+        PItem it;
+        int g, Wg;
+        bool fi;
+      };
+      auto load = [&](Cur &c) {
+        c.it = get_pitem<-1, false>(p, c.idx);
+        c.ns = c.it.bt.steps();
+        c.g = c.it.h / p.G;
+        c.fi = fill_item(p, c.it);
+        c.Wg = c.fi ? p.win_g[c.g] : 0;
+      };
+      auto settle = [&](Cur &c) {  // move to the next step some q tile uses (or past the end)
+        while (c.idx < total) {
+          for (; c.k < c.ns; ++c.k) {
+            int t;
+            bool u0, u1;
+            step_use(c.it.bt, c.k, t, u0, u1);
+            if (u0 || u1) return;
+          }
+          c.idx += ncl;
+          c.k = 0;
+          if (c.idx < total) load(c);
+        }
+      };
+      Cur kc, vc;
+      kc.idx = vc.idx = cid;
+      kc.k = vc.k = 0;
+      kc.T = vc.T = 0;
+      if (cid < total) {
+        load(kc);
+        load(vc);
+      }
+      settle(kc);
+      settle(vc);
+      uint32_t kfill = 0, vfill = 0, kcph = 0, vcph = 0;  // per slot: holds a filler tile / copied parity
+      while (kc.idx < total || vc.idx < total) {
+        bool did = false;
+        if (kc.idx < total) {
+          const int T = kc.T, ks = T % CC::kNK;
+          bool ok = T < CC::kNK || mbar_test(smem_u32(&bars.k_empty[ks]), ((T - CC::kNK) / CC::kNK) & 1);
+          // the filler CTA's stores still read the previous (filler) tile of this slot
+          if (ok && (kfill >> ks & 1)) {
+            ok = mbar_test(smem_u32(&bars.k_copied[ks]), kcph >> ks & 1);
+            if (ok) kcph ^= 1u << ks;
+          }
+          if (ok) {
+            const int t = kc.it.bt.at(kc.k);
+            const bool ft = kc.fi && fill_tile(p, kc.it.i0, kc.it.N, kc.Wg, t);  // some CTA stores it
+            kfill = (kfill & ~(1u << ks)) | ((uint32_t)ft << ks);
+            const uint32_t kbar = smem_u32(&bars.k_full[ks]);
+            mbar_expect_tx(kbar, C::kTileBytes);  // both halves
+            for (int sl = 0; sl < C::kSlabs; ++sl)
+              tma_load_4d_mc(k_smem + ks * C::kTileBytes + sl * C::kSlabBytes + rank * 64 * 128, &tm_kh, kbar, sl * 64,
+                             kc.g, t * kN + 64 * rank, kc.it.b, 3);
+            if (ft && fill_rank(kc.it, t) == rank) mbar_arrive(smem_u32(&bars.k_issued[ks]));
+            ++kc.T;
+            ++kc.k;
+            settle(kc);
+            did = true;
+          }
+        }
+        if (vc.idx < total) {
+          const int T = vc.T, vs = T % CC::kNV;
+          bool ok = T < CC::kNV || mbar_test(smem_u32(&bars.v_empty[vs]), ((T - CC::kNV) / CC::kNV) & 1);
+          if (ok && (vfill >> vs & 1)) {
+            ok = mbar_test(smem_u32(&bars.v_copied[vs]), vcph >> vs & 1);
+            if (ok) vcph ^= 1u << vs;
+          }
+          if (ok) {
+            const int t = vc.it.bt.at(vc.k);
+            const bool ft = vc.fi && fill_tile(p, vc.it.i0, vc.it.N, vc.Wg, t);
+            vfill = (vfill & ~(1u << vs)) | ((uint32_t)ft << vs);
+            const uint32_t vbar = smem_u32(&bars.v_full[vs]);
+            mbar_expect_tx(vbar, C::kTileBytes);
+            for (int sl = 0; sl < C::kSlabs; ++sl)
+              tma_load_4d_mc(v_smem + vs * C::kTileBytes + sl * C::kSlabBytes + rank * 64 * 128, &tm_vh, vbar, sl * 64,
+                             vc.g, t * kN + 64 * rank, vc.it.b, 3);
+            if (ft && fill_rank(vc.it, t) == rank) mbar_arrive(smem_u32(&bars.v_issued[vs]));
+            ++vc.T;
+            ++vc.k;
+            settle(vc);
+            did = true;
+          }
+        }
+        if (!did) __nanosleep(20);
+      }
+    }
+  } else if (warp == kCWarpQ) {
+    if (lane == 0) {
+      int ic = 0, T = 0;
+      uint32_t kiph = 0, viph = 0;
+      for (int idx = cid; idx < total; idx += ncl) {
+        const PItem it = get_pitem<-1, false>(p, idx);
+        if (rank == 0 || it.bt.has1) {
+          const int qb = ic % CC::kQ;
+          if (ic >= CC::kQ) mbar_wait(smem_u32(&bars.q_empty[qb]), (ic / CC::kQ - 1) & 1);
+          ++ic;
+          const uint32_t qbar = smem_u32(&bars.q_full[qb]);
+          mbar_expect_tx(qbar, C::kTileBytes);
+          for (int sl = 0; sl < C::kSlabs; ++sl)
+            tma_load_4d(q_smem + qb * C::kTileBytes + sl * C::kSlabBytes, &tm_q, qbar, sl * 64, it.h,
+                        (int)(it.i0 + rank * kM), it.b);
+        }
+        if (idx + ncl < total) {  // warm L2 with the next item's Q tile
+          const PItem nx = get_pitem<-1, false>(p, idx + ncl);
+          if (rank == 0 || nx.bt.has1)
+            for (int sl = 0; sl < C::kSlabs; ++sl)
+              tma_prefetch_4d(&tm_q, sl * 64, nx.h, (int)(nx.i0 + rank * kM), nx.b);
+        }
+        // fused cache fill of the tiles on this CTA's diagonal (as in the two-tile kernel; the
+        // copied-barriers are arrived in BOTH CTAs, whose producers both refill the slot)
+        const int ns = it.bt.steps();
+        const bool fi = p.fill && fill_item(p, it);
+        if (!fi) {
+          for (int k = 0; k < ns; ++k) {
+            int t;
+            bool u0, u1;
+            step_use(it.bt, k, t, u0, u1);
+            T += (u0 || u1);
+          }
+          continue;
+        }
+        const int g = it.h / p.G;
+        const int Wg = p.win_g[g];
+        const int64_t region = (int64_t)it.b * p.rows_per_seq + p.g_off[g];
+        uint32_t pend[4];
+        int np_ = 0;
+        for (int k = 0; k < ns; ++k) {
+          int t;
+          bool u0, u1;
+          step_use(it.bt, k, t, u0, u1);
+          if (!u0 && !u1) continue;
+          if (fill_tile(p, it.i0, it.N, Wg, t) && fill_rank(it, t) == rank) {
+            const int ks = T % CC::kNK, vs = T % CC::kNV;
+            mbar_wait(smem_u32(&bars.k_issued[ks]), kiph >> ks & 1);
+            kiph ^= 1u << ks;
+            mbar_wait(smem_u32(&bars.k_full[ks]), (T / CC::kNK) & 1);
+            fill_store<D>(p, k_smem + ks * C::kTileBytes, &tm_kc16, &tm_kc1, region, it.N, Wg, t);
+            mbar_wait(smem_u32(&bars.v_issued[vs]), viph >> vs & 1);
+            viph ^= 1u << vs;
+            mbar_wait(smem_u32(&bars.v_full[vs]), (T / CC::kNV) & 1);
+            fill_store<D>(p, v_smem + vs * C::kTileBytes, &tm_vc16, &tm_vc1, region, it.N, Wg, t);
+            pend[np_++] = smem_u32(&bars.k_copied[ks]);
+            pend[np_++] = smem_u32(&bars.v_copied[vs]);
+          }
+          ++T;
+        }
+        if (np_) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          for (int q = 0; q < np_; ++q) {
+            mbar_arrive(pend[q]);
+            mbar_arrive_cluster(mapa_shared(pend[q], peer));
+          }
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // cache writes complete
+    }
+  } else if (warp == kCWarpMMA) {
+    cl_mma_s_role<D>(p, bars, tmem, q_smem, k_smem, total, rank, cid, ncl);
+  } else if (warp == kCWarpPV) {
+    cl_mma_pv_role<D>(p, bars, tmem, v_smem, total, rank, cid, ncl);
+  }
+  }
+
+  __syncwarp();  // producer lanes 1-31 wait for lane 0: the cluster barrier is warp-aligned
+  tc_fence_before();
+  cluster_sync();  // no CTA leaves while its peer may still multicast into it or arrive on it
+  if (warp == kCWarpMMA) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
 int num_sms_pp() { return device_sm_count(); }
+// MOA_PP_CLUSTER=1 routes the uniform token-mask prefill to the clustered kernel (an
+// experiment: parity-green, ~15 % slower than the two-tile kernel on C2/C4)
+bool legacy_pp() {
+  const char *e = getenv("MOA_PP_CLUSTER");  // read per launch (host only): tests switch it
+  return !(e && e[0] == '1');
+}
 
 template <int D>
 int launch_pp(const PrefillArgs &a, void *stream) {
@@ -1013,6 +1674,33 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   // the token mask (bshift < 0) and the block mask are separate instantiations, so the
   // token path carries no block-mode arithmetic
   const bool rag = p.seq_n != nullptr;
+  if (!rag && p.bshift < 0 && !legacy_pp()) {
+    // uniform token mask: the clustered kernel (a pair of SMs per 256-row item)
+    alignas(64) CUtensorMap mkh, mvh;
+    if (!make_tile_map(&mkh, a.k, D, ngl, a.N, a.batch, a.kv_row_stride, kN / 2) ||
+        !make_tile_map(&mvh, a.v, D, ngl, a.N, a.batch, a.kv_row_stride, kN / 2))
+      return (int)cudaErrorInvalidValue;
+    auto ck = prefill_cl_kernel<D>;
+    cudaError_t e = cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, CCfg<D>::kSmemBytes);
+    if (e != cudaSuccess) return (int)e;
+    const int total = p.n_items * p.batch;
+    const int ncl = total < num_sms_pp() / 2 ? total : num_sms_pp() / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ncl);
+    cfg.blockDim = dim3(kCThreads);
+    cfg.dynamicSmemBytes = CCfg<D>::kSmemBytes;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, ck, mq, mkh, mvh, *mk16, *mv16, *mk1, *mv1, p);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+  }
   auto kern = p.bshift < 0    ? (rag ? prefill_pp_kernel<D, -1, true> : prefill_pp_kernel<D, -1, false>)
               : p.bshift == 6 ? (rag ? prefill_pp_kernel<D, 6, true> : prefill_pp_kernel<D, 6, false>)
                               : (rag ? prefill_pp_kernel<D, kBsRuntime, true>

@@ -35,14 +35,38 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
 constexpr int ITERS = 256;
 
 // FLAGS: 1 max, 2 pack+store P, 4 row sum, 8 TMEM load each iteration
-template <int POLY, int FLAGS>
+__device__ volatile int g_stop;
+template <int POLY, int FLAGS, int HOG = 0>
 __global__ void __launch_bounds__(256, 1) bench(long long *cyc, float *sink) {
   __shared__ uint32_t tbase;
+  __shared__ __align__(1024) uint8_t opnd[32768];  // zero A and B operands of the hog's MMAs
+  __shared__ int stop;
   const int warp = threadIdx.x / 32;
   if (warp == 0) tmem_alloc<512>(__cvta_generic_to_shared(&tbase));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (HOG) {
+    for (int i = threadIdx.x; i < 8192; i += blockDim.x) reinterpret_cast<uint32_t *>(opnd)[i] = 0;
+    if (threadIdx.x == 0) stop = 0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (warp == 4) {  // tensor-core hog on sub-partition 0: back-to-back 128x128x16 MMAs into columns 384..511
+      const uint32_t a = (uint32_t)__cvta_generic_to_shared(opnd);
+      const uint64_t ad = smem_desc_sw128(a, 16, 1024), bd = smem_desc_sw128(a + 16384, 16, 1024);
+      constexpr uint32_t id = idesc_bf16_f32(128, 128, false);
+      long long n = 0;
+      while (!*(volatile int *)&stop) {
+        if (elect_one())
+          for (int k = 0; k < 8; ++k) mma_ss(tbase + 384, ad, bd, id, 1u);
+        __syncwarp();
+        ++n;
+      }
+      if ((threadIdx.x & 31) == 0) cyc[blockIdx.x * 8 + 7] = n;
+      return;
+    }
+    if (warp > 4) return;
+  }
   const uint32_t tmem = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (warp >= 4 ? 256u : 0u);
   {
     uint32_t init[32];
@@ -139,17 +163,40 @@ __global__ void __launch_bounds__(256, 1) bench(long long *cyc, float *sink) {
   }
   const long long t1 = clock64();
   if ((threadIdx.x & 31) == 0) cyc[blockIdx.x * 8 + warp] = t1 - t0;
+  if (HOG) {
+    __syncwarp();
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // the four softmax warps are done
+    if (threadIdx.x == 0) *(volatile int *)&stop = 1;
+  }
   if (l == 12345.f || xr == 0x12345u) sink[threadIdx.x] = l + (float)xr;
+  if (HOG) {
+    // the hog warp returned early: wait for its MMAs before freeing TMEM (commit to a local barrier)
+    __shared__ uint64_t done;
+    if (threadIdx.x == 0) {
+      mbar_init(smem_u32(&done), 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (warp == 0) {
+      if (elect_one()) mma_commit(smem_u32(&done));
+      __syncwarp();
+      mbar_wait(smem_u32(&done), 0);
+      tc_fence_after();
+      tmem_dealloc<512>(tbase);
+    }
+    return;
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<512>(tbase);
 }
 
-template <int POLY, int FLAGS>
+template <int POLY, int FLAGS, int HOG = 0>
 void run(const char *name, int warps, long long *d_cyc, float *d_sink, int nsm) {
-  bench<POLY, FLAGS><<<nsm, warps * 32>>>(d_cyc, d_sink);
+  bench<POLY, FLAGS, HOG><<<nsm, HOG ? 160 : warps * 32>>>(d_cyc, d_sink);
   cudaDeviceSynchronize();
-  bench<POLY, FLAGS><<<nsm, warps * 32>>>(d_cyc, d_sink);
+  bench<POLY, FLAGS, HOG><<<nsm, HOG ? 160 : warps * 32>>>(d_cyc, d_sink);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     printf("%s: %s\n", name, cudaGetErrorString(e));
@@ -160,7 +207,17 @@ void run(const char *name, int warps, long long *d_cyc, float *d_sink, int nsm) 
   double s = 0;
   for (int b = 0; b < nsm; ++b)
     for (int w = 0; w < warps; ++w) s += h[b * 8 + w];
-  printf("%-34s warps %d: %7.1f cycles per 128x128 tile step\n", name, warps, s / (nsm * warps) / ITERS);
+  printf("%-34s warps %d: %7.1f cycles per 128x128 tile step", name, warps, s / (nsm * warps) / ITERS);
+  if (HOG) {
+    double w[4] = {0, 0, 0, 0}, m = 0;
+    for (int b = 0; b < nsm; ++b) {
+      for (int k = 0; k < 4; ++k) w[k] += h[b * 8 + k];
+      m += h[b * 8 + 7];
+    }
+    printf("  (per warp: %.0f %.0f %.0f %.0f; hog MMA groups %.0f)", w[0] / nsm / ITERS, w[1] / nsm / ITERS,
+           w[2] / nsm / ITERS, w[3] / nsm / ITERS, m / nsm);
+  }
+  printf("\n");
 }
 
 int main() {
@@ -169,6 +226,8 @@ int main() {
   cudaMalloc(&d_cyc, sizeof(long long) * 148 * 8);
   cudaMalloc(&d_sink, 4096);
   int nsm = 148;
+  run<4, 15, 1>("full + MMA hog on sub-partition 0", 4, d_cyc, d_sink, nsm);
+  run<4, 15>("full (no hog)", 4, d_cyc, d_sink, nsm);
   for (int w : {4, 8}) {
     run<-1, 15>("full, MUFU bf16x2", w, d_cyc, d_sink, nsm);
     run<-2, 15>("full, MUFU f16x2", w, d_cyc, d_sink, nsm);

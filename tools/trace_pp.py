@@ -2,6 +2,7 @@
 
     python tools/build_variant.py trace -DMOA_PP_DIAG_TRACE
     MOA_LIB=tools/bin/libmoa_trace.so python tools/trace_pp.py [C2] [n_events]
+    (MOA_PP_CLUSTER=1 MOA_TRACE_CL=1 ...: the clustered kernel -- S warp, softmax groups A/B, PV warp)
 """
 import ctypes
 import math
@@ -17,8 +18,8 @@ from paper_2406_14909_b200 import _lib  # noqa: E402
 from moa_workloads import CONFIGS, prefill_qkv, rule_table  # noqa: E402
 
 TAGS = {1: "waits done, wait for turn", 2: "turn taken", 3: "dispatch done, pass turn", 4: "-",
-        5: "-", 10: "mma p_full0 ok", 11: "mma p_full1 ok", 20: "mma PV0 issued", 21: "mma PV1 issued",
-        30: "mma S0 issued", 31: "mma S1 issued", 40: "sm s_full seen", 41: "sm p_full arrive", 42: "sm S loaded", 43: "sm exps issued", 44: "sm P stored"}
+        5: "-", 10: "mma PV waits done", 11: "mma p_full1 ok", 20: "mma PV issued", 21: "mma PV1 issued",
+        30: "mma S issued", 31: "mma S1 issued", 40: "sm s_full seen", 41: "sm p_full arrive", 42: "sm S loaded+max", 43: "sm m_prev known", 44: "sm exps done", 45: "sm P buffer free", 46: "sm s_full probe (1 ready, 2 not)", 2: "mma S waits done", 3: "mma k_full ok", 4: "mma k_full probe (1 ready, 2 not)", 50: "K slot free, load issued"}
 
 
 def main(name="C2", nev=120):
@@ -43,14 +44,16 @@ def main(name="C2", nev=120):
     for r in range(4):
         for i in range(cnt[r]):
             x = buf[r * 4096 + i]
-            ev.append((x & ((1 << 56) - 1), r, x >> 56))
+            ev.append((x & ((1 << 48) - 1), r, x >> 56, (x >> 48) & 0xff))
     ev.sort()
     t0 = ev[0][0]
     start = len(ev) // 3
     prev = ev[start][0]
-    for c, r, tag in ev[start:start + nev]:
-        who = ["MMA0", "SM0 ", "SM1 ", "MMA1"][r]
-        print(f"{c - t0:10d} (+{c - prev:5d})  {who} {TAGS.get(tag, tag)}")
+    for c, r, tag, arg in ev[start:start + nev]:
+        who = ["MMA0", "SM0 ", "SM1 ", "MMA1"][r] if r != 2 or tag < 50 else "KPRD"
+        if os.environ.get("MOA_TRACE_CL"):
+            who = ["MMAS", "SMA ", "SMB ", "MMAV"][r]
+        print(f"{c - t0:10d} (+{c - prev:5d})  {who} {TAGS.get(tag, tag)}" + (f" [{arg}]" if arg else ""))
         prev = c
 
 
