@@ -54,10 +54,20 @@ constexpr int kIThreads = 320;
 constexpr int kWTma = 8, kWMma = 9;
 constexpr int kKVStagesMax = 4;
 constexpr uint32_t kITmemCols = 512;  // buffer u: S (128 cols) | G (128 cols)
-#ifndef MOA_INF_POLY_EVERY
-#define MOA_INF_POLY_EVERY 2
+#ifndef MOA_INF_RCP4
+#define MOA_INF_RCP4 1  // +1.5 % at N = 8k (with the per-pass polynomial shares below)
 #endif
-constexpr int kPolyEvery = MOA_INF_POLY_EVERY;  // exponential pair c on the FMA pipe iff c % kPolyEvery == kPolyEvery - 1
+constexpr bool kRcpQuad = MOA_INF_RCP4;  // pass 1: one MUFU reciprocal per four keys instead of two
+// exponential pair c on the FMA pipe iff c % kPoly == kPoly - 1, per pass (pass 0 sums, pass 1
+// E); measured at N = 8k (A/B, tools/time_influence.py): one pair in 2 for both passes 0.268 of
+// the bf16 burst, 3 / 3 0.277, 6 / 8 0.286 (pass 1's reciprocal already keeps MUFU busy)
+#ifndef MOA_INF_POLY0
+#define MOA_INF_POLY0 6
+#endif
+#ifndef MOA_INF_POLY1
+#define MOA_INF_POLY1 8
+#endif
+constexpr int kPoly0 = MOA_INF_POLY0, kPoly1 = MOA_INF_POLY1;
 constexpr int kPairRound = 32;  // kv tiles between the two warps of a query block meeting
 constexpr float kRefLazy = 8.f;   // pass 0: refresh the exponent reference when the max grows by > 2^8
 constexpr float kStarLazy = 4.f;  // pass 0: move the designated key when a key beats it by > 2^4
@@ -305,7 +315,7 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
           pj *= a;
           mr = mx;
         }
-        // packed f32x2 arithmetic, four independent sums, one exponential pair in kPolyEvery
+        // packed f32x2 arithmetic, four independent sums, one exponential pair in kPoly0
         // on the FMA pipe -- except in diagonal tiles: masked keys must add exactly 0 (MUFU
         // ex2(-inf) = 0; the polynomial bottoms out at 2^-126, and on a row with one visible
         // key any nonzero rest would turn its E from 0 into noise).  mr = -inf: this half has
@@ -318,7 +328,7 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
           for (int c = 0; c < kCols; c += 2) {
             float ya, yb, ea, eb;
             f2upk(ffma2(f2pk(s[c], s[c + 1]), sl2, nm2), ya, yb);
-            if (decltype(poly)::value && (c >> 1) % kPolyEvery == kPolyEvery - 1) {
+            if (decltype(poly)::value && (c >> 1) % kPoly0 == kPoly0 - 1) {
               exp2_poly2(ya, yb, ea, eb);
             } else {
               ea = fast_exp2(ya);
@@ -398,17 +408,18 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
           acc += (c == kst || c > dd) ? 0.f : e;
         }
       } else {
-        // E = p (C1 - G l) / (l - p) on packed pairs; one exponential pair in kPolyEvery on
+        // E = p (C1 - G l) / (l - p) on packed pairs; one exponential pair in kPoly1 on
         // the FMA pipe.  A pair's two quotients share one MUFU reciprocal:
         // qa / da + qb / db = (qa db + qb da) / (da db)  (da, db in [1, l]: no overflow)
         const uint64_t sl2 = f2pk(p.sl2, p.sl2), nm2 = f2pk(-m, -m), nl2 = f2pk(-l, -l), l2 = f2pk(l, l),
                        c12 = f2pk(C1, C1), m12 = f2pk(-1.f, -1.f);
         float a[4] = {0.f, 0.f, 0.f, 0.f};
+        float pn = 0.f, pd = 1.f;  // kRcpQuad: the first pair of a quad (numerator, denominator)
 #pragma unroll
         for (int c = 0; c < kCols; c += 2) {
           float ya, yb, ea, eb;
           f2upk(ffma2(f2pk(s[c], s[c + 1]), sl2, nm2), ya, yb);
-          if ((c >> 1) % kPolyEvery == kPolyEvery - 1) {
+          if ((c >> 1) % kPoly1 == kPoly1 - 1) {
             exp2_poly2(ya, yb, ea, eb);
           } else {
             ea = fast_exp2(ya);
@@ -420,7 +431,19 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
           const uint64_t q2 = fmul2(p2, ffma2(f2pk(g[c], g[c + 1]), nl2, c12));
           float qa, qb;
           f2upk(fmul2(q2, f2pk(db, da)), qa, qb);
-          a[(c >> 1) & 3] = fmaf(qa + qb, fast_rcp(da * db), a[(c >> 1) & 3]);
+          if (kRcpQuad) {
+            // two pairs share one reciprocal: n1 / d1 + n2 / d2 = (n1 d2 + n2 d1) / (d1 d2), with
+            // d = da db in [1, l^2] per pair (l <= 2^8 N: the product of two stays far below 2^127)
+            const float nn = qa + qb, dd = da * db;
+            if ((c >> 1) & 1) {
+              a[(c >> 2) & 3] = fmaf(fmaf(pn, dd, nn * pd), fast_rcp(pd * dd), a[(c >> 2) & 3]);
+            } else {
+              pn = nn;
+              pd = dd;
+            }
+          } else {
+            a[(c >> 1) & 3] = fmaf(qa + qb, fast_rcp(da * db), a[(c >> 1) & 3]);
+          }
         }
         acc = (a[0] + a[1]) + (a[2] + a[3]);
       }
