@@ -49,9 +49,18 @@ using namespace ptx;
 
 constexpr int kIM = 128;        // q rows per tile (MMA M)
 constexpr int kIN = 128;        // keys per kv tile (MMA N)
-constexpr int kCols = 64;       // keys per elementwise warp and tile (= the paper's block)
-constexpr int kIThreads = 320;
-constexpr int kWTma = 8, kWMma = 9;
+constexpr int kCols = 64;       // keys per block (the paper's block)
+#ifndef MOA_INF_EW16
+#define MOA_INF_EW16 1
+#endif
+// elementwise warps: 4 row quarters (TMEM lanes) x kNQ column parts of each 128-key tile (kW keys
+// each); 16 warps (four per sub-partition, 32 keys each) hide the TMEM-load and MUFU latency that
+// bounded 8 warps (two per sub-partition, 64 keys each)
+constexpr int kNQ = MOA_INF_EW16 ? 4 : 2;
+constexpr int kW = kIN / kNQ;
+constexpr int kEW = 4 * kNQ;
+constexpr int kIThreads = 32 * (kEW + 2);
+constexpr int kWTma = kEW, kWMma = kEW + 1;
 constexpr int kKVStagesMax = 4;
 constexpr uint32_t kITmemCols = 512;  // buffer u: S (128 cols) | G (128 cols)
 #ifndef MOA_INF_RCP4
@@ -59,13 +68,13 @@ constexpr uint32_t kITmemCols = 512;  // buffer u: S (128 cols) | G (128 cols)
 #endif
 constexpr bool kRcpQuad = MOA_INF_RCP4;  // pass 1: one MUFU reciprocal per four keys instead of two
 // exponential pair c on the FMA pipe iff c % kPoly == kPoly - 1, per pass (pass 0 sums, pass 1
-// E); measured at N = 8k (A/B, tools/time_influence.py): one pair in 2 for both passes 0.268 of
-// the bf16 burst, 3 / 3 0.277, 6 / 8 0.286 (pass 1's reciprocal already keeps MUFU busy)
+// E); measured at N = 8k (A/B, tools/time_influence.py, 8 elementwise warps): one pair in 2 for
+// both passes 0.268 of the bf16 burst, 3 / 3 0.277, 6 / 8 0.286; 16 warps: 6 / 8 0.291, 4 / 4 0.295
 #ifndef MOA_INF_POLY0
-#define MOA_INF_POLY0 6
+#define MOA_INF_POLY0 4
 #endif
 #ifndef MOA_INF_POLY1
-#define MOA_INF_POLY1 8
+#define MOA_INF_POLY1 4
 #endif
 constexpr int kPoly0 = MOA_INF_POLY0, kPoly1 = MOA_INF_POLY1;
 constexpr int kPairRound = 32;  // kv tiles between the two warps of a query block meeting
@@ -192,14 +201,17 @@ __device__ __forceinline__ void merge_stats(float m0, float L0, float U0, float 
 template <int D>
 __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint32_t tmem, int warp, int lane,
                                             float (*pair)[2][kPairRound], float (*xs)[6][kIM]) {
-  const int hf = warp >> 2, wq = warp & 3;
+  const int cq = warp >> 2, wq = warp & 3;        // column part, row quarter
+  const int hf = cq * kW / kCols;                 // key block of the tile this warp's keys are in
+  const int cp = (cq * kW % kCols) / kW;          // part of that block
   const int row = wq * 32 + lane;
   const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
   const int r = wq >> 1;                          // query block of this warp inside the q tile
-  const int pair_bar = 1 + 2 * hf + r;            // named barrier of the two warps of a (query block, half)
-  const int half_bar = 5 + wq;                    // named barrier of the two halves of a row quarter
+  const int pair_bar = 1 + 2 * hf + r;            // named barrier of the warps of a (query block, key block)
+  constexpr int kPairThreads = 64 * (kCols / kW);
+  const int half_bar = 5 + wq;                    // named barrier of the column parts of a row quarter
   int sc = 0;
-  float s[kCols], g[kCols];
+  float s[kW], g[kW];
   for (int idx = blockIdx.x; idx < p.total; idx += gridDim.x) {
     const IItem it = get_iitem(p, idx);
     const int64_t ti0 = it.i0;
@@ -218,19 +230,20 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
       mbar_wait_warp(smem_u32(&bars.s_full[u]), (sc >> 1) & 1);
       ++sc;
       tc_fence_after();
-      const uint32_t base = tmem + 256u * u + lane_off + 64u * hf;
+      const uint32_t base = tmem + 256u * u + lane_off + (uint32_t)(kW * cq);
       if (MOA_INF_DIAG != 5) {
         if (MOA_INF_DIAG != 7) {
-          tmem_ld32(base, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-          tmem_ld32(base + 32u, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+#pragma unroll
+          for (int h = 0; h < kW / 32; ++h) tmem_ld32(base + 32u * h, *reinterpret_cast<uint32_t(*)[32]>(&s[32 * h]));
         }
         // wait between the S and G pairs: with all four 32-column loads in flight before one
         // wait the step took ~1400 cycles longer (tools/build_variant.py diag 1 vs 8: 1.57 vs
         // 0.67 ms at N = 8k with no elementwise work); two in flight cost nothing measurable
         tmem_wait_ld();
         if (MOA_INF_DIAG != 6) {
-          tmem_ld32(base + 128u, *reinterpret_cast<uint32_t(*)[32]>(&g[0]));
-          tmem_ld32(base + 160u, *reinterpret_cast<uint32_t(*)[32]>(&g[32]));
+#pragma unroll
+          for (int h = 0; h < kW / 32; ++h)
+            tmem_ld32(base + 128u + 32u * h, *reinterpret_cast<uint32_t(*)[32]>(&g[32 * h]));
         }
         tmem_wait_ld();
       }
@@ -240,12 +253,12 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
     };
     auto lane_load = [&](int t) {
       load_tile();
-      const int64_t j0 = (int64_t)t * kIN + kCols * hf;  // first key of this warp's half
-      const bool diag = j0 + kCols - 1 > wrow0;           // keys past some row of the warp
+      const int64_t j0 = (int64_t)t * kIN + kW * cq;  // first key of this warp's part
+      const bool diag = j0 + kW - 1 > wrow0;           // keys past some row of the warp
       if (diag) {  // keys past the row: never visible
         const int dd = (int)(i - j0);
 #pragma unroll
-        for (int c = 0; c < kCols; ++c)
+        for (int c = 0; c < kW; ++c)
           if (c > dd) s[c] = -INFINITY;
       }
       return diag;
@@ -255,12 +268,12 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
       if (MOA_INF_DIAG >= 3) continue;
       const bool diag = lane_load(t);
       if (MOA_INF_DIAG == 1 || MOA_INF_DIAG >= 5) continue;
-      const int64_t j0 = (int64_t)t * kIN + kCols * hf;
+      const int64_t j0 = (int64_t)t * kIN + kW * cq;
       float mq[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) mq[a] = fmaxf(s[a], s[a + 4]);
 #pragma unroll
-      for (int c = 8; c < kCols; c += 8)
+      for (int c = 8; c < kW; c += 8)
 #pragma unroll
         for (int a = 0; a < 4; ++a) mq[a] = fmax3(mq[a], s[c + a], s[c + a + 4]);
       const float mxr = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));  // raw max
@@ -270,15 +283,15 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
       // well conditioned; for random scores this happens in the row's first tile only
       const bool sw = mx > xsv + kStarLazy;
       if (__any_sync(0xffffffffu, sw)) {
-        int ks = kCols;
+        int ks = kW;
         float gst = 0.f;
 #pragma unroll
-        for (int c = kCols - 1; c >= 0; --c) {
+        for (int c = kW - 1; c >= 0; --c) {
           const bool hit = s[c] == mxr;
           ks = hit ? c : ks;
           gst = hit ? g[c] : gst;
         }
-        if (!sw) ks = kCols;
+        if (!sw) ks = kW;
         const float mn = fmaxf(mr, mx);
         if (mn > mr) {  // new reference (the first visible tile: mr = -inf, the sums are 0)
           const float a = mr == -INFINITY ? 0.f : fast_exp2(mr - mn);
@@ -294,7 +307,7 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
         float rs = 0.f, us = 0.f;
         const float nm = mr == -INFINITY ? 0.f : -mr;
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) {
+        for (int c = 0; c < kW; ++c) {
           const float e = c == ks ? 0.f : fast_exp2(fmaf(s[c], p.sl2, nm));
           rs += e;
           us = fmaf(g[c], e, us);
@@ -325,7 +338,7 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
         uint64_t r2[2] = {0ull, 0ull}, u2[2] = {0ull, 0ull};
         auto sweep = [&](auto poly) {
 #pragma unroll
-          for (int c = 0; c < kCols; c += 2) {
+          for (int c = 0; c < kW; c += 2) {
             float ya, yb, ea, eb;
             f2upk(ffma2(f2pk(s[c], s[c + 1]), sl2, nm2), ya, yb);
             if (decltype(poly)::value && (c >> 1) % kPoly0 == kPoly0 - 1) {
@@ -354,29 +367,47 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
     // designated key stays designated (first key on a tie), the other one joins the rest.  Both
     // warps evaluate the same expression on (half 0, half 1): bit-identical results.
     if (MOA_INF_DIAG != 1 && MOA_INF_DIAG < 3) {
-      xs[hf][0][row] = mr;
-      xs[hf][1][row] = pj;
-      xs[hf][2][row] = Lr;
-      xs[hf][3][row] = Ur;
-      xs[hf][4][row] = Gs;
-      xs[hf][5][row] = __int_as_float(js);
-      asm volatile("bar.sync %0, 64;" ::"r"(half_bar) : "memory");
-      const float mr0 = xs[0][0][row], mr1 = xs[1][0][row];
-      const int j0s = __float_as_int(xs[0][5][row]), j1s = __float_as_int(xs[1][5][row]);
-      const float mm = fmaxf(mr0, mr1);
-      const float w0 = mr0 == -INFINITY ? 0.f : fast_exp2(mr0 - mm), w1 = mr1 == -INFINITY ? 0.f : fast_exp2(mr1 - mm);
-      const float p0 = xs[0][1][row] * w0, p1 = xs[1][1][row] * w1;
-      const bool take0 = j1s < 0 || (j0s >= 0 && (p0 > p1 || (p0 == p1 && j0s < j1s)));
-      const float L0 = xs[0][2][row] * w0, L1 = xs[1][2][row] * w1;
-      const float U0 = xs[0][3][row] * w0, U1 = xs[1][3][row] * w1;
-      const float G0 = xs[0][4][row], G1 = xs[1][4][row];
+      xs[cq][0][row] = mr;
+      xs[cq][1][row] = pj;
+      xs[cq][2][row] = Lr;
+      xs[cq][3][row] = Ur;
+      xs[cq][4][row] = Gs;
+      xs[cq][5][row] = __int_as_float(js);
+      asm volatile("bar.sync %0, %1;" ::"r"(half_bar), "r"(32 * kNQ) : "memory");
+      float mm = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) mm = fmaxf(mm, xs[q][0][row]);
+      float pq[kNQ], wgt[kNQ];
+      int jq[kNQ];
+      int take = 0;
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) {
+        const float mq = xs[q][0][row];
+        wgt[q] = mq == -INFINITY ? 0.f : fast_exp2(mq - mm);
+        pq[q] = xs[q][1][row] * wgt[q];
+        jq[q] = __float_as_int(xs[q][5][row]);
+      }
+      // the designated key of the merged row: the largest designated weight (first key on a tie)
+#pragma unroll
+      for (int q = 1; q < kNQ; ++q)
+        if (jq[q] >= 0 && (jq[take] < 0 || pq[q] > pq[take] || (pq[q] == pq[take] && jq[q] < jq[take]))) take = q;
+      float Ls = 0.f, Us = 0.f, Lo = 0.f, Uo = 0.f;
+#pragma unroll
+      for (int q = 0; q < kNQ; ++q) {
+        Ls += xs[q][2][row] * wgt[q];
+        Us += xs[q][3][row] * wgt[q];
+        if (q != take) {
+          Lo += pq[q];
+          Uo += xs[q][4][row] * pq[q];
+        }
+      }
       mr = mm;
-      pj = take0 ? p0 : p1;
-      Gs = take0 ? G0 : G1;
-      js = take0 ? j0s : j1s;
-      Lr = (L0 + L1) + (take0 ? p1 : p0);
-      Ur = (U0 + U1) + (take0 ? G1 * p1 : G0 * p0);
-      asm volatile("bar.sync %0, 64;" ::"r"(half_bar) : "memory");  // both read before the next item's write
+      pj = pq[take];
+      Gs = xs[take][4][row];
+      js = jq[take];
+      Lr = Ls + Lo;
+      Ur = Us + Uo;
+      asm volatile("bar.sync %0, %1;" ::"r"(half_bar), "r"(32 * kNQ) : "memory");  // all read before the next item's write
     }
     const float m = mr;
     // l = sum of all p; C1 = R l; the designated key: E = pj (Ur - Gs Lr) / (l Lr) (0 for a
@@ -390,19 +421,19 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
     for (int t = 0; t <= tl; ++t) {
       if (MOA_INF_DIAG >= 3) continue;
       load_tile();
-      const int64_t j0 = (int64_t)t * kIN + kCols * hf;
-      const bool diag = j0 + kCols - 1 > wrow0;
+      const int64_t j0 = (int64_t)t * kIN + kW * cq;
+      const bool diag = j0 + kW - 1 > wrow0;
       const int jb = 2 * t + hf;  // key block
-      const int kst = js - (int)j0;  // the star's column (outside [0, 64) if not in this half)
+      const int kst = js - (int)j0;  // the star's column (outside [0, kW) if not in this part)
       float acc = 0.f;
-      const bool star_here = kst >= 0 && kst < kCols;
+      const bool star_here = kst >= 0 && kst < kW;
       if (MOA_INF_DIAG == 1 || MOA_INF_DIAG >= 5) {
         acc = s[lane] + g[lane];
       } else if (diag || __any_sync(0xffffffffu, star_here)) {
         // diagonal tiles (causal mask) and tiles holding some row's star (split off)
-        const int dd = diag ? (int)(i - j0) : kCols;
+        const int dd = diag ? (int)(i - j0) : kW;
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) {
+        for (int c = 0; c < kW; ++c) {
           const float pe = c > dd ? 0.f : fast_exp2(fmaf(s[c], p.sl2, -m));
           const float e = __fdividef(pe * fmaf(-g[c], l, C1), l - pe);
           acc += (c == kst || c > dd) ? 0.f : e;
@@ -416,7 +447,7 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
         float a[4] = {0.f, 0.f, 0.f, 0.f};
         float pn = 0.f, pd = 1.f;  // kRcpQuad: the first pair of a quad (numerator, denominator)
 #pragma unroll
-        for (int c = 0; c < kCols; c += 2) {
+        for (int c = 0; c < kW; c += 2) {
           float ya, yb, ea, eb;
           f2upk(ffma2(f2pk(s[c], s[c + 1]), sl2, nm2), ya, yb);
           if ((c >> 1) % kPoly1 == kPoly1 - 1) {
@@ -455,14 +486,17 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
       // kPairRound tiles) and meet once per round: fixed-order sum (deterministic), one store per block
       if (lane == 0) pair[warp][(t / kPairRound) & 1][t % kPairRound] = acc;
       if (t % kPairRound == kPairRound - 1 || t == tl) {
-        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-        if ((wq & 1) == 0 && rows_real > 0) {
+        asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "r"(kPairThreads) : "memory");
+        if ((wq & 1) == 0 && cp == 0 && rows_real > 0) {
           const int t0 = t - t % kPairRound;
           for (int tt = t0 + lane; tt <= t; tt += 32) {
             const int jbt = 2 * tt + hf;
             if (jbt > ib) continue;  // no causal pairs above the diagonal
             const int sl = tt % kPairRound, bu = (tt / kPairRound) & 1;
-            const float tot = pair[warp][bu][sl] + pair[warp + 1][bu][sl];
+            // the block's warps: row quarters wq, wq + 1 x the block's column parts (fixed order)
+            float tot = pair[warp][bu][sl] + pair[warp + 1][bu][sl];
+#pragma unroll
+            for (int q = 1; q < kCols / kW; ++q) tot += pair[warp + 4 * q][bu][sl] + pair[warp + 4 * q + 1][bu][sl];
             const int64_t jt = (int64_t)jbt * kCols;
             const int64_t cols_real = p.N - jt < kCols ? p.N - jt : kCols;
             const float mean = tot / (float)(rows_real * cols_real);
@@ -473,7 +507,7 @@ __device__ __forceinline__ void inf_ew_role(const IParams &p, IBars &bars, uint3
       (void)jb;
     }
     // blocks above the diagonal have no causal pairs (both halves' blocks, written by half 0)
-    if (!p.accumulate && hf == 0 && (wq & 1) == 0 && rows_real > 0)
+    if (!p.accumulate && cq == 0 && (wq & 1) == 0 && rows_real > 0)
       for (int64_t b2 = ib + 1 + lane; b2 < p.nb; b2 += 32) orow[b2] = 0.f;
   }
 }
@@ -486,8 +520,8 @@ __global__ void __launch_bounds__(kIThreads, 1)
   using C = ICfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ IBars bars;
-  __shared__ float pair[8][2][kPairRound];  // [warp][round parity][tile in round] query-block row sums
-  __shared__ float xs[2][6][kIM];           // [half][mr, pj, Lr, Ur, Gs, js][row] pass-0 statistics exchange
+  __shared__ float pair[kEW][2][kPairRound];  // [warp][round parity][tile in round] query-block row sums
+  __shared__ float xs[kNQ][6][kIM];           // [column part][mr, pj, Lr, Ur, Gs, js][row] pass-0 statistics exchange
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t smem_base = smem_u32(smem_raw);
   if (smem_base & 1023u) __trap();
@@ -499,7 +533,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
     mbar_init(smem_u32(&bars.q_empty), 1);
     for (int u = 0; u < 2; ++u) {
       mbar_init(smem_u32(&bars.s_full[u]), 1);
-      mbar_init(smem_u32(&bars.s_free[u]), 8);  // the 8 elementwise warps
+      mbar_init(smem_u32(&bars.s_free[u]), kEW);  // the elementwise warps
     }
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(smem_u32(&bars.kv_full[s]), 1);
@@ -519,7 +553,7 @@ __global__ void __launch_bounds__(kIThreads, 1)
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
 
-  if (warp < 8) {
+  if (warp < kEW) {
     inf_ew_role<D>(p, bars, tmem, warp, lane, pair, xs);
   } else if (warp == kWTma) {
     if (lane == 0) {
