@@ -183,6 +183,7 @@ moa_status moa_create(moa_ctx **out, int device, moa_dtype dtype, int num_layers
   if (kv_group_begin < 0 || kv_group_end > num_kv_heads || kv_group_begin >= kv_group_end)
     return fail(MOA_ERR_SHAPE, "kv-group shard [%d, %d) invalid for %d groups", kv_group_begin,
                 kv_group_end, num_kv_heads);
+  int sms = 148;  // planning-only contexts (device -1) plan for a B200
   if (device >= 0) {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
@@ -194,10 +195,12 @@ moa_status moa_create(moa_ctx **out, int device, moa_dtype dtype, int num_layers
     if (prop.major != 10 || prop.minor != 0)
       return fail(MOA_ERR_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)",
                   device, prop.major, prop.minor);
+    sms = prop.multiProcessorCount;
   }
   moa_ctx *c = new (std::nothrow) moa_ctx();
   if (!c) return fail(MOA_ERR_OOM, "host allocation failed");
   c->device = device;
+  c->num_sms = sms;
   c->dtype = dtype;
   c->L = num_layers;
   c->Hq = num_q_heads;
@@ -361,7 +364,7 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
 
   // decode work list: split every group region into chunks of ~chunk_rows rows
   int64_t total_rows = off * ctx->max_batch;
-  const int64_t target_ctas = 148 * 6;
+  const int64_t target_ctas = (int64_t)ctx->num_sms * 6;
   int64_t c = (total_rows + target_ctas - 1) / target_ctas;
   c = ((c + 63) / 64) * 64;
   c = std::max<int64_t>(64, std::min<int64_t>(c, 4096));

@@ -191,6 +191,7 @@ struct LayerPlan {
 
 struct moa_ctx {
   int device = -1;
+  int num_sms = 148;  // SM count of `device` (planning-only contexts: a B200's)
   moa_dtype dtype = MOA_BF16;
   int L = 0, Hq = 0, Hkv = 0, G = 1, d = 128, max_batch = 1;
   int g0 = 0, g1 = 0, ngl = 0, nql = 0;  // local groups [g0, g1), counts
