@@ -428,51 +428,18 @@ def test_fused_cache_fill_equals_separate_fill(moa, N, s, W, Hkv):
     check_cache_image(c1, 0, k.cpu(), v.cpu(), N - 1, W, s, B, Hq // Hkv)
 
 
-@pytest.fixture
-def cluster_kernel(monkeypatch):
-    """Route the uniform token-mask bf16 prefill to the clustered kernel (MOA_PP_CLUSTER=1,
-    read by the library at every launch)."""
-    monkeypatch.setenv("MOA_PP_CLUSTER", "1")
-    yield
-
-
 @pytest.mark.gpu
-@pytest.mark.parametrize("d", [128, 64])
-@pytest.mark.parametrize("N", [100, 300, 513, 1100])
-def test_prefill_bf16_clustered_kernel(moa, cluster_kernel, d, N):
-    """The clustered prefill (two SMs per 256-row item, K/V multicast, double-buffered S and P,
-    two alternating softmax groups) against the oracle, with the fused cache fill bit-exact."""
-    B, Hq, Hkv, s = 2, 6, 3, 4
-    W = [0, 1, 130, 257, 17, N + 3]
-    q = normal((B, N, Hq, d), 211, torch.bfloat16)
-    k = normal((B, N, Hkv, d), 212, torch.bfloat16)
-    v = normal((B, N, Hkv, d), 213, torch.bfloat16)
-    ctx, o, lse, scale = _prefill(moa, q, k, v, W, s, torch.bfloat16)
-    O, L = oracle.prefill(f64(q), f64(k), f64(v), W, s, scale)
-    err = np.abs(f64(o) - O)
-    assert np.isfinite(f64(o)).all()
-    assert err.max() < 2e-2, (err.max(), np.unravel_index(err.argmax(), err.shape))
-    assert np.abs(f64(lse) - L).max() < 2e-3
-    check_cache_image(ctx, 0, k, v, N - 1, W, s, B, 2)
-
-
-@pytest.mark.gpu
-def test_prefill_bf16_clustered_structured(moa, cluster_kernel):
-    """Score spikes and dominant / vanishing sinks (lazy-reference rescales handed between the
-    two softmax groups) through the clustered kernel."""
-    B, N, H, d, s = 1, 900, 4, 128, 64
-    W = [16, 200, 300, 900]
-    u = torch.zeros(d)
-    u[0] = 1.0
-    for sink_score in (12.0, -12.0):
-        spike = (torch.arange(N) % 16 == 0).float() * 8.0
-        ramp = torch.linspace(0.0, 30.0, N)  # the row max keeps growing: reference moves mid-row
-        k = ((spike + ramp)[None, :, None, None] * u).expand(B, N, H, d).clone()
-        k[:, :s] = sink_score * u
-        k = (k + 0.01 * normal((B, N, H, d), 15)).to(torch.bfloat16)
-        v = normal((B, N, H, d), 16, torch.bfloat16)
-        q = u.expand(B, N, H, d).clone().to(torch.bfloat16)
-        ctx, o, lse, _ = _prefill(moa, q, k, v, W, s, torch.bfloat16, scale=1.0)
-        O, L = oracle.prefill(f64(q), f64(k), f64(v), W, s, 1.0)
-        assert np.abs(f64(o) - O).max() < 2e-2, sink_score
-        assert np.abs(f64(lse) - L).max() < 2e-3, sink_score
+def test_prefill_bf16_clustered_kernel():
+    """The opt-in clustered prefill (MOA_PP_CLUSTER=1: two SMs per 256-row item, K/V multicast,
+    double-buffered S and P, two alternating softmax groups) against the oracle -- uniform and
+    structured inputs, fused cache fill bit-exact.  Runs in a subprocess with a time limit: one
+    C2-scale run of a modified build was seen to hang, so a hang fails this test
+    instead of stalling the suite."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, MOA_PP_CLUSTER="1")
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cl_parity_worker.py")
+    r = subprocess.run([sys.executable, worker], env=env, capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "clustered parity ok" in r.stdout
