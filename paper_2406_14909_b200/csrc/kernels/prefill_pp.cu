@@ -670,9 +670,11 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
           // key j0+c visible to row i  <=>  c <= i-j0  and  (c < s-j0  or  j0+c >= lo_i)
           const int dd = (int)(i - j0), sk = (int)(p.n_sink - j0), lo = (int)(lo_i - j0) - 1;
 #pragma unroll
-          for (int c = 0; c < kCols; ++c) {
-            const bool vis = c <= dd && (c < sk || c > lo);
-            if (!vis) x[c] = -INFINITY;
+          for (int w = 0; w < kCols / 32; ++w) {  // as 32-bit visibility words (see softmax_role)
+            const uint32_t vis = bits_le(dd - 32 * w) & (bits_le(sk - 1 - 32 * w) | ~bits_le(lo - 32 * w));
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (!(vis & (1u << e))) x[32 * w + e] = -INFINITY;
           }
         }
         float mx[8];
