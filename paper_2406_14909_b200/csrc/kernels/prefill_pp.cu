@@ -107,7 +107,17 @@ struct PpParams {
   const int64_t *g_off;
   const int32_t *win_g;
   const int32_t *fill_h;  // [ngl] local q-head whose last q block fills the group (-1: none)
+  // uniform batch: per-CTA schedule (CTA c runs entries [sched_off[c], sched_off[c+1]) of
+  // (h | b << 16, q_block)); null: entry idx = blockIdx.x + k * gridDim.x of the item list x batch
+  const int32_t *sched, *sched_off;
 };
+
+// the work entries of this CTA: [item_begin, item_end) in steps of item_step
+__device__ __forceinline__ int item_begin(const PpParams &p) { return p.sched ? p.sched_off[blockIdx.x] : (int)blockIdx.x; }
+__device__ __forceinline__ int item_end(const PpParams &p, int total) {
+  return p.sched ? p.sched_off[blockIdx.x + 1] : total;
+}
+__device__ __forceinline__ int item_step(const PpParams &p) { return p.sched ? 1 : (int)gridDim.x; }
 
 struct PBars {
   uint64_t q_full[2], q_empty[2];
@@ -179,6 +189,11 @@ __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
     // 32-bit index from the live (b, h): W stays cheap to re-derive (a 64-bit index or a W
     // carried in the item cost the softmax 45-100% through register spills)
     it.W = p.win_bq[it.b * p.nql + it.h];
+  } else if (p.sched) {  // greedy per-CTA schedule: explicit (h | b << 16, q-block) entries
+    const int e = p.sched[2 * idx];
+    it.b = e >> 16;
+    it.h = e & 0xffff;
+    it.i0 = (int64_t)p.sched[2 * idx + 1] * (2 * kM);
   } else {
     const int wi = idx / p.batch;
     it.b = idx - wi * p.batch;
@@ -360,7 +375,7 @@ __device__ __forceinline__ void mma_role(const PpParams &p, PBars &bars, uint32_
     PPTR(j ? 3 : 0, 3)
     asm volatile("bar.arrive %0, 64;" ::"r"(kBarTurn0 + (j ^ 1)) : "memory");
   };
-  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+  for (int idx = item_begin(p), idx_end = item_end(p, total); idx < idx_end; idx += item_step(p)) {
     const PItem it = get_pitem<BS, RAG>(p, idx);
     const bool mine = j == 0 || it.bt.has1;  // this q tile has rows in the item
     const TileRanges r = j ? it.bt.r[1] : it.bt.r[0];
@@ -464,7 +479,7 @@ __device__ __forceinline__ void softmax_role(const PpParams &p, PBars &bars, uin
   (void)trn_arg_;
   int sc = 0;  // S handshakes of this tile
   int ic = 0;  // items of this tile
-  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+  for (int idx = item_begin(p), idx_end = item_end(p, total); idx < idx_end; idx += item_step(p)) {
     const PItem it = get_pitem<BS, RAG>(p, idx);
     if (j == 1 && !it.bt.has1) continue;
     const int64_t ti0 = it.i0 + j * kM;                     // first row of this q tile
@@ -638,7 +653,7 @@ __device__ __forceinline__ void softmax_split_role(const PpParams &p, PBars &bar
   (void)trn_arg_;
   int sc[2] = {0, 0};  // S handshakes per tile
   int ic[2] = {0, 0};  // items per tile
-  for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+  for (int idx = item_begin(p), idx_end = item_end(p, total); idx < idx_end; idx += item_step(p)) {
     const PItem it = get_pitem<BS, RAG>(p, idx);
     const bool has1 = it.bt.has1;
     float m_used[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
@@ -852,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int T = 0;
       uint32_t kfill = 0, vfill = 0, kcph = 0, vcph = 0;  // per slot: holds a filler tile / copied parity
-      for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      for (int idx = item_begin(p), idx_end = item_end(p, total); idx < idx_end; idx += item_step(p)) {
         const PItem it = get_pitem<BS, RAG>(p, idx);
         const int g = it.h / p.G;
         const bool fi = fill_item(p, it);
@@ -898,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int qc[2] = {0, 0};
       int T = 0;  // K/V ring step (the producer's count)
       uint32_t kiph = 0, viph = 0;  // per slot: parity of the next issued-barrier phase
-      for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      for (int idx = item_begin(p), idx_end = item_end(p, total); idx < idx_end; idx += item_step(p)) {
         const PItem it = get_pitem<BS, RAG>(p, idx);
         for (int j = 0; j < 2; ++j) {
           if (j == 1 && !it.bt.has1) continue;
@@ -911,8 +926,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         (int)(it.i0 + j * kM), it.b);
         }
         // warm L2 with the next item's Q tiles (their loads wait for this item's last S MMAs)
-        if (idx + (int)gridDim.x < total) {
-          const PItem nx = get_pitem<BS, RAG>(p, idx + gridDim.x);
+        if (idx + item_step(p) < idx_end) {
+          const PItem nx = get_pitem<BS, RAG>(p, idx + item_step(p));
           for (int j = 0; j < (nx.bt.has1 ? 2 : 1); ++j)
             for (int sl = 0; sl < C::kSlabs; ++sl)
               tma_prefetch_4d(&tm_q, sl * 64, nx.h, (int)(nx.i0 + j * kM), nx.b);
@@ -1676,7 +1691,10 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   // the token mask (bshift < 0) and the block mask are separate instantiations, so the
   // token path carries no block-mode arithmetic
   const bool rag = p.seq_n != nullptr;
+  p.sched = rag ? nullptr : a.d_sched2;
+  p.sched_off = rag ? nullptr : a.d_sched2_off;
   if (!rag && p.bshift < 0 && !legacy_pp()) {
+    p.sched = p.sched_off = nullptr;  // the clustered kernel walks the item list per cluster
     // uniform token mask: the clustered kernel (a pair of SMs per 256-row item)
     alignas(64) CUtensorMap mkh, mvh;
     if (!make_tile_map(&mkh, a.k, D, ngl, a.N, a.batch, a.kv_row_stride, kN / 2) ||
@@ -1710,7 +1728,7 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   if (e != cudaSuccess) return (int)e;
   const int total = rag ? p.n_items : p.n_items * p.batch;
-  const int grid = total < num_sms_pp() ? total : num_sms_pp();
+  const int grid = p.sched ? a.sched2_ctas : (total < num_sms_pp() ? total : num_sms_pp());
   kern<<<grid, kThreads, C::kSmemBytes, (cudaStream_t)stream>>>(mq, mk, mv, *mk16, *mv16, *mk1, *mv1, p);
   return (int)cudaGetLastError();
 }

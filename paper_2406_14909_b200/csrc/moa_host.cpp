@@ -12,6 +12,7 @@
 #include <cstring>
 #include <new>
 #include <numeric>
+#include <queue>
 
 #include "moa_internal.h"
 
@@ -98,6 +99,7 @@ void free_tables(LayerPlan &p) {
   p.d_win_q = p.d_win_g = nullptr;
   p.d_g_off = nullptr;
   p.d_items = p.d_items2 = p.d_chunks = p.d_g_chunk = p.d_gc_off = p.d_fill_h = nullptr;
+  p.d_sched2 = p.d_sched2_off = nullptr;
   p.d_counters = nullptr;
 }
 
@@ -114,7 +116,9 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   size_t o_gch = align16(o_chunks + p.chunks.size() * 4);
   size_t o_gco = align16(o_gch + p.g_chunk.size() * 4);
   size_t o_fh = align16(o_gco + p.gc_off.size() * 4);
-  size_t o_cnt = align16(o_fh + p.fill_h.size() * 4);
+  size_t o_sch = align16(o_fh + p.fill_h.size() * 4);
+  size_t o_scho = align16(o_sch + p.sched2.size() * 4);
+  size_t o_cnt = align16(o_scho + p.sched2_off.size() * 4);
   size_t total = align16(o_cnt + (size_t)ctx->max_batch * ctx->ngl * 4);
   std::vector<unsigned char> host(total, 0);
   std::memcpy(host.data() + o_winq, p.win_q.data(), p.win_q.size() * 4);
@@ -126,6 +130,8 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   std::memcpy(host.data() + o_gch, p.g_chunk.data(), p.g_chunk.size() * 4);
   std::memcpy(host.data() + o_gco, p.gc_off.data(), p.gc_off.size() * 4);
   std::memcpy(host.data() + o_fh, p.fill_h.data(), p.fill_h.size() * 4);
+  std::memcpy(host.data() + o_sch, p.sched2.data(), p.sched2.size() * 4);
+  std::memcpy(host.data() + o_scho, p.sched2_off.data(), p.sched2_off.size() * 4);
   DeviceGuard dg(ctx->device);
   free_tables(p);
   void *d = nullptr;
@@ -148,6 +154,8 @@ moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   p.d_gc_off = reinterpret_cast<const int32_t *>(b + o_gco);
   p.d_counters = reinterpret_cast<int *>(b + o_cnt);
   p.d_fill_h = reinterpret_cast<const int32_t *>(b + o_fh);
+  p.d_sched2 = p.sched2.empty() ? nullptr : reinterpret_cast<const int32_t *>(b + o_sch);
+  p.d_sched2_off = p.sched2_off.empty() ? nullptr : reinterpret_cast<const int32_t *>(b + o_scho);
   return MOA_OK;
 }
 
@@ -357,6 +365,33 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
     return a.cnt > b.cnt;
   });
   np.items2.resize(its.size() * 2);
+  {
+    // per-CTA schedule of the (item, b) entries for a batch of max_batch: greedy list scheduling
+    // in the item order above (each entry to the least-loaded CTA; cost = MMA tiles of the item)
+    const int B = ctx->max_batch;
+    const int64_t total = (int64_t)its.size() * B;
+    const int ncta = (int)std::min<int64_t>(total, std::max(1, ctx->num_sms));
+    std::vector<std::vector<int32_t>> per(ncta);
+    using Slot = std::pair<int64_t, int>;  // (load, cta)
+    std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+    for (int c = 0; c < ncta; ++c) heap.push({0, c});
+    for (size_t i = 0; i < its.size(); ++i)
+      for (int b = 0; b < B; ++b) {
+        Slot sl = heap.top();
+        heap.pop();
+        per[sl.second].push_back(its[i].h | (b << 16));
+        per[sl.second].push_back(its[i].qt);
+        heap.push({sl.first + std::max(1, its[i].cnt), sl.second});
+      }
+    np.sched2.clear();
+    np.sched2_off.assign(ncta + 1, 0);
+    for (int c = 0; c < ncta; ++c) {
+      np.sched2_off[c] = (int32_t)(np.sched2.size() / 2);
+      np.sched2.insert(np.sched2.end(), per[c].begin(), per[c].end());
+    }
+    np.sched2_off[ncta] = (int32_t)(np.sched2.size() / 2);
+    np.sched2_batch = B;
+  }
   for (size_t i = 0; i < its.size(); ++i) {
     np.items2[2 * i] = its[i].h;
     np.items2[2 * i + 1] = its[i].qt;
@@ -649,6 +684,11 @@ static moa_status check_launch_common(const moa_ctx *ctx, int layer, int batch) 
 static bool aligned16(const void *ptr) { return ((uintptr_t)ptr & 15) == 0; }
 
 // MOA_PP_FUSED_FILL=0: moa_prefill runs the separate cache-fill kernel (A/B diagnostics)
+static bool sched2_enabled() {  // MOA_PP_SCHED=0: static round robin over the item list (A/B)
+  const char *e = std::getenv("MOA_PP_SCHED");
+  return !(e && e[0] == '0');
+}
+
 static bool fused_fill_enabled() {
   static const bool on = [] {
     const char *e = std::getenv("MOA_PP_FUSED_FILL");
@@ -688,6 +728,11 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   a.nql = ctx->nql; a.G = ctx->G; a.d = ctx->d;
   a.d_win_q = p.d_win_q; a.d_items = p.d_items; a.n_items = (int)(p.items.size() / 2);
   a.d_items2 = p.d_items2; a.n_items2 = (int)(p.items2.size() / 2);
+  // greedy per-CTA schedule: planned for max_batch (the common case); other batches round robin
+  const bool sched = p.d_sched2 && batch == p.sched2_batch && sched2_enabled();
+  a.d_sched2 = sched ? p.d_sched2 : nullptr;
+  a.d_sched2_off = sched ? p.d_sched2_off : nullptr;
+  a.sched2_ctas = sched ? (int)p.sched2_off.size() - 1 : 0;
   a.bshift = p.bshift;
   if (p.rag_batch) {
     if (batch != p.rag_batch)

@@ -143,6 +143,12 @@ struct LayerPlan {
   std::vector<int32_t> items;    // prefill work items (h_local, q_tile): heads heaviest first, q tiles of a
                                  // head consecutive (L2 sharing of its K/V), heaviest first
   std::vector<int32_t> items2;   // prefill work items of two q tiles (h_local, q_block of 2*kTile rows), same order
+  // the items2 x max_batch entries (h | b << 16, q_block) grouped by CTA: greedy list scheduling of
+  // the LPT-ordered list over the SMs (each entry to the least-loaded CTA), CTA c runs entries
+  // [sched2_off[c], sched2_off[c + 1]) -- the static round robin leaves the busiest SM 7-14 % above
+  // the mean on C2 layers, greedy ~1 %
+  std::vector<int32_t> sched2, sched2_off;
+  int sched2_batch = 0;
   std::vector<int32_t> chunks;   // decode chunks: (g_local, row_begin, row_end) triples
   std::vector<int32_t> g_chunk;  // first chunk of each group, size ngl + 1
   int chunk_rows = 0;
@@ -158,6 +164,7 @@ struct LayerPlan {
   const int64_t *d_g_off = nullptr;
   const int32_t *d_items = nullptr;
   const int32_t *d_items2 = nullptr;
+  const int32_t *d_sched2 = nullptr, *d_sched2_off = nullptr;
   const int32_t *d_chunks = nullptr;
   const int32_t *d_g_chunk = nullptr;
   const int32_t *d_fill_h = nullptr;  // [ngl] local q-head of the group whose last q block fills the cache
@@ -231,6 +238,8 @@ struct PrefillArgs {
   int n_items;
   const int32_t *d_items2;  // (h_local, q_block) pairs of the two-tile kernel
   int n_items2;
+  const int32_t *d_sched2, *d_sched2_off;  // per-CTA schedule of (h | b << 16, q_block) (null: round robin)
+  int sched2_ctas;
   int bshift;               // -1 token mask, else log2(block size) (block mode)
   const int64_t *d_seq_n;   // ragged: per-sequence N_b [batch] (null: every sequence has N)
   const int32_t *d_win_bq;  // ragged: per-sequence windows [batch, nql] (null: d_win_q)
