@@ -105,6 +105,34 @@ void free_tables(LayerPlan &p) {
 
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// schedule cost of a two-tile item (MOA_PP_SCHED_COST, tuning): 0 = MMA tiles of both q tiles,
+// 1 = union steps (the two tiles ping-pong, a step costs about the same either way; default:
+// C4 40 layers +0.5-1.7 % over 0, C2 within noise), 2 = MMA tiles + half a tile per EDGE tile
+int sched_cost_mode() {
+  static const int m = [] {
+    const char *e = std::getenv("MOA_PP_SCHED_COST");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+int sched_cost(const moa::BlockTiles &bt, int64_t i0, int64_t N, int W, int s, int bshift) {
+  const int mma = bt.r[0].count() + (bt.has1 ? bt.r[1].count() : 0);
+  const int mode = sched_cost_mode();
+  if (mode == 1) return 2 * bt.steps();
+  if (mode == 2) {
+    int edge = 0;
+    for (int j = 0; j < (bt.has1 ? 2 : 1); ++j) {
+      const int64_t t0 = i0 + j * moa::kTile, t1 = std::min<int64_t>(N, t0 + moa::kTile) - 1;
+      const moa::TileRanges &r = bt.r[j];
+      for (int k = 0; k < r.count(); ++k) edge += !moa::kv_tile_full(t0, t1, r.at(k), W, s, bshift);
+    }
+    return 2 * mma + edge;
+  }
+  return mma;
+}
+
+
+
 moa_status upload_tables(moa_ctx *ctx, LayerPlan &p) {
   if (ctx->device < 0) return MOA_OK;
   size_t o_winq = 0;
@@ -317,7 +345,7 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
   // first (so the kernel tail holds light work), and the q tiles of one head consecutively,
   // heaviest first: CTAs running concurrently then share their heads' K/V tiles in L2.
   const int nqt = (int)((N + moa::kTile - 1) / moa::kTile);
-  struct It { int h, qt, cnt; int64_t hcost; };
+  struct It { int h, qt, cnt; int64_t hcost; int sc = 0; };
   std::vector<It> its;
   its.reserve((size_t)ctx->nql * nqt);
   for (int h = 0; h < ctx->nql; ++h) {
@@ -356,6 +384,7 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
       const int c = bt.r[0].count() + (bt.has1 ? bt.r[1].count() : 0);
       hc += c;
       its.push_back({h, qb, c, 0});
+      its.back().sc = sched_cost(bt, (int64_t)qb * 2 * moa::kTile, N, np.win_q[h], n_sink, bshift);
     }
     for (size_t k = first; k < its.size(); ++k) its[k].hcost = hc;
   }
@@ -381,7 +410,7 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
         heap.pop();
         per[sl.second].push_back(its[i].h | (b << 16));
         per[sl.second].push_back(its[i].qt);
-        heap.push({sl.first + std::max(1, its[i].cnt), sl.second});
+        heap.push({sl.first + std::max(1, its[i].sc), sl.second});
       }
     np.sched2.clear();
     np.sched2_off.assign(ncta + 1, 0);

@@ -8,6 +8,7 @@ for r in $(seq 1 $REPS); do
     if [ "$v" = main ]; then lib=paper_2406_14909_b200/libmoa.so;
     elif [ "$v" = cluster ]; then lib=paper_2406_14909_b200/libmoa.so; env="MOA_PP_CLUSTER=1";
     elif [ "$v" = nosched ]; then lib=paper_2406_14909_b200/libmoa.so; env="MOA_PP_SCHED=0";
+    elif [ "${v#cost}" != "$v" ]; then lib=paper_2406_14909_b200/libmoa.so; env="MOA_PP_SCHED_COST=${v#cost}";
     else lib=tools/bin/libmoa_$v.so; fi
     echo -n "$v: "; env $env MOA_LIB=$lib timeout 300 python tools/time_prefill.py $ARGS 2>&1 | tail -1
   done
