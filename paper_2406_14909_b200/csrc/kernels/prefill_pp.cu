@@ -181,11 +181,12 @@ __device__ __forceinline__ void store_o_chunk32(__nv_bfloat16 *dst, const float 
 template <int BS, bool RAG>
 __device__ __forceinline__ PItem get_pitem(const PpParams &p, int idx) {
   PItem it;
-  if (RAG) {  // ragged list: (h | b << 16, q-block) of real items only, LPT order
-    const int e = p.items[2 * idx];
+  if (RAG) {  // ragged list: (h | b << 16, q-block) of real items only, LPT order (or per-CTA schedule)
+    const int32_t *src = p.sched ? p.sched : p.items;
+    const int e = src[2 * idx];
     it.b = e >> 16;
     it.h = e & 0xffff;
-    it.i0 = (int64_t)p.items[2 * idx + 1] * (2 * kM);
+    it.i0 = (int64_t)src[2 * idx + 1] * (2 * kM);
     // 32-bit index from the live (b, h): W stays cheap to re-derive (a 64-bit index or a W
     // carried in the item cost the softmax 45-100% through register spills)
     it.W = p.win_bq[it.b * p.nql + it.h];
@@ -1691,8 +1692,8 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   // the token mask (bshift < 0) and the block mask are separate instantiations, so the
   // token path carries no block-mode arithmetic
   const bool rag = p.seq_n != nullptr;
-  p.sched = rag ? nullptr : a.d_sched2;
-  p.sched_off = rag ? nullptr : a.d_sched2_off;
+  p.sched = a.d_sched2;  // uniform or ragged per-CTA schedule (null: round robin)
+  p.sched_off = a.d_sched2_off;
   if (!rag && p.bshift < 0 && !legacy_pp()) {
     p.sched = p.sched_off = nullptr;  // the clustered kernel walks the item list per cluster
     // uniform token mask: the clustered kernel (a pair of SMs per 256-row item)

@@ -90,6 +90,8 @@ void free_ragged(LayerPlan &p) {
   p.rag_win.clear();
   p.rag_items2.clear();
   p.d_rag_items2 = nullptr;
+  p.d_rag_sched2 = p.d_rag_sched2_off = nullptr;
+  p.rag_sched2_ctas = 0;
 }
 
 void free_tables(LayerPlan &p) {
@@ -104,6 +106,32 @@ void free_tables(LayerPlan &p) {
 }
 
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// greedy list scheduling of work entries (pairs, in priority order) onto ncta CTAs: each entry
+// to the least-loaded CTA; out = the entries grouped by CTA, off[c] = first entry of CTA c
+void greedy_schedule(const std::vector<int32_t> &entries, const std::vector<int> &cost, int ncta,
+                     std::vector<int32_t> &out, std::vector<int32_t> &off) {
+  std::vector<std::vector<int32_t>> per(ncta);
+  using Slot = std::pair<int64_t, int>;  // (load, cta)
+  std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
+  for (int c = 0; c < ncta; ++c) heap.push({0, c});
+  for (size_t i = 0; i < cost.size(); ++i) {
+    Slot sl = heap.top();
+    heap.pop();
+    per[sl.second].push_back(entries[2 * i]);
+    per[sl.second].push_back(entries[2 * i + 1]);
+    heap.push({sl.first + std::max(1, cost[i]), sl.second});
+  }
+  out.clear();
+  off.assign(ncta + 1, 0);
+  for (int c = 0; c < ncta; ++c) {
+    off[c] = (int32_t)(out.size() / 2);
+    out.insert(out.end(), per[c].begin(), per[c].end());
+  }
+  off[ncta] = (int32_t)(out.size() / 2);
+}
+
+
 
 // schedule cost of a two-tile item (MOA_PP_SCHED_COST, tuning): 0 = MMA tiles of both q tiles,
 // 1 = union steps (the two tiles ping-pong, a step costs about the same either way; default:
@@ -396,29 +424,20 @@ moa_status moa_set_spans_blocked(moa_ctx *ctx, int layer, const int32_t *window_
   np.items2.resize(its.size() * 2);
   {
     // per-CTA schedule of the (item, b) entries for a batch of max_batch: greedy list scheduling
-    // in the item order above (each entry to the least-loaded CTA; cost = MMA tiles of the item)
+    // in the item order above (cost: sched_cost)
     const int B = ctx->max_batch;
-    const int64_t total = (int64_t)its.size() * B;
-    const int ncta = (int)std::min<int64_t>(total, std::max(1, ctx->num_sms));
-    std::vector<std::vector<int32_t>> per(ncta);
-    using Slot = std::pair<int64_t, int>;  // (load, cta)
-    std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> heap;
-    for (int c = 0; c < ncta; ++c) heap.push({0, c});
+    std::vector<int32_t> ent;
+    std::vector<int> cost;
+    ent.reserve(its.size() * B * 2);
+    cost.reserve(its.size() * B);
     for (size_t i = 0; i < its.size(); ++i)
       for (int b = 0; b < B; ++b) {
-        Slot sl = heap.top();
-        heap.pop();
-        per[sl.second].push_back(its[i].h | (b << 16));
-        per[sl.second].push_back(its[i].qt);
-        heap.push({sl.first + std::max(1, its[i].sc), sl.second});
+        ent.push_back(its[i].h | (b << 16));
+        ent.push_back(its[i].qt);
+        cost.push_back(its[i].sc);
       }
-    np.sched2.clear();
-    np.sched2_off.assign(ncta + 1, 0);
-    for (int c = 0; c < ncta; ++c) {
-      np.sched2_off[c] = (int32_t)(np.sched2.size() / 2);
-      np.sched2.insert(np.sched2.end(), per[c].begin(), per[c].end());
-    }
-    np.sched2_off[ncta] = (int32_t)(np.sched2.size() / 2);
+    const int ncta = (int)std::min<size_t>(cost.size(), (size_t)std::max(1, ctx->num_sms));
+    greedy_schedule(ent, cost, ncta, np.sched2, np.sched2_off);
     np.sched2_batch = B;
   }
   for (size_t i = 0; i < its.size(); ++i) {
@@ -526,7 +545,7 @@ moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq
   // padded N, so a block costs what it costs there), in the uniform order of moa_set_spans:
   // heads by total kv-tile count over the batch, heaviest first; inside a head the items
   // heaviest first, q block then sequence (a uniform batch gives exactly the uniform list)
-  struct It { int b, h, qb, cnt; int64_t hcost; };
+  struct It { int b, h, qb, cnt; int64_t hcost; int sc = 0; };
   std::vector<It> its;
   for (int h = 0; h < ctx->nql; ++h) {
     const size_t first = its.size();
@@ -540,6 +559,8 @@ moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq
         const int c = bt.r[0].count() + (bt.has1 ? bt.r[1].count() : 0);
         hc += c;
         its.push_back({b, h, qb, c, 0});
+        its.back().sc = sched_cost(bt, (int64_t)qb * 2 * moa::kTile, p.N, rw[(size_t)b * ctx->nql + h], p.n_sink,
+                                   p.bshift);
       }
     }
     for (size_t k = first; k < its.size(); ++k) its[k].hcost = hc;
@@ -552,20 +573,29 @@ moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq
     return x.b < y.b;
   });
   std::vector<int32_t> ri(its.size() * 2);
+  std::vector<int> rcost(its.size());
   for (size_t i = 0; i < its.size(); ++i) {
     ri[2 * i] = its[i].h | (its[i].b << 16);
     ri[2 * i + 1] = its[i].qb;
+    rcost[i] = its[i].sc;
   }
+  // per-CTA greedy schedule of the ragged items (their costs vary with every sequence's length)
+  std::vector<int32_t> rs, rso;
+  if (!its.empty()) greedy_schedule(ri, rcost, (int)std::min<size_t>(its.size(), (size_t)std::max(1, ctx->num_sms)), rs, rso);
   DeviceGuard dg(ctx->device);
   free_ragged(p);
   if (ctx->device >= 0) {
     const size_t o_w = align16((size_t)batch * 8);
     const size_t o_i = align16(o_w + rw.size() * 4);
-    const size_t total = o_i + ri.size() * 4;
+    const size_t o_s = align16(o_i + ri.size() * 4);
+    const size_t o_so = align16(o_s + rs.size() * 4);
+    const size_t total = o_so + rso.size() * 4;
     std::vector<unsigned char> host(total, 0);
     std::memcpy(host.data(), rn.data(), rn.size() * 8);
     std::memcpy(host.data() + o_w, rw.data(), rw.size() * 4);
     std::memcpy(host.data() + o_i, ri.data(), ri.size() * 4);
+    std::memcpy(host.data() + o_s, rs.data(), rs.size() * 4);
+    std::memcpy(host.data() + o_so, rso.data(), rso.size() * 4);
     void *d = nullptr;
     cudaError_t e = cudaMalloc(&d, total);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(ragged tables)");
@@ -578,6 +608,9 @@ moa_status moa_set_ragged(moa_ctx *ctx, int layer, int batch, const int64_t *seq
     p.d_seq_n = static_cast<const int64_t *>(d);
     p.d_win_bq = reinterpret_cast<const int32_t *>(static_cast<unsigned char *>(d) + o_w);
     p.d_rag_items2 = reinterpret_cast<const int32_t *>(static_cast<unsigned char *>(d) + o_i);
+    p.d_rag_sched2 = rs.empty() ? nullptr : reinterpret_cast<const int32_t *>(static_cast<unsigned char *>(d) + o_s);
+    p.d_rag_sched2_off = rso.empty() ? nullptr : reinterpret_cast<const int32_t *>(static_cast<unsigned char *>(d) + o_so);
+    p.rag_sched2_ctas = rso.empty() ? 0 : (int)rso.size() - 1;
   }
   p.rag_items2 = std::move(ri);
   p.rag_batch = batch;
@@ -762,6 +795,12 @@ static moa_status prefill_common(moa_ctx *ctx, int layer, const void *q, const v
   a.d_sched2 = sched ? p.d_sched2 : nullptr;
   a.d_sched2_off = sched ? p.d_sched2_off : nullptr;
   a.sched2_ctas = sched ? (int)p.sched2_off.size() - 1 : 0;
+  if (p.rag_batch > 0) {  // ragged batch: its own schedule of the real items
+    const bool rs = p.d_rag_sched2 && sched2_enabled();
+    a.d_sched2 = rs ? p.d_rag_sched2 : nullptr;
+    a.d_sched2_off = rs ? p.d_rag_sched2_off : nullptr;
+    a.sched2_ctas = rs ? p.rag_sched2_ctas : 0;
+  }
   a.bshift = p.bshift;
   if (p.rag_batch) {
     if (batch != p.rag_batch)

@@ -176,6 +176,8 @@ struct LayerPlan {
   std::vector<int32_t> rag_items2;  // two-tile prefill items of the ragged batch (h | b << 16, q_block)
   void *d_rag = nullptr;
   const int32_t *d_rag_items2 = nullptr;
+  const int32_t *d_rag_sched2 = nullptr, *d_rag_sched2_off = nullptr;  // per-CTA greedy schedule of rag_items2
+  int rag_sched2_ctas = 0;
   const int64_t *d_seq_n = nullptr;
   const int32_t *d_win_bq = nullptr;
   // TMA tensor maps (CUtensorMap, 128 B) over the bound K / V cache of this layer:
