@@ -1646,7 +1646,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
 int num_sms_pp() { return device_sm_count(); }
 // MOA_PP_CLUSTER=1 routes the uniform token-mask prefill to the clustered kernel (an
 // experiment: parity-green, ~15 % slower than the two-tile kernel on C2/C4)
-bool legacy_pp() {
+bool two_tile_pp() {
   const char *e = getenv("MOA_PP_CLUSTER");  // read per launch (host only): tests switch it
   return !(e && e[0] == '1');
 }
@@ -1694,7 +1694,7 @@ int launch_pp(const PrefillArgs &a, void *stream) {
   const bool rag = p.seq_n != nullptr;
   p.sched = a.d_sched2;  // uniform or ragged per-CTA schedule (null: round robin)
   p.sched_off = a.d_sched2_off;
-  if (!rag && p.bshift < 0 && !legacy_pp()) {
+  if (!rag && p.bshift < 0 && !two_tile_pp()) {
     p.sched = p.sched_off = nullptr;  // the clustered kernel walks the item list per cluster
     // uniform token mask: the clustered kernel (a pair of SMs per 256-row item)
     alignas(64) CUtensorMap mkh, mvh;
