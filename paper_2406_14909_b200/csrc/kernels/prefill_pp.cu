@@ -51,11 +51,13 @@ constexpr int kWarpKV = 8, kWarpMMA = 9, kWarpQ = 10, kWarpMMA1 = 11, kSoftmaxWa
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // setmaxnreg split: 8 softmax warps x MOA_PP_REG_SOFTMAX + 4 other warps x MOA_PP_REG_OTHER <= 64K
+// 216 / 72 with the K 2 / V 3 ring: C2 +1.6 %, C4 +1.9 % over 208 / 88 with K 3 / V 2 (A/B after
+// the greedy schedule; before it the two measured within noise)
 #ifndef MOA_PP_REG_SOFTMAX
-#define MOA_PP_REG_SOFTMAX 208
+#define MOA_PP_REG_SOFTMAX 216
 #endif
 #ifndef MOA_PP_REG_OTHER
-#define MOA_PP_REG_OTHER 88
+#define MOA_PP_REG_OTHER 72
 #endif
 static_assert((8 * MOA_PP_REG_SOFTMAX + 4 * MOA_PP_REG_OTHER) * 32 <= 65536, "setmaxnreg split exceeds the register file");
 static_assert(MOA_PP_REG_SOFTMAX % 8 == 0 && MOA_PP_REG_OTHER % 8 == 0, "setmaxnreg counts must be multiples of 8");
@@ -78,10 +80,11 @@ struct PCfg {
   static constexpr int kTileBytes = kM * D * 2;
   static constexpr int kSlabBytes = kM * 128;
 #ifndef MOA_PP_NK128
-#define MOA_PP_NK128 3
+#define MOA_PP_NK128 2  // K ring stages at d = 128 (V gets 5 - NK); NK 4 (V 1) stalls
 #endif
   static constexpr int kNK = D == 128 ? MOA_PP_NK128 : 6;
   static constexpr int kNV = D == 128 ? 5 - MOA_PP_NK128 : 4;
+  static_assert(kNK >= 2 && kNV >= 2, "prefill K/V rings need two stages each");
   static constexpr int kSmemBytes = (2 + kNK + kNV) * kTileBytes;  // base 1024-aligned (see kernel)
   static constexpr uint32_t kColO0 = 256, kColO1 = 256 + D;
 };
