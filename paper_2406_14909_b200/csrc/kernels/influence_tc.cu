@@ -69,12 +69,13 @@ constexpr uint32_t kITmemCols = 512;  // buffer u: S (128 cols) | G (128 cols)
 constexpr bool kRcpQuad = MOA_INF_RCP4;  // pass 1: one MUFU reciprocal per four keys instead of two
 // exponential pair c on the FMA pipe iff c % kPoly == kPoly - 1, per pass (pass 0 sums, pass 1
 // E); measured at N = 8k (A/B, tools/time_influence.py, 8 elementwise warps): one pair in 2 for
-// both passes 0.268 of the bf16 burst, 3 / 3 0.277, 6 / 8 0.286; 16 warps: 6 / 8 0.291, 4 / 4 0.295
+// both passes 0.268 of the bf16 burst, 3 / 3 0.277, 6 / 8 0.286; 16 warps: 6 / 8 0.291, 4 / 4 0.295;
+// with the snake item order: 4 / 4 0.305, 4 / 6 0.307, 5 / 5 0.306, 3 / 3 0.298
 #ifndef MOA_INF_POLY0
 #define MOA_INF_POLY0 4
 #endif
 #ifndef MOA_INF_POLY1
-#define MOA_INF_POLY1 4
+#define MOA_INF_POLY1 6
 #endif
 constexpr int kPoly0 = MOA_INF_POLY0, kPoly1 = MOA_INF_POLY1;
 constexpr int kPairRound = 32;  // kv tiles between the two warps of a query block meeting
