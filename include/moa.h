@@ -444,6 +444,16 @@ moa_status moa_prefill_tiles(const moa_ctx *ctx, int layer, int q_head_local, in
  * first.  items: 2 * max_items int32. */
 moa_status moa_prefill_items(const moa_ctx *ctx, int layer, int32_t *items, int max_items,
                              int32_t *n_items);
+/* Per-CTA schedule of the uniform bf16 two-tile prefill for a batch of max_batch
+ * (moa_set_spans): the (q_head_local | b << 16, q_block of 2*MOA_TILE rows) entries
+ * of every (work item, sequence), grouped by CTA -- greedy list scheduling of the
+ * item order above, each entry to the least-loaded CTA by its kv-tile steps; CTA c
+ * runs entries [offsets[c], offsets[c + 1]).  *n_ctas and *n_entries are set; at
+ * most max_entries entries (2 int32 each) and max_ctas + 1 offsets are written
+ * (NULL buffers: counts only).  The kernel launches *n_ctas CTAs when the batch is
+ * max_batch and MOA_PP_SCHED is not 0, else it walks the item list round robin. */
+moa_status moa_prefill_schedule(const moa_ctx *ctx, int layer, int32_t *entries, int max_entries,
+                                int32_t *offsets, int max_ctas, int32_t *n_entries, int32_t *n_ctas);
 /* Decode work list: n chunks of (group_local, row_begin, row_end). */
 moa_status moa_decode_chunks(const moa_ctx *ctx, int layer, int32_t *chunks, int max_chunks,
                              int32_t *n_chunks);

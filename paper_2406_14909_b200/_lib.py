@@ -64,6 +64,8 @@ _SIGS = [
     ("moa_prefill_tiles", c_int, [_P, c_int, c_int, c_int, POINTER(c_int32), POINTER(c_uint8), c_int,
                                   POINTER(c_int32)]),
     ("moa_prefill_items", c_int, [_P, c_int, POINTER(c_int32), c_int, POINTER(c_int32)]),
+    ("moa_prefill_schedule", c_int, [_P, c_int, POINTER(c_int32), c_int, POINTER(c_int32), c_int,
+                                     POINTER(c_int32), POINTER(c_int32)]),
     ("moa_decode_chunks", c_int, [_P, c_int, POINTER(c_int32), c_int, POINTER(c_int32)]),
     ("moa_next_pos", c_int, [_P, c_int, POINTER(c_int64)]),
     ("moa_attention_influence", c_int, [_P, _P, _P, _P, c_int, c_int64, c_int, c_int, c_int, c_int64, c_int64,

@@ -1587,6 +1587,25 @@ moa_status moa_prefill_items(const moa_ctx *ctx, int layer, int32_t *items, int 
   return ok();
 }
 
+moa_status moa_prefill_schedule(const moa_ctx *ctx, int layer, int32_t *entries, int max_entries,
+                                int32_t *offsets, int max_ctas, int32_t *n_entries, int32_t *n_ctas) {
+  moa_status st = check_layer(ctx, layer, true);
+  if (st) return st;
+  if (!n_entries || !n_ctas) return fail(MOA_ERR_INVALID_ARG, "n_entries / n_ctas is NULL");
+  const LayerPlan &p = ctx->layers[layer];
+  const int ne = (int)(p.sched2.size() / 2), nc = p.sched2_off.empty() ? 0 : (int)p.sched2_off.size() - 1;
+  *n_entries = ne;
+  *n_ctas = nc;
+  if (entries)
+    for (int i = 0; i < ne && i < max_entries; ++i) {
+      entries[2 * i] = p.sched2[2 * i];
+      entries[2 * i + 1] = p.sched2[2 * i + 1];
+    }
+  if (offsets)
+    for (int c = 0; c <= nc && c <= max_ctas; ++c) offsets[c] = p.sched2_off[c];
+  return ok();
+}
+
 moa_status moa_decode_chunks(const moa_ctx *ctx, int layer, int32_t *chunks, int max_chunks,
                              int32_t *n_chunks) {
   moa_status st = check_layer(ctx, layer, true);

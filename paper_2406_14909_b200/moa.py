@@ -218,6 +218,17 @@ class MoAContext:
         check(self.lib.moa_prefill_items(self.ctx, layer, buf, n.value, byref(n)), "moa_prefill_items")
         return [(buf[2 * i], buf[2 * i + 1]) for i in range(n.value)]
 
+    def prefill_schedule(self, layer: int):
+        """Per-CTA prefill schedule: (entries [(h | b << 16, q_block)], offsets per CTA)."""
+        ne, nc = c_int32(), c_int32()
+        check(self.lib.moa_prefill_schedule(self.ctx, layer, None, 0, None, 0, byref(ne), byref(nc)),
+              "moa_prefill_schedule")
+        ent = (c_int32 * max(1, 2 * ne.value))()
+        off = (c_int32 * max(1, nc.value + 1))()
+        check(self.lib.moa_prefill_schedule(self.ctx, layer, ent, ne.value, off, nc.value, byref(ne), byref(nc)),
+              "moa_prefill_schedule")
+        return [(ent[2 * i], ent[2 * i + 1]) for i in range(ne.value)], list(off)[: nc.value + 1]
+
     def decode_chunks(self, layer: int):
         n = c_int32()
         check(self.lib.moa_decode_chunks(self.ctx, layer, None, 0, byref(n)), "moa_decode_chunks")

@@ -131,6 +131,41 @@ def test_prefill_items_head_grouped_order(moa):
         assert run == sorted(run, reverse=True)
 
 
+def _union_steps(c, h, qb, N):
+    """kv-tile steps of the two-tile item (h, q block qb): the union of both q tiles' tiles."""
+    tiles = set(c.prefill_tiles(0, h, 2 * qb)[0])
+    if (2 * qb + 1) * 128 < N:
+        tiles |= set(c.prefill_tiles(0, h, 2 * qb + 1)[0])
+    return len(tiles)
+
+
+@pytest.mark.parametrize("B", [1, 3, 8])
+def test_prefill_schedule_is_a_balanced_permutation(moa, B):
+    """The per-CTA prefill schedule (greedy list scheduling onto the SMs) holds every
+    (head, q block, sequence) exactly once, each CTA's entries in the item order, and no CTA
+    above the greedy bound: max load <= mean + the largest entry (Graham's list-scheduling
+    bound), and within 3 % of the mean on a C2 layer (the static round robin: 7-14 %)."""
+    cfg, t = CONFIGS["C2"], rule_table("C2")
+    N, s = cfg.N, cfg.n_sink
+    for layer in (0, 20, 31):
+        W = [oracle.window_of(oracle.span_of(a, b, N), s) for a, b in zip(t["alpha"][layer], t["beta"][layer])]
+        c = moa.MoAContext(1, cfg.hq, cfg.hkv, cfg.head_dim, B, device=-1)
+        c.set_spans(0, W, s, N)
+        ent, off = c.prefill_schedule(0)
+        nqb = (N + 255) // 256
+        assert sorted(ent) == sorted((h | (b << 16), qb) for h in range(cfg.hq) for qb in range(nqb)
+                                     for b in range(B))
+        ncta = len(off) - 1
+        assert ncta == min(148, cfg.hq * nqb * B) and off[0] == 0 and off[-1] == len(ent)
+        assert all(off[i] < off[i + 1] for i in range(ncta))  # every CTA has work
+        cost = {(h, qb): _union_steps(c, h, qb, N) for h in range(cfg.hq) for qb in range(nqb)}
+        loads = [sum(2 * cost[(e & 0xFFFF, q)] for e, q in ent[off[k]:off[k + 1]]) for k in range(ncta)]
+        mean = sum(loads) / ncta
+        assert max(loads) <= mean + 2 * max(cost.values()) + 1e-9
+        if B == 8:
+            assert max(loads) / mean < 1.03, (layer, max(loads) / mean)
+
+
 def test_decode_chunks_cover_each_region_once(moa):
     W = [10, 700, 3000, 1, 64, 64, 2048, 5]
     s = 64
